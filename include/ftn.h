@@ -1,0 +1,270 @@
+/*
+ * ftn.h -- the C ABI of libftn, a B200 (sm_100a) library that executes the
+ * Fortran array statements arXiv 2409.18824 ("Fully integrating the Flang
+ * Fortran compiler with standard MLIR", N. Brown) lowers from Flang's
+ * HLFIR/FIR to standard MLIR (memref / scf / affine / linalg).
+ *
+ * Citation keys: P:n = the paper line n; S:n = SPEC.md line n;
+ * R#n = reading n listed in DESIGN.md section 3 (where the paper is silent).
+ *
+ * Conventions for every call
+ *   - Plain C: no C++ or CUDA types.  A stream is a cudaStream_t passed as
+ *     ftn_stream_t (void*); NULL is the legacy default stream.
+ *   - Memory: the CALLER owns every buffer, on the device, and every
+ *     workspace; the library never frees caller memory.  Descriptors
+ *     (ftn_desc_t) live in host memory and are copied by value into kernel
+ *     parameters; the array elements they describe live in device memory.
+ *   - Validation: every argument is checked on the host before anything is
+ *     launched; on error nothing is launched and no output is touched
+ *     (no partial output).  The status tells what failed;
+ *     ftn_last_error() gives thread-local detail text.
+ *   - Asynchrony: compute calls enqueue kernels on `stream` and return; a
+ *     device fault surfaces at the caller's next synchronisation.  Scalar
+ *     results are written to DEVICE memory.
+ *   - No CPU fallback: on a device that is not sm_100 the calls return
+ *     FTN_ERR_DEVICE.
+ *   - Calls on distinct streams are thread-safe; an ftn_comm_t is used by one
+ *     thread at a time.
+ */
+#ifndef FTN_H
+#define FTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTN_MAX_RANK 3
+
+/* Element types: Fortran real(8), real(4), integer(4) (default kind, R#20),
+ * integer(8).  elem_len 8/4/4/8 bytes. */
+typedef enum { FTN_I32 = 1, FTN_I64 = 2, FTN_F32 = 3, FTN_F64 = 4 } ftn_type_t;
+
+/* One dimension of a Fortran array ("tracks the starting location of
+ * each dimension"; P:237 subviews carry "offsets, sizes and strides").
+ * sm is the signed distance in BYTES between consecutive elements of the
+ * dimension (it may be negative for a section with a negative step). */
+typedef struct {
+  int64_t lower_bound;
+  int64_t extent;
+  int64_t sm;
+} ftn_dim_t;
+
+/* A fir.box-like descriptor.  base_addr is the device address of element
+ * (lower_bound_1, ..., lower_bound_rank); element (j_1..j_r) is at
+ *   base_addr + sum_d (j_d - lower_bound_d) * dim[d].sm
+ * i.e. the origin subtraction of P:233 folded into each access.  Array
+ * element order is column-major: dim[0] varies fastest (R#1).
+ * rank 0 describes a scalar operand at base_addr (device memory). */
+typedef struct {
+  void* base_addr;
+  int64_t elem_len;
+  int32_t rank;
+  int32_t type; /* ftn_type_t */
+  ftn_dim_t dim[FTN_MAX_RANK];
+} ftn_desc_t;
+
+typedef enum {
+  FTN_OK = 0,
+  FTN_ERR_NULL = 1,        /* a required pointer is NULL */
+  FTN_ERR_RANK = 2,        /* rank outside what the call accepts */
+  FTN_ERR_TYPE = 3,        /* element type mismatch / unsupported type */
+  FTN_ERR_SHAPE = 4,       /* operands are not conformable */
+  FTN_ERR_BOUNDS = 5,      /* section outside its parent, zero step */
+  FTN_ERR_DIM = 6,         /* bad DIM argument of an inquiry */
+  FTN_ERR_ALIGN = 7,       /* an entry point that requires alignment did not get it */
+  FTN_ERR_UNSUPPORTED = 8, /* a valid Fortran form this library does not implement (MASK=, rank > 3) */
+  FTN_ERR_WORKSPACE = 9,   /* workspace NULL or smaller than *_workspace_size */
+  FTN_ERR_DEVICE = 10,     /* current device is not sm_100 */
+  FTN_ERR_CUDA = 11,       /* a CUDA launch / API error */
+  FTN_ERR_NCCL = 12        /* an NCCL error */
+} ftn_status_t;
+
+typedef void* ftn_stream_t; /* cudaStream_t */
+
+/* ---------------------------------------------------------------- a1 / a2
+ * Descriptors and inquiry (host only, pure; no device access). */
+
+/* Declaration `T :: x(lb(1):lb(1)+ext(1)-1, ...)` of a contiguous array at
+ * base (P:217 allocatables; P:233 lower bounds).  Strides are the packed
+ * column-major ones: sm_1 = elem_len, sm_{d+1} = sm_d * ext_d.  rank 0..3;
+ * ext >= 0. */
+ftn_status_t ftn_desc_contiguous(ftn_desc_t* out, void* base, int32_t type, int32_t rank,
+                                 const int64_t* lower_bounds, const int64_t* extents);
+
+/* Section `parent(lo(1):hi(1):step(1), ...)` (a subview -- same memory,
+ * new offsets/sizes/strides, no copy).  Per dimension the extent is
+ * max(0, (hi - lo + step) / step) (P:191 negative steps); the section's
+ * lower bounds are 1 (R#2); sm = step * parent sm; base = &parent(lo...).
+ * FTN_ERR_BOUNDS if a step is 0 or a selected element lies outside the parent
+ * (checked only when the extent is > 0).  *out is written only on FTN_OK. */
+ftn_status_t ftn_desc_section(ftn_desc_t* out, const ftn_desc_t* parent, const int64_t* lo,
+                              const int64_t* hi, const int64_t* step);
+
+/* LBOUND / UBOUND / SIZE / SHAPE ("SIZE corresponds directly to
+ * memref.dim").  dim is 1-based; ftn_size with dim == 0 is SIZE(x). */
+ftn_status_t ftn_lbound(const ftn_desc_t* x, int32_t dim, int64_t* out);
+ftn_status_t ftn_ubound(const ftn_desc_t* x, int32_t dim, int64_t* out);
+ftn_status_t ftn_size(const ftn_desc_t* x, int32_t dim, int64_t* out);
+ftn_status_t ftn_shape(const ftn_desc_t* x, int64_t* out /* [rank] */);
+
+/* ---------------------------------------------------------------- a3
+ * Element-wise array expressions.  Fortran assignment semantics: the whole
+ * right-hand side is evaluated before the left-hand side is defined (R#5);
+ * when dst shares memory with an operand through any mapping other than the
+ * identical one, the library evaluates into a temporary that it allocates on
+ * the stream (cudaMallocAsync) and frees after the store.  Operands must be
+ * conformable with dst (same rank and extents; lower bounds are ignored) or
+ * rank 0 (a scalar in device memory, broadcast).  All operands share dst's
+ * type. */
+
+typedef enum { FTN_ADD = 1, FTN_SUB = 2, FTN_MUL = 3, FTN_DIV = 4, FTN_MULADD = 5 } ftn_op_t;
+#define FTN_CONTRACT 1u /* MULADD as one fused multiply-add (single rounding), R#6 */
+
+/* dst = src.  rank 1..3. */
+ftn_status_t ftn_assign(const ftn_desc_t* dst, const ftn_desc_t* src, ftn_stream_t stream);
+
+/* dst = s, with s one element of dst's type read from HOST memory. */
+ftn_status_t ftn_fill(const ftn_desc_t* dst, const void* scalar_host, ftn_stream_t stream);
+
+/* dst = a op b (ADD/SUB/MUL/DIV) or dst = a*b + c (MULADD; c ignored otherwise).
+ * Reals: IEEE binary64/32 round-to-nearest-even, no contraction unless
+ * flags & FTN_CONTRACT (then MULADD is fma(a,b,c)).  Integers: modulo 2^w
+ * (R#9); DIV truncates toward zero and a zero divisor is undefined. */
+ftn_status_t ftn_elemental(int32_t op, const ftn_desc_t* dst, const ftn_desc_t* a,
+                           const ftn_desc_t* b, const ftn_desc_t* c, uint32_t flags,
+                           ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- a4
+ * Reductions to a scalar (a zero-initialised rank-0 output and a
+ * linalg.reduce over the array; MAXVAL and PRODUCT "are also implemented").
+ * x: rank 1..3, any strides.  result_dev: device pointer to one element of
+ * x's type.  ws: device workspace of at least ftn_reduce_workspace_size()
+ * bytes (8-byte aligned), not used concurrently by another call.
+ * Real SUM is combined in the documented order R, so results
+ * are deterministic, identical for a section and its packed copy, and within
+ * 4*n*2^-53*sum|x| of the exact sum (R#8).  Integer SUM wraps (exact).
+ * Empty arrays: SUM = 0, MAXVAL = -inf / most negative integer, MINVAL = +inf
+ * / most positive integer (R#10).  NaN is ignored by MAXVAL/MINVAL unless all
+ * elements are NaN (R#11). */
+ftn_status_t ftn_reduce_workspace_size(const ftn_desc_t* x, size_t* bytes);
+ftn_status_t ftn_sum(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes,
+                     ftn_stream_t stream);
+ftn_status_t ftn_maxval(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes,
+                        ftn_stream_t stream);
+ftn_status_t ftn_minval(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes,
+                        ftn_stream_t stream);
+/* DOT_PRODUCT(x, y) = SUM(x*y) for rank-1 real vectors of equal size (P:298,
+ * R#12); each product is rounded, then summed in order R, so the result is
+ * bit-identical to ftn_sum of the packed product vector.  Workspace as for
+ * ftn_sum(x). */
+ftn_status_t ftn_dot_product(const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev,
+                             void* ws, size_t ws_bytes, ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- a5
+ * dst = TRANSPOSE(src): dst(j,i) = src(i,j); src rank 2 with shape
+ * (n1,n2), dst rank 2 with shape (n2,n1), same type, any strides, no overlap
+ * (an overlapping dst is evaluated through a temporary). */
+ftn_status_t ftn_transpose(const ftn_desc_t* dst, const ftn_desc_t* src, ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- a6
+ * c = MATMUL(a, b) for real(8) rank-2 operands:
+ * c(i,j) = sum_l a(i,l) b(l,j); a (m,k), b (k,n), c (m,n).  Computed on the
+ * fp64 tensor cores (DMMA); the per-element summation order inside a tensor
+ * core step is the hardware's, so the result is within 4*k*2^-53*sum|a||b|
+ * of the exact value (R#8, R#14), and exact when all partial sums are
+ * representable (integer-valued data).  Operands that are not TMA-able
+ * (dim-1 stride != 8 bytes, a column stride that is not a multiple of 16
+ * bytes, a base that is not 16-byte aligned) are first packed into ws.
+ * c must not overlap a or b.  Rank-1 forms: FTN_ERR_UNSUPPORTED. */
+ftn_status_t ftn_matmul_workspace_size(const ftn_desc_t* c, const ftn_desc_t* a,
+                                       const ftn_desc_t* b, size_t* bytes);
+ftn_status_t ftn_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws,
+                        size_t ws_bytes, ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- a7
+ * Jacobi sweeps ("a Jacobi iteration solving Laplace's equation"; the
+ * DO-nest of R#16):
+ *   do s = 1, sweeps
+ *     unew(i,j) = coeff * (((u(i-1,j) + u(i+1,j)) + u(i,j-1)) + u(i,j+1))
+ *   (3-D: coeff * (((((u(i-1)+u(i+1)) + u(j-1)) + u(j+1)) + u(k-1)) + u(k+1)))
+ *   for every interior point, then swap(u, unew).
+ * u, unew: real(8), rank 2 (5-point) or rank 3 (7-point), conformable, not
+ * overlapping.  Only interior points are written: the caller presets the
+ * boundary of both arrays.  *result_in_unew (host) receives 1 when the final
+ * values are in unew (odd sweeps), else 0.  Bit-exact vs the oracle. */
+ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
+                        int32_t* result_in_unew, ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- a8
+ * Multi-GPU (one process per GPU, NCCL over NVLink).  The id travels between
+ * processes through the caller's own channel (torch.distributed store). */
+typedef struct ftn_comm_s* ftn_comm_t;
+#define FTN_COMM_ID_BYTES 128
+ftn_status_t ftn_comm_unique_id(uint8_t id[FTN_COMM_ID_BYTES]);
+ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank,
+                           const uint8_t id[FTN_COMM_ID_BYTES], int32_t device);
+ftn_status_t ftn_comm_destroy(ftn_comm_t comm);
+
+/* Global reductions of an array slab-distributed over the ranks along its
+ * last dimension (x_local is this rank's slab).  The result, identical on
+ * every rank, goes to result_dev.  Real SUM / DOT: each rank reduces its slab
+ * in order R, the p rank partials are all-gathered and combined by the same
+ * balanced tree, so the result equals the single-GPU one bit for bit when
+ * every slab holds the same power-of-two number of R chunks; otherwise it is
+ * within the bound of R#8.  MAX/MIN: all-reduce.  ws: ftn_reduce_workspace_size
+ * of x_local plus 8*(nranks+1) bytes. */
+ftn_status_t ftn_sum_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev, void* ws,
+                            size_t ws_bytes, ftn_stream_t stream);
+ftn_status_t ftn_maxval_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev,
+                               void* ws, size_t ws_bytes, ftn_stream_t stream);
+ftn_status_t ftn_minval_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev,
+                               void* ws, size_t ws_bytes, ftn_stream_t stream);
+ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local,
+                                    const ftn_desc_t* y_local, void* result_dev, void* ws,
+                                    size_t ws_bytes, ftn_stream_t stream);
+
+/* Distributed Jacobi: u_local / unew_local are this rank's slab of the global
+ * array along the last dimension INCLUDING one halo plane on each side
+ * (planes 1 and n_last of the local arrays); rank r's first owned plane
+ * follows rank r-1's last.  On the first and last rank the outer halo plane
+ * is the global boundary plane.  Each sweep exchanges the owned boundary
+ * planes with ranks r-1 / r+1 (ncclSend/ncclRecv) and updates the interior.
+ * Results are bit-identical to ftn_jacobi on the undivided array. */
+ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const ftn_desc_t* unew_local,
+                             int64_t sweeps, double coeff, int32_t* result_in_unew,
+                             ftn_stream_t stream);
+
+/* c(:, J_r) = MATMUL(a, b(:, J_r)): b_local / c_local are this rank's column
+ * block, a is replicated (see ftn_bcast).  No communication. */
+ftn_status_t ftn_matmul_colsharded(ftn_comm_t comm, const ftn_desc_t* c_local, const ftn_desc_t* a_full,
+                                   const ftn_desc_t* b_local, void* ws, size_t ws_bytes,
+                                   ftn_stream_t stream);
+/* Broadcast a contiguous array from root to every rank (ncclBroadcast). */
+ftn_status_t ftn_bcast(ftn_comm_t comm, const ftn_desc_t* x, int32_t root, ftn_stream_t stream);
+
+/* ---------------------------------------------------------------- support */
+
+/* Seeded synthetic inputs (not part of the method):
+ * element t (array element order) of dst gets a value derived from
+ *   h = splitmix64(seed ^ (array_id << 56) ^ t)
+ * mode 1 U[0,1) = (h >> 11) * 2^-53; 2 U[-1,1) = 2*U[0,1) - 1;
+ * 3 integer in [-8, 8] = (h >> 11) % 17 - 8; 4 t; 5 t mod 1024;
+ * 6 (integer types) the low bits of h. */
+typedef enum { FTN_GEN_U01 = 1, FTN_GEN_U11 = 2, FTN_GEN_INT8 = 3, FTN_GEN_LINEAR = 4,
+               FTN_GEN_MOD1024 = 5, FTN_GEN_RAW = 6 } ftn_gen_mode_t;
+ftn_status_t ftn_gen_fill(const ftn_desc_t* dst, uint64_t seed, uint64_t array_id, int32_t mode,
+                          ftn_stream_t stream);
+
+/* Number of kernels this library has launched in this process (all devices). */
+uint64_t ftn_launch_count(void);
+
+const char* ftn_status_string(ftn_status_t s);
+const char* ftn_last_error(void); /* thread-local detail of the last failure */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTN_H */
