@@ -214,8 +214,9 @@ ftn_status_t ftn_comm_destroy(ftn_comm_t comm);
  * in order R, the p rank partials are all-gathered and combined by the same
  * balanced tree, so the result equals the single-GPU one bit for bit when
  * every slab holds the same power-of-two number of R chunks; otherwise it is
- * within the bound of R#8.  MAX/MIN: all-reduce.  ws: ftn_reduce_workspace_size
- * of x_local plus 8*(nranks+1) bytes. */
+ * within the bound of R#8.  MAX/MIN and integer(8) SUM use the same all-gather +
+ * tree (exact).  real(8) and integer(8) only.  ws: ftn_reduce_workspace_size of
+ * x_local plus 8*(nranks+1) bytes, 8-byte aligned. */
 ftn_status_t ftn_sum_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev, void* ws,
                             size_t ws_bytes, ftn_stream_t stream);
 ftn_status_t ftn_maxval_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev,

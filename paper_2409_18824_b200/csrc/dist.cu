@@ -1,0 +1,208 @@
+// Multi-GPU layer: one process per GPU, NCCL over
+// NVLink 5 / NVSwitch.  The paper itself only threads with OpenMP;
+// BASELINE's north star partitions the work where it shards naturally:
+//   * reductions: each rank reduces its slab in order R, the p rank partials are
+//     all-gathered and combined by the same balanced tree on every rank
+//     (deterministic; equal to the 1-GPU result when slabs are equal power-of-two
+//     multiples of the R chunk);
+//   * Jacobi: last-dimension slabs with one halo plane per side, halos exchanged
+//     with ncclSend/ncclRecv every sweep;
+//   * MATMUL: column blocks of b and c, a replicated (ftn_bcast once).
+#include "ftn_internal.cuh"
+
+#include <nccl.h>
+#include <cstring>
+
+struct ftn_comm_s {
+  ncclComm_t nccl;
+  int nranks, rank, device;
+};
+
+namespace ftn {
+size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b);
+ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws, size_t ws_bytes,
+                          cudaStream_t s);
+ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew);
+ftn_status_t jacobi_prepare();
+
+namespace {
+
+ftn_status_t nccl_fail(ncclResult_t r, const char* what) {
+  return fail(FTN_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define FTN_NCCL(expr)                                         \
+  do {                                                         \
+    ncclResult_t r__ = (expr);                                 \
+    if (r__ != ncclSuccess) return nccl_fail(r__, #expr);      \
+  } while (0)
+
+ncclDataType_t nccl_type(int32_t t) {
+  switch (t) {
+    case FTN_I32: return ncclInt32;
+    case FTN_I64: return ncclInt64;
+    case FTN_F32: return ncclFloat32;
+    default: return ncclFloat64;
+  }
+}
+
+ftn_status_t global_reduce(int kind, ftn_comm_t comm, const ftn_desc_t* x, const ftn_desc_t* y, void* result,
+                           void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (!comm) return fail(FTN_ERR_NULL, "global reduction: comm NULL");
+  if (!result) return fail(FTN_ERR_NULL, "global reduction: result NULL");
+  const size_t head = 8 * ((size_t)comm->nranks + 1);
+  if (!ws || ws_bytes < head + reduce_ws_bytes(desc_size(x)) || ((uintptr_t)ws % 8))
+    return fail(FTN_ERR_WORKSPACE, "global reduction: workspace must hold reduce_workspace_size + 8*(nranks+1) bytes");
+  if (x->type == FTN_I32)
+    return fail(FTN_ERR_UNSUPPORTED, "global reductions of integer(4) are not offered; use integer(8)");
+  char* w = (char*)ws;
+  void* local = w;
+  void* gathered = w + 8;
+  FTN_CHECK(reduce_local(kind, x, y, local, w + head, ws_bytes - head, s));
+  FTN_NCCL(ncclAllGather(local, gathered, 1, nccl_type(x->type), comm->nccl, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return tree_combine_launch(kind, x->type, gathered, comm->nranks, result, s);
+}
+
+bool plane_contiguous(const ftn_desc_t* d) {
+  int64_t expect = d->elem_len;
+  for (int k = 0; k < d->rank - 1; ++k) {
+    if (d->dim[k].sm != expect) return false;
+    expect *= d->dim[k].extent;
+  }
+  return true;
+}
+
+}  // namespace
+}  // namespace ftn
+
+using namespace ftn;
+
+extern "C" {
+
+ftn_status_t ftn_comm_unique_id(uint8_t id[FTN_COMM_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == FTN_COMM_ID_BYTES, "ncclUniqueId size");
+  if (!id) return fail(FTN_ERR_NULL, "ftn_comm_unique_id: id NULL");
+  ncclUniqueId u;
+  FTN_NCCL(ncclGetUniqueId(&u));
+  memcpy(id, &u, sizeof(u));
+  return FTN_OK;
+}
+
+ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank, const uint8_t id[FTN_COMM_ID_BYTES],
+                           int32_t device) {
+  if (!comm || !id) return fail(FTN_ERR_NULL, "ftn_comm_init: NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FTN_ERR_SHAPE, "ftn_comm_init: bad rank / nranks");
+  FTN_CUDA(cudaSetDevice(device));
+  FTN_CHECK(require_sm100());
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  ftn_comm_s* c = new ftn_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  *comm = c;
+  return FTN_OK;
+}
+
+ftn_status_t ftn_comm_destroy(ftn_comm_t comm) {
+  if (!comm) return FTN_OK;
+  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  delete comm;
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+  return FTN_OK;
+}
+
+ftn_status_t ftn_sum_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev, void* ws, size_t ws_bytes,
+                            ftn_stream_t stream) {
+  FTN_CHECK(check_desc(x_local, "ftn_sum_global(x)", 1, FTN_MAX_RANK));
+  FTN_CHECK(require_sm100());
+  return global_reduce(RK_SUM, comm, x_local, nullptr, result_dev, ws, ws_bytes, (cudaStream_t)stream);
+}
+ftn_status_t ftn_maxval_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev, void* ws,
+                               size_t ws_bytes, ftn_stream_t stream) {
+  FTN_CHECK(check_desc(x_local, "ftn_maxval_global(x)", 1, FTN_MAX_RANK));
+  FTN_CHECK(require_sm100());
+  return global_reduce(RK_MAX, comm, x_local, nullptr, result_dev, ws, ws_bytes, (cudaStream_t)stream);
+}
+ftn_status_t ftn_minval_global(ftn_comm_t comm, const ftn_desc_t* x_local, void* result_dev, void* ws,
+                               size_t ws_bytes, ftn_stream_t stream) {
+  FTN_CHECK(check_desc(x_local, "ftn_minval_global(x)", 1, FTN_MAX_RANK));
+  FTN_CHECK(require_sm100());
+  return global_reduce(RK_MIN, comm, x_local, nullptr, result_dev, ws, ws_bytes, (cudaStream_t)stream);
+}
+ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local, const ftn_desc_t* y_local,
+                                    void* result_dev, void* ws, size_t ws_bytes, ftn_stream_t stream) {
+  FTN_CHECK(check_desc(x_local, "ftn_dot_product_global(x)", 1, 1));
+  FTN_CHECK(check_desc(y_local, "ftn_dot_product_global(y)", 1, 1));
+  if (x_local->type != FTN_F64 || y_local->type != FTN_F64) return fail(FTN_ERR_TYPE, "dot: real(8) only");
+  if (x_local->dim[0].extent != y_local->dim[0].extent) return fail(FTN_ERR_SHAPE, "dot: sizes differ");
+  FTN_CHECK(require_sm100());
+  return global_reduce(RK_DOT, comm, x_local, y_local, result_dev, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
+                             double coeff, int32_t* result_in_unew, ftn_stream_t stream) {
+  if (!comm) return fail(FTN_ERR_NULL, "ftn_jacobi_dist: comm NULL");
+  FTN_CHECK(jacobi_check(u, unew));
+  if (!plane_contiguous(u) || !plane_contiguous(unew))
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_dist: last-dimension planes must be contiguous");
+  if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: negative sweep count");
+  const int r = u->rank;
+  const int64_t nl = u->dim[r - 1].extent;
+  if (nl < 3) return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: a slab needs 1 owned plane + 2 halo planes");
+  FTN_CHECK(require_sm100());
+  FTN_CHECK(jacobi_prepare());
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t plane = (size_t)(desc_size(u) / nl);
+  const int lower = comm->rank - 1, upper = comm->rank + 1;
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    const ftn_desc_t* src = (sw % 2 == 0) ? u : unew;
+    const ftn_desc_t* dst = (sw % 2 == 0) ? unew : u;
+    char* b = (char*)src->base_addr;
+    const int64_t sm = src->dim[r - 1].sm;
+    // halo exchange of the source: owned boundary planes -> neighbours' halo planes
+    if (comm->nranks > 1) {
+      FTN_NCCL(ncclGroupStart());
+      if (lower >= 0) {
+        FTN_NCCL(ncclSend(b + 1 * sm, plane, ncclFloat64, lower, comm->nccl, s));
+        FTN_NCCL(ncclRecv(b + 0 * sm, plane, ncclFloat64, lower, comm->nccl, s));
+      }
+      if (upper < comm->nranks) {
+        FTN_NCCL(ncclSend(b + (nl - 2) * sm, plane, ncclFloat64, upper, comm->nccl, s));
+        FTN_NCCL(ncclRecv(b + (nl - 1) * sm, plane, ncclFloat64, upper, comm->nccl, s));
+      }
+      FTN_NCCL(ncclGroupEnd());
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    FTN_CHECK(jacobi_sweep(src, dst, coeff, 1, nl - 2, s));
+  }
+  if (result_in_unew) *result_in_unew = (int32_t)(sweeps % 2);
+  return FTN_OK;
+}
+
+ftn_status_t ftn_matmul_colsharded(ftn_comm_t comm, const ftn_desc_t* c_local, const ftn_desc_t* a_full,
+                                   const ftn_desc_t* b_local, void* ws, size_t ws_bytes, ftn_stream_t stream) {
+  if (!comm) return fail(FTN_ERR_NULL, "ftn_matmul_colsharded: comm NULL");
+  size_t need = 0;
+  FTN_CHECK(ftn_matmul_workspace_size(c_local, a_full, b_local, &need));
+  FTN_CHECK(require_sm100());
+  return matmul_local(c_local, a_full, b_local, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+ftn_status_t ftn_bcast(ftn_comm_t comm, const ftn_desc_t* x, int32_t root, ftn_stream_t stream) {
+  if (!comm) return fail(FTN_ERR_NULL, "ftn_bcast: comm NULL");
+  FTN_CHECK(check_desc(x, "ftn_bcast(x)", 1, FTN_MAX_RANK));
+  if (!desc_contiguous(x)) return fail(FTN_ERR_UNSUPPORTED, "ftn_bcast: array must be contiguous");
+  if (root < 0 || root >= comm->nranks) return fail(FTN_ERR_SHAPE, "ftn_bcast: bad root");
+  FTN_NCCL(ncclBroadcast(x->base_addr, x->base_addr, (size_t)desc_size(x), nccl_type(x->type), root, comm->nccl,
+                         (cudaStream_t)stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return FTN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,459 @@
+// Jacobi sweeps, P:92 ("a Jacobi iteration solving Laplace's
+// equation"), Table II (249 s for 1024^2 x 10^5 on one EPYC core), Table IV.
+//
+//   unew(i,j)   = c * (((u(i-1,j) + u(i+1,j)) + u(i,j-1)) + u(i,j+1))            (2-D)
+//   unew(i,j,k) = c * (((((u(i-1)+u(i+1)) + u(j-1)) + u(j+1)) + u(k-1)) + u(k+1))  (3-D)
+//
+// Same neighbour order and the same single rounding per add as the oracle
+// (compiled with -fmad=false), so results are bit-exact.
+//
+// HBM-bound at 16 B per lattice update (read u once, write unew once).  The
+// paper's stencil problems were missing vectorisation and dynamic shapes (P:281-
+// 286); here each CTA streams a strip of the grid through shared memory with TMA
+// (cp.async.bulk.tensor + mbarrier pipeline, one producer warp), so every u value
+// is read from HBM once per sweep and reused from shared memory by its 4 (6)
+// neighbours.
+//   2-D: strips 128 columns wide; stages of {130 x 32} rows (30 output rows, 1-row
+//        halo each side), 3 stages.
+//   3-D: columns of 128 x 16 points streamed along k; a ring of 5 planes
+//        {130 x 18}, outputs for plane k once plane k+1 has landed.
+// Work is split evenly over a persistent grid (2 CTAs per SM) in row (plane)
+// units, so every CTA moves the same number of bytes.
+#include "ftn_internal.cuh"
+
+#include <cstring>
+
+namespace ftn {
+namespace {
+
+// ---------------------------------------------------------------- 2-D
+constexpr int S2_W = 128;              // interior columns per strip
+constexpr int S2_BOXW = S2_W + 2;      // 130
+constexpr int S2_R = 30;               // output rows per stage
+constexpr int S2_BOXH = S2_R + 2;      // 32
+constexpr int S2_STAGES = 3;
+constexpr int S2_STAGE_BYTES = S2_BOXW * S2_BOXH * 8;  // 33280
+constexpr int S2_CONS_WARPS = S2_W / 32;               // 4
+constexpr int S2_THREADS = (S2_CONS_WARPS + 1) * 32;
+constexpr int S2_SMEM = S2_STAGES * S2_STAGE_BYTES + 128 + 64;
+
+struct J2Params {
+  char* dst;
+  int64_t d_sm1, d_sm2;
+  int64_t n1, n2;
+  int64_t tiles_i;  // strips
+  int64_t nrows;    // interior rows n2 - 2
+  int64_t total;    // tiles_i * nrows
+  int64_t per_cta;
+  int64_t lo;       // first output row (0-based position in dim 2)
+  double coeff;
+};
+
+// Iterate this CTA's chunks: (strip, first output row, row count)
+struct ChunkIter2 {
+  int64_t L, Lend, nrows, lo;
+  __device__ bool next(int64_t& strip, int64_t& j0, int& cnt) {
+    if (L >= Lend) return false;
+    strip = L / nrows;
+    const int64_t r = L % nrows;
+    int64_t left_in_strip = nrows - r;
+    int64_t left = Lend - L;
+    int64_t n = left_in_strip < left ? left_in_strip : left;
+    if (n > S2_R) n = S2_R;
+    j0 = lo + r;  // 0-based row position
+    cnt = (int)n;
+    L += n;
+    return true;
+  }
+};
+
+__global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant__ CUtensorMap src_map,
+                                                           const __grid_constant__ J2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S2_STAGES * S2_STAGE_BYTES);
+  uint64_t* empty = full + S2_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S2_STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], S2_CONS_WARPS);
+    }
+    dev::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t L0 = (int64_t)blockIdx.x * p.per_cta;
+  const int64_t L1 = min(L0 + p.per_cta, p.total);
+
+  if (warp == S2_CONS_WARPS) {
+    if (lane == 0) {
+      dev::prefetch_tma(&src_map);
+      ChunkIter2 it{L0, L1, p.nrows, p.lo};
+      int64_t strip, j0;
+      int cnt;
+      for (int k = 0; it.next(strip, j0, cnt); ++k) {
+        const int s = k % S2_STAGES;
+        if (k >= S2_STAGES) dev::mbar_wait(&empty[s], ((k / S2_STAGES) - 1) & 1);
+        dev::mbar_arrive_expect_tx(&full[s], S2_STAGE_BYTES);
+        dev::tma_load_2d(smem + s * S2_STAGE_BYTES, &src_map, &full[s], (int32_t)(strip * S2_W - 1),
+                         (int32_t)(j0 - 1));
+      }
+    }
+    return;
+  }
+
+  const int x = threadIdx.x;  // column within the strip
+  ChunkIter2 it{L0, L1, p.nrows, p.lo};
+  int64_t strip, j0;
+  int cnt;
+  const double c = p.coeff;
+  for (int k = 0; it.next(strip, j0, cnt); ++k) {
+    const int s = k % S2_STAGES;
+    const int64_t i = strip * S2_W + x;
+    const bool active = i >= 1 && i <= p.n1 - 2;
+    dev::mbar_wait(&full[s], (k / S2_STAGES) & 1);
+    const double* t = reinterpret_cast<const double*>(smem + s * S2_STAGE_BYTES);
+    // smem row r holds u(:, j0 - 1 + r); column x + 1 holds i
+    double up = t[x + 1], mid = t[S2_BOXW + x + 1];
+    char* out = p.dst + i * p.d_sm1 + j0 * p.d_sm2;
+    for (int r = 1; r <= cnt; ++r) {
+      const double* row = t + r * S2_BOXW;
+      const double down = row[S2_BOXW + x + 1];
+      double v = row[x] + row[x + 2];
+      v = v + up;
+      v = v + down;
+      if (active) *reinterpret_cast<double*>(out) = c * v;
+      out += p.d_sm2;
+      up = mid;
+      mid = down;
+    }
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(&empty[s]);
+  }
+}
+
+// ---------------------------------------------------------------- 3-D
+constexpr int S3_W = 128, S3_H = 16;
+constexpr int S3_BOXW = S3_W + 2, S3_BOXH = S3_H + 2;  // 130 x 18
+constexpr int S3_STAGES = 5;
+constexpr int S3_PLANE_BYTES = S3_BOXW * S3_BOXH * 8;  // 18720 (TMA transaction bytes)
+constexpr int S3_PLANE_STRIDE = (S3_PLANE_BYTES + 127) / 128 * 128;  // 128-byte aligned stages
+constexpr int S3_ROWS_PER_THREAD = 8;
+constexpr int S3_CONS_THREADS = S3_W * S3_H / S3_ROWS_PER_THREAD;  // 256
+constexpr int S3_CONS_WARPS = S3_CONS_THREADS / 32;                // 8
+constexpr int S3_THREADS = S3_CONS_THREADS + 32;
+constexpr int S3_SMEM = S3_STAGES * S3_PLANE_STRIDE + 128 + 128;
+
+struct J3Params {
+  char* dst;
+  int64_t d_sm1, d_sm2, d_sm3;
+  int64_t n1, n2, n3;
+  int64_t tiles_i, tiles_j;
+  int64_t nk;      // interior planes n3 - 2
+  int64_t total;   // tiles_i * tiles_j * nk
+  int64_t per_cta;
+  int64_t lo;      // first output plane
+  double coeff;
+};
+
+struct SegIter3 {
+  int64_t L, Lend, nk, lo;
+  __device__ bool next(int64_t& col, int64_t& k0, int64_t& n) {
+    if (L >= Lend) return false;
+    col = L / nk;
+    const int64_t r = L % nk;
+    const int64_t a = nk - r, b = Lend - L;
+    n = a < b ? a : b;
+    k0 = lo + r;
+    L += n;
+    return true;
+  }
+};
+
+__global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant__ CUtensorMap src_map,
+                                                           const __grid_constant__ J3Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S3_STAGES * S3_PLANE_STRIDE);
+  uint64_t* empty = full + S3_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S3_STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], S3_CONS_WARPS);
+    }
+    dev::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t L0 = (int64_t)blockIdx.x * p.per_cta;
+  const int64_t L1 = min(L0 + p.per_cta, p.total);
+
+  if (warp == S3_CONS_WARPS) {
+    if (lane == 0) {
+      dev::prefetch_tma(&src_map);
+      SegIter3 it{L0, L1, p.nk, p.lo};
+      int64_t col, k0, n;
+      int64_t gp = 0;  // global plane counter of this CTA
+      while (it.next(col, k0, n)) {
+        const int32_t ci = (int32_t)((col % p.tiles_i) * S3_W - 1);
+        const int32_t cj = (int32_t)((col / p.tiles_i) * S3_H - 1);
+        for (int64_t kk = k0 - 1; kk <= k0 + n; ++kk, ++gp) {
+          const int s = (int)(gp % S3_STAGES);
+          if (gp >= S3_STAGES) dev::mbar_wait(&empty[s], (uint32_t)(((gp / S3_STAGES) - 1) & 1));
+          dev::mbar_arrive_expect_tx(&full[s], S3_PLANE_BYTES);
+          dev::tma_load_3d(smem + s * S3_PLANE_STRIDE, &src_map, &full[s], ci, cj, (int32_t)kk);
+        }
+      }
+    }
+    return;
+  }
+
+  const int x = threadIdx.x % S3_W;
+  const int yb = threadIdx.x / S3_W;  // 0..1
+  SegIter3 it{L0, L1, p.nk, p.lo};
+  int64_t col, k0, n;
+  int64_t gp = 0;
+  const double c = p.coeff;
+  while (it.next(col, k0, n)) {
+    const int64_t i = (col % p.tiles_i) * S3_W + x;
+    const int64_t jbase = (col / p.tiles_i) * S3_H + yb * S3_ROWS_PER_THREAD;
+    const bool iact = i >= 1 && i <= p.n1 - 2;
+    // planes gp (k0-1) and gp+1 (k0) first
+    dev::mbar_wait(&full[gp % S3_STAGES], (uint32_t)((gp / S3_STAGES) & 1));
+    dev::mbar_wait(&full[(gp + 1) % S3_STAGES], (uint32_t)(((gp + 1) / S3_STAGES) & 1));
+    for (int64_t q = 0; q < n; ++q) {
+      const int64_t pn = gp + q + 2;  // plane k+1
+      dev::mbar_wait(&full[pn % S3_STAGES], (uint32_t)((pn / S3_STAGES) & 1));
+      const double* Pm = reinterpret_cast<const double*>(smem + ((gp + q) % S3_STAGES) * S3_PLANE_STRIDE);
+      const double* P0 = reinterpret_cast<const double*>(smem + ((gp + q + 1) % S3_STAGES) * S3_PLANE_STRIDE);
+      const double* Pp = reinterpret_cast<const double*>(smem + (pn % S3_STAGES) * S3_PLANE_STRIDE);
+      const int64_t k = k0 + q;
+      const int r0 = yb * S3_ROWS_PER_THREAD + 1;  // smem row of the first j
+      double jm = P0[(r0 - 1) * S3_BOXW + x + 1];
+      double jc = P0[r0 * S3_BOXW + x + 1];
+      char* out = p.dst + i * p.d_sm1 + jbase * p.d_sm2 + k * p.d_sm3;
+#pragma unroll
+      for (int jj = 0; jj < S3_ROWS_PER_THREAD; ++jj) {
+        const int r = r0 + jj;
+        const double jp = P0[(r + 1) * S3_BOXW + x + 1];
+        double v = P0[r * S3_BOXW + x] + P0[r * S3_BOXW + x + 2];
+        v = v + jm;
+        v = v + jp;
+        v = v + Pm[r * S3_BOXW + x + 1];
+        v = v + Pp[r * S3_BOXW + x + 1];
+        const int64_t j = jbase + jj;
+        if (iact && j >= 1 && j <= p.n2 - 2) *reinterpret_cast<double*>(out) = c * v;
+        out += p.d_sm2;
+        jm = jc;
+        jc = jp;
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[(gp + q) % S3_STAGES]);  // plane k-1 is done
+    }
+    __syncwarp();
+    if (lane == 0) {
+      dev::mbar_arrive(&empty[(gp + n) % S3_STAGES]);
+      dev::mbar_arrive(&empty[(gp + n + 1) % S3_STAGES]);
+    }
+    gp += n + 2;
+  }
+}
+
+// ---------------------------------------------------------------- generic (any strides)
+struct JGParams {
+  KDesc src, dst;
+  int rank;
+  int64_t n1, n2, n3;
+  int64_t k_lo, k_hi;  // planes (3-D) / rows (2-D) of the last dim to update, inclusive
+  double coeff;
+};
+
+__global__ void __launch_bounds__(256) jacobi_generic(const __grid_constant__ JGParams p) {
+  const int64_t m1 = p.n1 - 2;
+  const int64_t m2 = p.rank == 3 ? p.n2 - 2 : 1;
+  const int64_t nl = p.k_hi - p.k_lo + 1;
+  const int64_t total = m1 * m2 * nl;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 1 + t % m1;
+    const int64_t rest = t / m1;
+    const char* b = p.src.base;
+    const int64_t s0 = p.src.sm[0], s1 = p.src.sm[1], s2 = p.src.sm[2];
+    if (p.rank == 2) {
+      const int64_t j = p.k_lo + rest;
+      const char* c0 = b + i * s0 + j * s1;
+      double v = *(const double*)(c0 - s0) + *(const double*)(c0 + s0);
+      v = v + *(const double*)(c0 - s1);
+      v = v + *(const double*)(c0 + s1);
+      *(double*)(p.dst.base + i * p.dst.sm[0] + j * p.dst.sm[1]) = p.coeff * v;
+    } else {
+      const int64_t j = 1 + rest % m2;
+      const int64_t k = p.k_lo + rest / m2;
+      const char* c0 = b + i * s0 + j * s1 + k * s2;
+      double v = *(const double*)(c0 - s0) + *(const double*)(c0 + s0);
+      v = v + *(const double*)(c0 - s1);
+      v = v + *(const double*)(c0 + s1);
+      v = v + *(const double*)(c0 - s2);
+      v = v + *(const double*)(c0 + s2);
+      *(double*)(p.dst.base + i * p.dst.sm[0] + j * p.dst.sm[1] + k * p.dst.sm[2]) = p.coeff * v;
+    }
+  }
+}
+
+bool stencil_tma_able(const ftn_desc_t* d) {
+  if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
+  for (int k = 1; k < d->rank; ++k)
+    if (d->dim[k].sm <= 0 || (d->dim[k].sm % 16) != 0 || d->dim[k].sm >= (1ll << 40)) return false;
+  for (int k = 0; k < d->rank; ++k)
+    if (d->dim[k].extent >= (1ll << 31)) return false;
+  return true;
+}
+
+ftn_status_t make_stencil_map(CUtensorMap* m, const ftn_desc_t* d) {
+  uint64_t dims[3] = {(uint64_t)d->dim[0].extent, (uint64_t)d->dim[1].extent,
+                      (uint64_t)(d->rank == 3 ? d->dim[2].extent : 1)};
+  uint64_t strides[2] = {(uint64_t)d->dim[1].sm, (uint64_t)(d->rank == 3 ? d->dim[2].sm : 0)};
+  if (d->rank == 2) {
+    uint32_t box[2] = {S2_BOXW, S2_BOXH};
+    return encode_tma(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, d->base_addr, dims, strides, box,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  uint32_t box[3] = {S3_BOXW, S3_BOXH, 1};
+  return encode_tma(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, d->base_addr, dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+// One sweep src -> dst over last-dimension planes [lo, hi] (inclusive, 0-based,
+// interior only).  TMA path when the whole range is the full interior and both
+// descriptors are TMA-able; otherwise the generic kernel.
+ftn_status_t sweep(const ftn_desc_t* src, const ftn_desc_t* dst, const CUtensorMap* map, double coeff, int64_t lo,
+                   int64_t hi, cudaStream_t s) {
+  const int rank = src->rank;
+  const int64_t n1 = src->dim[0].extent, n2 = src->dim[1].extent, n3 = rank == 3 ? src->dim[2].extent : 1;
+  const int64_t nlast = rank == 3 ? n3 : n2;
+  if (n1 < 3 || n2 < 3 || (rank == 3 && n3 < 3)) return FTN_OK;  // no interior
+  if (lo < 1) lo = 1;
+  if (hi > nlast - 2) hi = nlast - 2;
+  if (hi < lo) return FTN_OK;
+  const int sms = num_sms();
+  if (map) {
+    if (rank == 2) {
+      J2Params p;
+      p.dst = (char*)dst->base_addr;
+      p.d_sm1 = dst->dim[0].sm;
+      p.d_sm2 = dst->dim[1].sm;
+      p.n1 = n1;
+      p.n2 = n2;
+      p.tiles_i = (n1 + S2_W - 1) / S2_W;
+      p.nrows = hi - lo + 1;
+      p.total = p.tiles_i * p.nrows;
+      p.coeff = coeff;
+      int64_t grid = (int64_t)sms * 2;
+      if (grid > p.total) grid = p.total;
+      p.per_cta = (p.total + grid - 1) / grid;
+      grid = (p.total + p.per_cta - 1) / p.per_cta;
+      p.lo = lo;
+      jacobi2d_tma<<<(unsigned)grid, S2_THREADS, S2_SMEM, s>>>(*map, p);
+      return after_launch("jacobi2d_tma");
+    } else {
+      J3Params p;
+      p.dst = (char*)dst->base_addr;
+      p.d_sm1 = dst->dim[0].sm;
+      p.d_sm2 = dst->dim[1].sm;
+      p.d_sm3 = dst->dim[2].sm;
+      p.n1 = n1;
+      p.n2 = n2;
+      p.n3 = n3;
+      p.tiles_i = (n1 + S3_W - 1) / S3_W;
+      p.tiles_j = (n2 + S3_H - 1) / S3_H;
+      p.nk = hi - lo + 1;
+      p.total = p.tiles_i * p.tiles_j * p.nk;
+      p.coeff = coeff;
+      int64_t grid = (int64_t)sms * 2;
+      if (grid > p.total) grid = p.total;
+      p.per_cta = (p.total + grid - 1) / grid;
+      grid = (p.total + p.per_cta - 1) / p.per_cta;
+      p.lo = lo;
+      jacobi3d_tma<<<(unsigned)grid, S3_THREADS, S3_SMEM, s>>>(*map, p);
+      return after_launch("jacobi3d_tma");
+    }
+  }
+  JGParams g;
+  g.src = to_kdesc(src);
+  g.dst = to_kdesc(dst);
+  g.rank = rank;
+  g.n1 = n1;
+  g.n2 = n2;
+  g.n3 = n3;
+  g.k_lo = lo;
+  g.k_hi = hi;
+  g.coeff = coeff;
+  const int64_t total = (n1 - 2) * (rank == 3 ? n2 - 2 : 1) * (hi - lo + 1);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  jacobi_generic<<<(unsigned)blocks, 256, 0, s>>>(g);
+  return after_launch("jacobi_generic");
+}
+
+}  // namespace
+
+// Used by the distributed layer: one sweep over planes [lo, hi] of the last dim.
+ftn_status_t jacobi_sweep(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t lo, int64_t hi,
+                          cudaStream_t stream) {
+  CUtensorMap m;
+  const CUtensorMap* mp = nullptr;
+  if (stencil_tma_able(src)) {
+    FTN_CHECK(make_stencil_map(&m, src));
+    mp = &m;
+  }
+  return sweep(src, dst, mp, coeff, lo, hi, stream);
+}
+
+ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
+  FTN_CHECK(check_desc(u, "ftn_jacobi(u)", 2, 3));
+  FTN_CHECK(check_desc(unew, "ftn_jacobi(unew)", 2, 3));
+  if (u->type != FTN_F64 || unew->type != FTN_F64) return fail(FTN_ERR_TYPE, "ftn_jacobi: real(8) only");
+  if (!same_shape(u, unew)) return fail(FTN_ERR_SHAPE, "ftn_jacobi: u and unew are not conformable");
+  if (desc_overlap(u, unew)) return fail(FTN_ERR_SHAPE, "ftn_jacobi: u and unew overlap");
+  return FTN_OK;
+}
+
+static bool g_attr_done[64];
+
+ftn_status_t jacobi_prepare() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_attr_done[dev & 63]) {
+    FTN_CUDA(cudaFuncSetAttribute(jacobi2d_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, S2_SMEM));
+    FTN_CUDA(cudaFuncSetAttribute(jacobi3d_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, S3_SMEM));
+    g_attr_done[dev & 63] = true;
+  }
+  return FTN_OK;
+}
+
+}  // namespace ftn
+
+using namespace ftn;
+
+extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
+                                   int32_t* result_in_unew, ftn_stream_t stream) {
+  FTN_CHECK(jacobi_check(u, unew));
+  if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi: negative sweep count");
+  FTN_CHECK(require_sm100());
+  FTN_CHECK(jacobi_prepare());
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
+  CUtensorMap mu, mw;
+  if (tma) {
+    FTN_CHECK(make_stencil_map(&mu, u));
+    FTN_CHECK(make_stencil_map(&mw, unew));
+  }
+  const int64_t nlast = u->dim[u->rank - 1].extent;
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    const bool even = (sw % 2) == 0;
+    const ftn_desc_t* src = even ? u : unew;
+    const ftn_desc_t* dst = even ? unew : u;
+    FTN_CHECK(sweep(src, dst, tma ? (even ? &mu : &mw) : nullptr, coeff, 1, nlast - 2, s));
+  }
+  if (result_in_unew) *result_in_unew = (int32_t)(sweeps % 2);
+  return FTN_OK;
+}

@@ -1,0 +1,129 @@
+"""GPU parity: Jacobi sweeps (TMA 2-D / 3-D kernels and the generic strided kernel) vs the
+oracle, bit-exact (R#16, R#23)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import FArray as OA
+
+pytestmark = pytest.mark.gpu
+C2, C3 = 0.25, 1.0 / 6.0
+
+
+@pytest.fixture(scope="module")
+def ftn():
+    from paper_2409_18824_b200 import ftn
+    return ftn
+
+
+def _run_both(ftn, u0, sweeps, coeff, lbs=None):
+    U, W = ftn.FArray.from_numpy(u0, lbs), ftn.FArray.from_numpy(u0, lbs)
+    in_new = ftn.jacobi(U, W, sweeps, coeff)
+    got = (W if in_new else U).to_numpy()
+    uo, wo = u0.copy(order="F"), u0.copy(order="F")
+    in_new_o = oracle.jacobi(OA(uo, lbs), OA(wo, lbs), sweeps, coeff)
+    assert in_new == in_new_o
+    return got, (wo if in_new_o else uo)
+
+
+@pytest.mark.parametrize("shape", [(3, 3), (3, 40), (40, 3), (4, 5), (129, 31), (130, 62), (131, 100),
+                                   (257, 65), (300, 301), (1000, 77)])
+@pytest.mark.parametrize("sweeps", [1, 2, 5])
+def test_2d_vs_oracle(ftn, shape, sweeps):
+    u0 = synth.jacobi_init(shape, array_id=sum(shape))
+    got, ref = _run_both(ftn, u0, sweeps, C2, [0, -7])
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("shape", [(3, 3, 3), (5, 4, 3), (40, 3, 9), (3, 40, 9), (130, 18, 7), (131, 19, 11),
+                                   (64, 64, 64), (257, 35, 20), (100, 33, 41)])
+@pytest.mark.parametrize("sweeps", [1, 3])
+def test_3d_vs_oracle(ftn, shape, sweeps):
+    u0 = synth.jacobi_init(shape, array_id=sum(shape))
+    got, ref = _run_both(ftn, u0, sweeps, C3, [1, 1, 1])
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_every_extent_2d(ftn):
+    """Each extent in [3, 40] in each dimension (strip / chunk / halo remainders)."""
+    for n in range(3, 41):
+        for shape in ((n, 37), (37, n)):
+            u0 = synth.jacobi_init(shape, array_id=n)
+            got, ref = _run_both(ftn, u0, 2, C2)
+            np.testing.assert_array_equal(got, ref, err_msg=str(shape))
+
+
+def test_harmonic_fixed_points(ftn):
+    i, j = np.meshgrid(np.arange(200.0), np.arange(150.0), indexing="ij")
+    for f in (i + 2 * j, i * j, i * i - j * j):
+        u0 = np.asfortranarray(f)
+        got, _ = _run_both(ftn, u0, 4, C2)
+        np.testing.assert_array_equal(got, u0)
+    i, j, k = np.meshgrid(np.arange(140.0), np.arange(20.0), np.arange(12.0), indexing="ij")
+    u3 = np.asfortranarray(i + 2 * j + 3 * k)
+    got, _ = _run_both(ftn, u3, 3, C3)
+    np.testing.assert_array_equal(got, u3)
+
+
+def test_strided_generic_path(ftn):
+    """Sections (dim-1 stride 16 B, reversed dim 2) take the generic kernel; same bits."""
+    big = synth.jacobi_init((61, 50))
+    Bu, Bw = ftn.FArray.from_numpy(big), ftn.FArray.from_numpy(big)
+    su, sw = Bu.section((1, 61, 2), (50, 1, -1)), Bw.section((1, 61, 2), (50, 1, -1))
+    in_new = ftn.jacobi(su, sw, 3)
+    got = (sw if in_new else su).to_numpy()
+    ou, ow = big.copy(order="F"), big.copy(order="F")
+    so, sow = OA(ou).section((1, 61, 2), (50, 1, -1)), OA(ow).section((1, 61, 2), (50, 1, -1))
+    oracle.jacobi(so, sow, 3, C2)
+    np.testing.assert_array_equal(got, sow.to_numpy() if in_new else so.to_numpy())
+    b3 = synth.jacobi_init((20, 9, 8))
+    U3, W3 = ftn.FArray.from_numpy(b3), ftn.FArray.from_numpy(b3)
+    s3u, s3w = U3.section((20, 1, -1), (1, 9), (1, 8)), W3.section((20, 1, -1), (1, 9), (1, 8))
+    ftn.jacobi(s3u, s3w, 1)
+    o3u, o3w = b3.copy(order="F"), b3.copy(order="F")
+    oracle.jacobi(OA(o3u).section((20, 1, -1), (1, 9, 1), (1, 8, 1)), OA(o3w).section((20, 1, -1), (1, 9, 1), (1, 8, 1)),
+                  1, C3)
+    np.testing.assert_array_equal(s3w.to_numpy(), OA(o3w).section((20, 1, -1), (1, 9, 1), (1, 8, 1)).to_numpy())
+
+
+def test_zero_sweeps_and_errors(ftn):
+    u0 = synth.jacobi_init((10, 10))
+    U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+    assert ftn.jacobi(U, W, 0) is False
+    np.testing.assert_array_equal(U.to_numpy(), u0)
+    with pytest.raises(ftn.FtnError):
+        ftn.jacobi(U, ftn.FArray.empty((10, 11)), 1)
+    with pytest.raises(ftn.FtnError):
+        ftn.jacobi(U, U, 1)
+
+
+@pytest.mark.slow
+def test_c2_full_size_sampled(ftn):
+    """C2 at full size (8192^2, 100 sweeps, the bench's launch configuration): every sampled
+    output point is recomputed by the oracle on its dependence cone (a 203x203 window, which
+    the 100 sweeps cannot see past), bit-exact; plus a full-size harmonic field."""
+    n, sweeps = 8192, 100
+    U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+    ftn.gen_fill(U, synth.SEED, 0, ftn.GEN_U01)
+    for face in ((1, n), (1, 1)), ((1, n), (n, n)), ((1, 1), (1, n)), ((n, n), (1, n)):
+        ftn.fill(U.section(*face), 0.0)
+    ftn.fill(U.section((1, n), (1, 1)), 1.0)
+    ftn.assign(W, U)
+    u_host = U.to_numpy()
+    in_new = ftn.jacobi(U, W, sweeps)
+    res = (W if in_new else U)
+    rng = np.random.default_rng(0)
+    pts = [(1, 1), (n - 2, n - 2), (0, 5), (4000, 1), (1, 4000)] + [tuple(int(v) for v in rng.integers(0, n, 2))
+                                                                      for _ in range(10)]
+    R = sweeps + 1
+    for (i, j) in pts:
+        i0, i1 = max(0, i - R), min(n, i + R + 1)
+        j0, j1 = max(0, j - R), min(n, j + R + 1)
+        win = np.asfortranarray(u_host[i0:i1, j0:j1])
+        a, b = win.copy(order="F"), win.copy(order="F")
+        new = oracle.jacobi(OA(a), OA(b), sweeps, C2)
+        ref = (b if new else a)[i - i0, j - j0]
+        got = res.section((i + 1, i + 1), (j + 1, j + 1)).to_numpy()[0, 0]
+        assert got == ref, (i, j)
