@@ -1,0 +1,466 @@
+"""Benchmark of the Fortran array path of arXiv 2409.18824 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--rows all|none|...] [--impl reference]
+
+Headline (BASELINE.json configs[1]): the 2-D 5-point Jacobi of real(8) 8192^2, one step =
+100 sweeps (ftn_jacobi); value = GLUPS = interior points x sweeps / time.  With N > 1
+(torchrun) every rank owns an 8192 x 8192 slab of an 8192 x (8192 N) grid and exchanges one
+halo column per sweep over NCCL (ftn_jacobi_dist): weak scaling.
+
+"rows" reports every other SURVEY §8 row on its BASELINE config, each with a roofline
+fraction: C4 element-wise / reductions (GB/s), C3 MATMUL (TFLOP/s), C5 3-D Jacobi (GLUPS),
+and the paper's Table III shapes.  Inputs are synthetic (splitmix64, seed 18824) and
+generated on the device by ftn_gen_fill; every working set is larger than the 126 MB L2.
+
+--impl reference times the oracle (oracle/, plain C) on the host cores on a bounded sample
+of the same workload (there is no reference code base for this paper).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 18824
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0          # GB/s, B200_PROFILING.md fallback
+FP64_PEAK_TFLOPS = 148 * 1.965 * 128 / 1000.0   # 37.2: SMs x max clock x DMMA FLOP/clk/SM (probe: 37.1 measured)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed regions."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.active = False
+        self.lock = threading.Lock()
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            with self.lock:
+                if self.active:
+                    self.samples.append(parts)
+
+    def timing(self, on: bool):
+        with self.lock:
+            self.active = on
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        with self.lock:
+            s = list(self.samples)
+        if not s:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(float(x[0]) for x in s if x[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for x in s for k in range(4) if x[2 + k].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": float(s[0][1]), "reasons": reasons,
+                "samples": len(s)}
+
+
+# ----------------------------------------------------------------------------------- timing helpers
+def timed(torch, fn, steps, warmup, clocks=None, dist=None):
+    """W untimed runs, then `steps` runs bracketed by barrier + synchronize; CUDA events on the
+    current stream.  Returns seconds for all steps (max over ranks)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.timing(True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.timing(False)
+    t = a.elapsed_time(b) / 1e3
+    if dist is not None:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        dist.barrier()
+    return t
+
+
+def jacobi_faces(ftn, U, n1, n2):
+    """synth.jacobi_init recipe on the device: interior U[0,1), j=1 face 1.0, other faces 0."""
+    ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
+    for tr in (((1, n1), (n2, n2)), ((1, 1), (1, n2)), ((n1, n1), (1, n2))):
+        ftn.fill(U.section(*tr), 0.0)
+    ftn.fill(U.section((1, n1), (1, 1)), 1.0)
+
+
+# ----------------------------------------------------------------------------------- headline
+def bench_jacobi2d(torch, ftn, args, ctx):
+    n, sweeps = 8192, 100
+    N, rank = ctx["world"], ctx["rank"]
+    if N == 1:
+        U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+        jacobi_faces(ftn, U, n, n)
+        ftn.assign(W, U)
+        step = lambda: ftn.jacobi(U, W, sweeps)  # noqa: E731
+        interior = (n - 2) * (n - 2)
+    else:
+        # weak scaling: global grid 8192 x (8192 N + 2); this rank owns planes [1 + r n, (r+1) n]
+        nl = n + 2
+        U, W = ftn.FArray.empty((n, nl)), ftn.FArray.empty((n, nl))
+        ftn.gen_fill(U, SEED, 1 + rank, ftn.GEN_U01)
+        ftn.fill(U.section((1, 1), (1, nl)), 0.0)
+        ftn.fill(U.section((n, n), (1, nl)), 0.0)
+        if rank == 0:
+            ftn.fill(U.section((1, n), (1, 1)), 1.0)
+        if rank == N - 1:
+            ftn.fill(U.section((1, n), (nl, nl)), 0.0)
+        ftn.assign(W, U)
+        comm = ctx["comm"]
+        step = lambda: comm.jacobi(U, W, sweeps)  # noqa: E731
+        interior = (n - 2) * n * N
+    l0 = ftn.launch_count()
+    t = timed(torch, step, args.steps, args.warmup, ctx["clocks"], ctx["dist"])
+    launches = ftn.launch_count() - l0 - args.warmup * (sweeps + (0 if N == 1 else sweeps))
+    glups = interior * sweeps * args.steps / t / 1e9
+    per_launch_bytes = 16 * (n - 2) * (n - 2 if N == 1 else n)       # algorithmic: read u once, write unew once
+    achieved = per_launch_bytes * sweeps * args.steps / t / 1e9      # GB/s, launches back to back
+    res = {"value": glups, "ms_per_step": t / args.steps * 1e3, "launches": launches,
+           "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes}
+    # ---- e2e: through the C ABI from pinned host buffers (H2D of u, D2H of the result inside)
+    if N == 1:
+        # pinned host buffers with the Fortran (column-major) layout: the copies are plain DMAs
+        host_u = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
+        host_u.copy_(U.tensor)
+        host_out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
+        U2, W2 = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+
+        def e2e_step():
+            U2.tensor.copy_(host_u, non_blocking=True)
+            ftn.assign(W2, U2)
+            new = ftn.jacobi(U2, W2, sweeps)
+            host_out.copy_((W2 if new else U2).tensor, non_blocking=True)
+
+        te = timed(torch, e2e_step, max(3, args.steps // 2), 1, None, None)
+        res["e2e"] = {"value": interior * sweeps * max(3, args.steps // 2) / te / 1e9, "unit": "GLUPS",
+                      "h2d_bytes_per_step": host_u.numel() * 8, "d2h_bytes_per_step": host_out.numel() * 8}
+        del host_u, host_out, U2, W2
+    del U, W
+    torch.cuda.empty_cache()
+    return res
+
+
+# ----------------------------------------------------------------------------------- §8 rows
+def bench_rows(torch, ftn, args, ctx, hbm_peak):
+    rows = {}
+    N, rank = ctx["world"], ctx["rank"]
+    steps, warm = max(3, args.steps // 2), 2
+    dist = ctx["dist"]
+    comm = ctx.get("comm")
+
+    def gbs_row(name, nbytes, fn, units=None):
+        t = timed(torch, fn, steps, warm, None, dist)
+        gbs = nbytes * N * steps / t / 1e9
+        rows[name] = {"value": gbs, "unit": "GB/s", "ms": t / steps * 1e3,
+                      "roofline": {"bound": "hbm", "frac": gbs / N / hbm_peak}}
+
+    # C4: 1024^3 arrays x(-511:512, 0:1023, 1:1024); at N>1 slabs of 1024/N planes (strong scaling)
+    if "c4" in args.rows:
+        nk = 1024 // N
+        shape = (1024, 1024, nk)
+        lbs = [-511, 0, 1 + rank * nk]
+        arrs = [ftn.FArray.empty(shape, lbounds=lbs) for _ in range(4)]
+        for k, a in enumerate(arrs):
+            ftn.gen_fill(a, SEED, 10 + k, ftn.GEN_U01)
+        b, c, d, r = arrs
+        n_el = 1024 * 1024 * nk
+        gbs_row("c4_muladd_r=b*c+d", 32 * n_el, lambda: ftn.muladd(r, b, c, d))
+        out = torch.empty((), dtype=torch.float64, device="cuda")
+        if N == 1:
+            gbs_row("c4_sum", 8 * n_el, lambda: ftn.sum(b, out))
+            gbs_row("c4_maxval", 8 * n_el, lambda: ftn.maxval(b, out))
+            gbs_row("c4_minval", 8 * n_el, lambda: ftn.minval(b, out))
+            fx = ftn.FArray(b.tensor.permute(2, 1, 0).reshape(-1))
+            fy = ftn.FArray(c.tensor.permute(2, 1, 0).reshape(-1))
+            gbs_row("c4_dot_product", 16 * n_el, lambda: ftn.dot_product(fx, fy, out))
+        else:
+            gbs_row("c4_sum_global", 8 * n_el, lambda: comm.sum(b, out))
+            gbs_row("c4_maxval_global", 8 * n_el, lambda: comm.maxval(b, out))
+            fx = ftn.FArray(b.tensor.permute(2, 1, 0).reshape(-1))
+            fy = ftn.FArray(c.tensor.permute(2, 1, 0).reshape(-1))
+            gbs_row("c4_dot_product_global", 16 * n_el, lambda: comm.dot_product(fx, fy, out))
+        del arrs, b, c, d, r, fx, fy
+        torch.cuda.empty_cache()
+        # section variant: parents (1:1024,1:1024,1:2048/N), sections (:,:,1::2)
+        parents = [ftn.FArray.empty((1024, 1024, 2 * nk)) for _ in range(4)]
+        for k, p in enumerate(parents):
+            ftn.gen_fill(p, SEED, 20 + k, ftn.GEN_U01)
+        secs = [p.section((1, 1024), (1, 1024), (1, 2 * nk, 2)) for p in parents]
+        gbs_row("c4_section_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2]))
+        if N == 1:
+            gbs_row("c4_section_sum", 8 * n_el, lambda: ftn.sum(secs[0], out))
+        del parents, secs
+        torch.cuda.empty_cache()
+
+    # C3: MATMUL 8192^3, column blocks of b and c over the ranks (a replicated)
+    if "c3" in args.rows:
+        n = 8192
+        nc = n // N
+        A = ftn.FArray.empty((n, n))
+        B = ftn.FArray.empty((n, nc))
+        C = ftn.FArray.empty((n, nc))
+        ftn.gen_fill(A, SEED, 1, ftn.GEN_U11)
+        ftn.gen_fill(B, SEED, 2 + rank, ftn.GEN_U11)
+        fn = (lambda: ftn.matmul(C, A, B)) if N == 1 else (lambda: comm.matmul(C, A, B))
+        t = timed(torch, fn, steps, warm, ctx["clocks"], dist)
+        tf = 2.0 * n * n * n * steps / t / 1e12
+        rows["c3_matmul_8192"] = {"value": tf, "unit": "TFLOP/s", "ms": t / steps * 1e3,
+                                  "roofline": {"bound": "fp64 tensor (DMMA)", "frac": tf / N / FP64_PEAK_TFLOPS,
+                                               "peak": FP64_PEAK_TFLOPS}}
+        if N == 1:
+            Ac, Bc = A.tensor, B.tensor
+            tc = timed(torch, lambda: torch.matmul(Ac, Bc), 3, 1, None, None)
+            rows["c3_matmul_8192"]["cublas_dgemm_tflops_context"] = 2.0 * n ** 3 * 3 / tc / 1e12
+        del A, B, C
+        torch.cuda.empty_cache()
+
+    # paper Table III shapes (1 GPU): transpose int32 32768^2, sum 32768^2, dot 2^27, matmul 4096^3
+    if "paper" in args.rows and N == 1:
+        n = 32768
+        a = ftn.FArray.empty((n, n), dtype=torch.int32)
+        ftn.gen_fill(a, SEED, 1, ftn.GEN_LINEAR)
+        r = ftn.FArray.empty((n, n), dtype=torch.int32)
+        gbs_row("paper_transpose_int32_32768", 8 * n * n, lambda: ftn.transpose(r, a))
+        del a, r
+        torch.cuda.empty_cache()
+        s = ftn.FArray.empty((n, n))
+        ftn.gen_fill(s, SEED, 2, ftn.GEN_U01)
+        out = torch.empty((), dtype=torch.float64, device="cuda")
+        gbs_row("paper_sum_32768", 8 * n * n, lambda: ftn.sum(s, out))
+        del s
+        torch.cuda.empty_cache()
+        m = 1 << 27
+        x, y = ftn.FArray.empty((m,)), ftn.FArray.empty((m,))
+        ftn.gen_fill(x, SEED, 3, ftn.GEN_U11)
+        ftn.gen_fill(y, SEED, 4, ftn.GEN_U11)
+        gbs_row("paper_dot_2^27", 16 * m, lambda: ftn.dot_product(x, y, out))
+        del x, y
+        k = 4096
+        A, B, C = (ftn.FArray.empty((k, k)) for _ in range(3))
+        ftn.gen_fill(A, SEED, 5, ftn.GEN_U11)
+        ftn.gen_fill(B, SEED, 6, ftn.GEN_U11)
+        t = timed(torch, lambda: ftn.matmul(C, A, B), steps, warm, None, None)
+        tf = 2.0 * k ** 3 * steps / t / 1e12
+        rows["paper_matmul_4096"] = {"value": tf, "unit": "TFLOP/s", "ms": t / steps * 1e3,
+                                     "roofline": {"bound": "fp64 tensor (DMMA)", "frac": tf / FP64_PEAK_TFLOPS}}
+        del A, B, C
+        torch.cuda.empty_cache()
+
+    # C5: 3-D 7-point Jacobi 2048^3 (slabs of 2048/N planes + halos at N > 1), 10 sweeps per step
+    if "c5" in args.rows:
+        n, sweeps = 2048, 10
+        free = torch.cuda.mem_get_info()[0]
+        if N == 1:
+            need = 2 * n ** 3 * 8
+            if free > need + (2 << 30):
+                U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
+                ftn.gen_fill(U, SEED, 7, ftn.GEN_U01)
+                ftn.assign(W, U)
+                t = timed(torch, lambda: ftn.jacobi(U, W, sweeps), max(2, steps // 2), 1, ctx["clocks"], dist)
+                interior = (n - 2) ** 3
+                del U, W
+            else:
+                t, interior = None, 0
+        else:
+            from paper_2409_18824_b200 import dist as D
+            g0, nl = D.jacobi_slab(n, N, rank)
+            U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
+            ftn.gen_fill(U, SEED, 7 + rank, ftn.GEN_U01)
+            ftn.assign(W, U)
+            t = timed(torch, lambda: comm.jacobi(U, W, sweeps), max(2, steps // 2), 1, ctx["clocks"], dist)
+            interior = (n - 2) ** 3
+            del U, W
+        torch.cuda.empty_cache()
+        if t:
+            ns = max(2, steps // 2)
+            gl = interior * sweeps * ns / t / 1e9
+            rows["c5_jacobi3d_2048"] = {"value": gl, "unit": "GLUPS", "ms_per_sweep": t / ns / sweeps * 1e3,
+                                        "roofline": {"bound": "hbm", "frac": gl * 16 / N / hbm_peak}}
+    return rows
+
+
+# ----------------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_jacobi(budget_s=12.0, max_sweeps=100):
+    """The oracle's Jacobi (oracle/ftn_oracle.c, OpenMP over independent rows) on the full 8192^2
+    grid of the headline workload, for as many sweeps as fit the budget."""
+    import numpy as np
+    import oracle
+    import synth
+    n = 8192
+    u = synth.jacobi_init((n, n))
+    w = u.copy(order="F")
+    U, Wd = oracle.FArray(u), oracle.FArray(w)
+    t0 = time.perf_counter()
+    oracle.jacobi(U, Wd, 1, 0.25)
+    t1 = time.perf_counter() - t0
+    sweeps = int(max(1, min(max_sweeps, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.jacobi(U, Wd, sweeps, 0.25)
+    t = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    threads = int(os.environ.get("OMP_NUM_THREADS", cores))
+    del u, w, np
+    return {"value": (n - 2) ** 2 * sweeps / t / 1e9, "unit": "GLUPS", "cores": threads, "kind": "oracle",
+            "sample": f"full 8192^2 grid, {sweeps} of the 100 sweeps ({t:.1f} s), OpenMP over rows"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores (no reference code base exists)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import synth
+    n = 8192
+    u = synth.jacobi_init((n, n))
+    w = u.copy(order="F")
+    U, Wd = oracle.FArray(u), oracle.FArray(w)
+    for _ in range(args.warmup):
+        oracle.jacobi(U, Wd, 1, 0.25)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.jacobi(U, Wd, 1, 0.25)      # each step: a bounded sample = 1 of the 100 sweeps
+    t = time.perf_counter() - t0
+    glups = (n - 2) ** 2 * args.steps / t / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    cpu = {"value": glups, "unit": "GLUPS", "cores": cores, "kind": "oracle",
+           "sample": "1 sweep of the 8192^2 grid per step (the workload is 100 sweeps)"}
+    line = {"impl": "reference", "metric": METRIC, "value": glups, "unit": "GLUPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": CONFIG, "cpu_baseline": cpu,
+            "e2e": {"value": glups, "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    del np
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "Jacobi GLUPS (2-D 5-point, real(8) 8192^2, 100 sweeps per step)"
+CONFIG = {"workload": "BASELINE configs[1]: 2-D 5-point Jacobi stencil, real(8) 8192x8192, 100 sweeps",
+          "l2": "working set 2 x 512 MiB > 126 MB L2 (no flush needed)", "seed": SEED}
+
+
+def traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "jacobi2d_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
+    ap.add_argument("--rows", default="c4,c3,paper,c5", help="comma list of extra rows, or 'none'")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.rows = [] if args.rows == "none" else args.rows.split(",")
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    ctx = {"world": world, "rank": rank, "dist": None}
+    from paper_2409_18824_b200 import ftn
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ctx["dist"] = dist
+        ctx["comm"] = ftn.Comm.from_torch_distributed(local)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx["clocks"] = clocks
+    hbm_peak, peak_src = load_peaks()
+
+    head = bench_jacobi2d(torch, ftn, args, ctx)
+    rows = bench_rows(torch, ftn, args, ctx, hbm_peak) if args.rows else {}
+    clk = clocks.stop()
+
+    if rank == 0:
+        cpu = None if args.no_cpu or world > 1 else cpu_oracle_jacobi()
+        frac = head["achieved_gbs"] / world / hbm_peak
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(CONFIG, parallelism=f"slab{world}" if world > 1 else "1 GPU",
+                           global_grid=f"8192x{8192 * world + (2 if world > 1 else 0)}"),
+            "e2e": head.get("e2e"),
+            "gpu_launches": head["launches"],
+            "roofline": {"bound": "hbm", "kernel": "jacobi2d_tma", "achieved": head["achieved_gbs"] / world,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": frac, "peak_source": peak_src,
+                         "traffic": traffic_from_profiles(),
+                         "algorithmic_bytes_per_launch": head["per_launch_bytes"],
+                         "note": "16 B per interior point per sweep; time = all launches of the timed region"},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "rows": rows,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        ctx["comm"].destroy()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

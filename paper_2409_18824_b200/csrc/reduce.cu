@@ -44,11 +44,19 @@ __device__ __forceinline__ typename Acc<T>::type neutral() {
   if constexpr (KIND == RK_SUM || KIND == RK_DOT) {
     return A(0);
   } else if constexpr (std::is_floating_point<T>::value) {
-    return KIND == RK_MAX ? -INFINITY : INFINITY;
+    return NAN;  // maxNum/minNum ignore NaN: an all-NaN (or empty) combine stays NaN (R#11)
   } else {
     if constexpr (sizeof(T) == 4) return (A)(KIND == RK_MAX ? INT32_MIN : INT32_MAX);
     else return (A)(KIND == RK_MAX ? INT64_MIN : INT64_MAX);
   }
+}
+
+// MAXVAL / MINVAL of an empty array: -inf / +inf (R#10)
+template <typename T, int KIND>
+__device__ __forceinline__ typename Acc<T>::type empty_value() {
+  if constexpr (std::is_floating_point<T>::value && (KIND == RK_MAX || KIND == RK_MIN))
+    return KIND == RK_MAX ? -INFINITY : INFINITY;
+  return neutral<T, KIND>();
 }
 
 template <typename T, int KIND>
@@ -210,7 +218,9 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
   if (tau == 0) {
     const A b01 = combine<T, KIND>(wv[0], wv[1]), b23 = combine<T, KIND>(wv[2], wv[3]);
     const A b45 = combine<T, KIND>(wv[4], wv[5]), b67 = combine<T, KIND>(wv[6], wv[7]);
-    reinterpret_cast<A*>(out)[c] = combine<T, KIND>(combine<T, KIND>(b01, b23), combine<T, KIND>(b45, b67));
+    A r = combine<T, KIND>(combine<T, KIND>(b01, b23), combine<T, KIND>(b45, b67));
+    if (p.n == 0) r = empty_value<T, KIND>();
+    reinterpret_cast<A*>(out)[c] = r;
   }
 }
 

@@ -13,10 +13,10 @@
 // (cp.async.bulk.tensor + mbarrier pipeline, one producer warp), so every u value
 // is read from HBM once per sweep and reused from shared memory by its 4 (6)
 // neighbours.
-//   2-D: strips 128 columns wide; stages of {130 x 32} rows (30 output rows, 1-row
+//   2-D: strips 128 columns wide; stages of {132 x 32} rows (30 output rows, 1-row
 //        halo each side), 3 stages.
 //   3-D: columns of 128 x 16 points streamed along k; a ring of 5 planes
-//        {130 x 18}, outputs for plane k once plane k+1 has landed.
+//        {132 x 18}, outputs for plane k once plane k+1 has landed.
 // Work is split evenly over a persistent grid (2 CTAs per SM) in row (plane)
 // units, so every CTA moves the same number of bytes.
 #include "ftn_internal.cuh"
@@ -28,11 +28,15 @@ namespace {
 
 // ---------------------------------------------------------------- 2-D
 constexpr int S2_W = 128;              // interior columns per strip
-constexpr int S2_BOXW = S2_W + 2;      // 130
+// The box starts 2 columns left of the strip: TMA needs the dim-0 start of a box
+// 16-byte aligned (an odd fp64 coordinate such as -1 raises "illegal instruction",
+// tools/microbench/tma_probe.cu), so the halo column i0-1 comes with i0-2.
+constexpr int S2_BOXW = S2_W + 4;      // 132: columns i0-2 .. i0+129
+constexpr int S2_X0 = 2;               // smem column of i0
 constexpr int S2_R = 30;               // output rows per stage
 constexpr int S2_BOXH = S2_R + 2;      // 32
 constexpr int S2_STAGES = 3;
-constexpr int S2_STAGE_BYTES = S2_BOXW * S2_BOXH * 8;  // 33280
+constexpr int S2_STAGE_BYTES = S2_BOXW * S2_BOXH * 8;  // 33792
 constexpr int S2_CONS_WARPS = S2_W / 32;               // 4
 constexpr int S2_THREADS = (S2_CONS_WARPS + 1) * 32;
 constexpr int S2_SMEM = S2_STAGES * S2_STAGE_BYTES + 128 + 64;
@@ -91,13 +95,17 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
       ChunkIter2 it{L0, L1, p.nrows, p.lo};
       int64_t strip, j0;
       int cnt;
-      for (int k = 0; it.next(strip, j0, cnt); ++k) {
+      int k = 0;
+      for (; it.next(strip, j0, cnt); ++k) {
         const int s = k % S2_STAGES;
         if (k >= S2_STAGES) dev::mbar_wait(&empty[s], ((k / S2_STAGES) - 1) & 1);
         dev::mbar_arrive_expect_tx(&full[s], S2_STAGE_BYTES);
-        dev::tma_load_2d(smem + s * S2_STAGE_BYTES, &src_map, &full[s], (int32_t)(strip * S2_W - 1),
+        dev::tma_load_2d(smem + s * S2_STAGE_BYTES, &src_map, &full[s], (int32_t)(strip * S2_W - S2_X0),
                          (int32_t)(j0 - 1));
       }
+      // producer tail: do not retire while loads are in flight / unconsumed
+      for (int kk = k - S2_STAGES > 0 ? k - S2_STAGES : 0; kk < k; ++kk)
+        dev::mbar_wait(&empty[kk % S2_STAGES], (kk / S2_STAGES) & 1);
     }
     return;
   }
@@ -113,13 +121,14 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
     const bool active = i >= 1 && i <= p.n1 - 2;
     dev::mbar_wait(&full[s], (k / S2_STAGES) & 1);
     const double* t = reinterpret_cast<const double*>(smem + s * S2_STAGE_BYTES);
-    // smem row r holds u(:, j0 - 1 + r); column x + 1 holds i
-    double up = t[x + 1], mid = t[S2_BOXW + x + 1];
+    // smem row r holds u(:, j0 - 1 + r); column x + 2 holds i
+    const int xc = x + S2_X0;
+    double up = t[xc], mid = t[S2_BOXW + xc];
     char* out = p.dst + i * p.d_sm1 + j0 * p.d_sm2;
     for (int r = 1; r <= cnt; ++r) {
       const double* row = t + r * S2_BOXW;
-      const double down = row[S2_BOXW + x + 1];
-      double v = row[x] + row[x + 2];
+      const double down = row[S2_BOXW + xc];
+      double v = row[xc - 1] + row[xc + 1];
       v = v + up;
       v = v + down;
       if (active) *reinterpret_cast<double*>(out) = c * v;
@@ -134,9 +143,9 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
 
 // ---------------------------------------------------------------- 3-D
 constexpr int S3_W = 128, S3_H = 16;
-constexpr int S3_BOXW = S3_W + 2, S3_BOXH = S3_H + 2;  // 130 x 18
+constexpr int S3_BOXW = S3_W + 4, S3_BOXH = S3_H + 2;  // 132 x 18 (dim-0 start 16-byte aligned, see S2_BOXW)
 constexpr int S3_STAGES = 5;
-constexpr int S3_PLANE_BYTES = S3_BOXW * S3_BOXH * 8;  // 18720 (TMA transaction bytes)
+constexpr int S3_PLANE_BYTES = S3_BOXW * S3_BOXH * 8;  // 19008 (TMA transaction bytes)
 constexpr int S3_PLANE_STRIDE = (S3_PLANE_BYTES + 127) / 128 * 128;  // 128-byte aligned stages
 constexpr int S3_ROWS_PER_THREAD = 8;
 constexpr int S3_CONS_THREADS = S3_W * S3_H / S3_ROWS_PER_THREAD;  // 256
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
       int64_t col, k0, n;
       int64_t gp = 0;  // global plane counter of this CTA
       while (it.next(col, k0, n)) {
-        const int32_t ci = (int32_t)((col % p.tiles_i) * S3_W - 1);
+        const int32_t ci = (int32_t)((col % p.tiles_i) * S3_W - 2);
         const int32_t cj = (int32_t)((col / p.tiles_i) * S3_H - 1);
         for (int64_t kk = k0 - 1; kk <= k0 + n; ++kk, ++gp) {
           const int s = (int)(gp % S3_STAGES);
@@ -204,6 +213,8 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
           dev::tma_load_3d(smem + s * S3_PLANE_STRIDE, &src_map, &full[s], ci, cj, (int32_t)kk);
         }
       }
+      for (int64_t q = gp - S3_STAGES > 0 ? gp - S3_STAGES : 0; q < gp; ++q)   // producer tail
+        dev::mbar_wait(&empty[q % S3_STAGES], (uint32_t)((q / S3_STAGES) & 1));
     }
     return;
   }
@@ -229,18 +240,19 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
       const double* Pp = reinterpret_cast<const double*>(smem + (pn % S3_STAGES) * S3_PLANE_STRIDE);
       const int64_t k = k0 + q;
       const int r0 = yb * S3_ROWS_PER_THREAD + 1;  // smem row of the first j
-      double jm = P0[(r0 - 1) * S3_BOXW + x + 1];
-      double jc = P0[r0 * S3_BOXW + x + 1];
+      const int xc = x + 2;  // smem column of i
+      double jm = P0[(r0 - 1) * S3_BOXW + xc];
+      double jc = P0[r0 * S3_BOXW + xc];
       char* out = p.dst + i * p.d_sm1 + jbase * p.d_sm2 + k * p.d_sm3;
 #pragma unroll
       for (int jj = 0; jj < S3_ROWS_PER_THREAD; ++jj) {
         const int r = r0 + jj;
-        const double jp = P0[(r + 1) * S3_BOXW + x + 1];
-        double v = P0[r * S3_BOXW + x] + P0[r * S3_BOXW + x + 2];
+        const double jp = P0[(r + 1) * S3_BOXW + xc];
+        double v = P0[r * S3_BOXW + xc - 1] + P0[r * S3_BOXW + xc + 1];
         v = v + jm;
         v = v + jp;
-        v = v + Pm[r * S3_BOXW + x + 1];
-        v = v + Pp[r * S3_BOXW + x + 1];
+        v = v + Pm[r * S3_BOXW + xc];
+        v = v + Pp[r * S3_BOXW + xc];
         const int64_t j = jbase + jj;
         if (iact && j >= 1 && j <= p.n2 - 2) *reinterpret_cast<double*>(out) = c * v;
         out += p.d_sm2;

@@ -225,7 +225,9 @@ class FArray:
         st = self.tensor.untyped_storage()
         el = self.desc.elem_len
         base = self.tensor.data_ptr() - self.tensor.storage_offset() * el
-        off = self.desc.base_addr - base
+        off = (self.desc.base_addr or 0) - base
+        if self.size() == 0:
+            return torch.empty(self.shape, dtype=self.dtype, device=self.tensor.device)
         if off % el or any(s < 0 or s % el for s in self.strides):
             raise ValueError("view_tensor needs positive element-aligned strides")
         t = torch.empty(0, dtype=self.dtype, device=self.tensor.device)
