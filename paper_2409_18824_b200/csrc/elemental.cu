@@ -21,8 +21,8 @@ namespace {
 
 constexpr int EW_THREADS = 256;
 constexpr int EW_GROUP = 4;
-constexpr int EW_GROUPS_PER_THREAD = 2;
-constexpr int64_t EW_CHUNK = (int64_t)EW_THREADS * EW_GROUP * EW_GROUPS_PER_THREAD;  // 2048
+constexpr int EW_GROUPS_PER_THREAD = 1;  // + 6 CTAs/SM (<= 40 registers): 1536 threads x 96 B in flight per SM
+constexpr int64_t EW_CHUNK = (int64_t)EW_THREADS * EW_GROUP * EW_GROUPS_PER_THREAD;  // 1024
 
 enum { OP_COPY = 0, OP_GEN = 9 };
 enum { SC_NONE = 0, SC_DEVICE = 1, SC_VALUE = 2 };
@@ -140,9 +140,9 @@ __device__ __forceinline__ T load_scalar(const EwParams& p, int a) {
 }
 
 // One work item = EW_CHUNK consecutive elements of one merged "row" (dim 0).
-// Thread tau handles the groups at offsets g*1024 + 4*tau (g = 0, 1).
+// Thread tau handles the group at offset 4*tau.
 template <typename T, int OP, bool CONTRACT, bool VEC, int NOPS>
-__global__ void __launch_bounds__(EW_THREADS) ew_kernel(const __grid_constant__ EwParams p) {
+__global__ void __launch_bounds__(EW_THREADS, 6) ew_kernel(const __grid_constant__ EwParams p) {
   const int64_t G = gridDim.x;
   int64_t c = blockIdx.x % p.nchunk0;
   int64_t r = blockIdx.x / p.nchunk0;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(EW_THREADS) ew_kernel(const __grid_constant__ 
 template <typename T, int OP, bool CONTRACT, int NOPS>
 ftn_status_t launch_t(const EwParams& p, bool vec, cudaStream_t stream) {
   if (p.items == 0) return FTN_OK;
-  const int64_t max_blocks = (int64_t)num_sms() * (2048 / EW_THREADS) * 4;
+  const int64_t max_blocks = (int64_t)num_sms() * (2048 / EW_THREADS) * 8;
   const int blocks = (int)(p.items < max_blocks ? p.items : max_blocks);
   if (vec)
     ew_kernel<T, OP, CONTRACT, true, NOPS><<<blocks, EW_THREADS, 0, stream>>>(p);

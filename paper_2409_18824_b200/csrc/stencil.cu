@@ -46,27 +46,33 @@ struct J2Params {
   int64_t d_sm1, d_sm2;
   int64_t n1, n2;
   int64_t tiles_i;  // strips
-  int64_t nrows;    // interior rows n2 - 2
-  int64_t total;    // tiles_i * nrows
-  int64_t per_cta;
+  int64_t nrows;    // rows to update
+  int64_t seg;      // rows per work unit
+  int64_t units;    // tiles_i * ceil(nrows / seg)
   int64_t lo;       // first output row (0-based position in dim 2)
   double coeff;
 };
 
-// Iterate this CTA's chunks: (strip, first output row, row count)
+// Work units u = strip + tiles_i * segment (strip fastest), taken round-robin by the
+// CTAs: units of one wave are neighbouring strips over the same rows, so the halo
+// columns a CTA loads were just brought into L2 by its neighbours (no DRAM re-read).
+// Each unit is streamed in chunks of at most S2_R rows.
 struct ChunkIter2 {
-  int64_t L, Lend, nrows, lo;
-  __device__ bool next(int64_t& strip, int64_t& j0, int& cnt) {
-    if (L >= Lend) return false;
-    strip = L / nrows;
-    const int64_t r = L % nrows;
-    int64_t left_in_strip = nrows - r;
-    int64_t left = Lend - L;
-    int64_t n = left_in_strip < left ? left_in_strip : left;
-    if (n > S2_R) n = S2_R;
-    j0 = lo + r;  // 0-based row position
+  int64_t u, G, units, tiles, seg, nrows, lo;
+  int64_t strip = 0, r = 0, rend = 0;
+  __device__ bool next(int64_t& s_out, int64_t& j0, int& cnt) {
+    while (r >= rend) {
+      u += G;
+      if (u >= units) return false;
+      strip = u % tiles;
+      r = (u / tiles) * seg;
+      rend = min(r + seg, nrows);
+    }
+    const int64_t n = min((int64_t)S2_R, rend - r);
+    s_out = strip;
+    j0 = lo + r;
     cnt = (int)n;
-    L += n;
+    r += n;
     return true;
   }
 };
@@ -86,13 +92,13 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
     dev::fence_barrier_init();
   }
   __syncthreads();
-  const int64_t L0 = (int64_t)blockIdx.x * p.per_cta;
-  const int64_t L1 = min(L0 + p.per_cta, p.total);
+  const int64_t G = gridDim.x;
+  const ChunkIter2 it0{(int64_t)blockIdx.x - G, G, p.units, p.tiles_i, p.seg, p.nrows, p.lo};
 
   if (warp == S2_CONS_WARPS) {
     if (lane == 0) {
       dev::prefetch_tma(&src_map);
-      ChunkIter2 it{L0, L1, p.nrows, p.lo};
+      ChunkIter2 it = it0;
       int64_t strip, j0;
       int cnt;
       int k = 0;
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
   }
 
   const int x = threadIdx.x;  // column within the strip
-  ChunkIter2 it{L0, L1, p.nrows, p.lo};
+  ChunkIter2 it = it0;
   int64_t strip, j0;
   int cnt;
   const double c = p.coeff;
@@ -158,23 +164,24 @@ struct J3Params {
   int64_t d_sm1, d_sm2, d_sm3;
   int64_t n1, n2, n3;
   int64_t tiles_i, tiles_j;
-  int64_t nk;      // interior planes n3 - 2
-  int64_t total;   // tiles_i * tiles_j * nk
-  int64_t per_cta;
+  int64_t nk;      // planes to update
+  int64_t seg;     // planes per work unit
+  int64_t units;   // tiles_i * tiles_j * ceil(nk / seg)
   int64_t lo;      // first output plane
   double coeff;
 };
 
+// Work units u = column + ncols * segment (column = i-tile fastest, then j-tile), taken
+// round-robin: one wave streams neighbouring columns through the same planes together.
 struct SegIter3 {
-  int64_t L, Lend, nk, lo;
+  int64_t u, G, units, ncols, seg, nk, lo;
   __device__ bool next(int64_t& col, int64_t& k0, int64_t& n) {
-    if (L >= Lend) return false;
-    col = L / nk;
-    const int64_t r = L % nk;
-    const int64_t a = nk - r, b = Lend - L;
-    n = a < b ? a : b;
+    u += G;
+    if (u >= units) return false;
+    col = u % ncols;
+    const int64_t r = (u / ncols) * seg;
+    n = min(seg, nk - r);
     k0 = lo + r;
-    L += n;
     return true;
   }
 };
@@ -194,13 +201,13 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
     dev::fence_barrier_init();
   }
   __syncthreads();
-  const int64_t L0 = (int64_t)blockIdx.x * p.per_cta;
-  const int64_t L1 = min(L0 + p.per_cta, p.total);
+  const int64_t G = gridDim.x;
+  const SegIter3 it0{(int64_t)blockIdx.x - G, G, p.units, p.tiles_i * p.tiles_j, p.seg, p.nk, p.lo};
 
   if (warp == S3_CONS_WARPS) {
     if (lane == 0) {
       dev::prefetch_tma(&src_map);
-      SegIter3 it{L0, L1, p.nk, p.lo};
+      SegIter3 it = it0;
       int64_t col, k0, n;
       int64_t gp = 0;  // global plane counter of this CTA
       while (it.next(col, k0, n)) {
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
 
   const int x = threadIdx.x % S3_W;
   const int yb = threadIdx.x / S3_W;  // 0..1
-  SegIter3 it{L0, L1, p.nk, p.lo};
+  SegIter3 it = it0;
   int64_t col, k0, n;
   int64_t gp = 0;
   const double c = p.coeff;
@@ -311,6 +318,27 @@ __global__ void __launch_bounds__(256) jacobi_generic(const __grid_constant__ JG
   }
 }
 
+// Split `len` rows (planes) of each of `tiles` strips (columns) into segments so that the
+// units (tiles x segments) fill whole waves of `grid` CTAs: minimise
+//   wave-quantisation loss x re-read halo rows (2 per segment, they miss L2).
+void plan_units(int64_t tiles, int64_t len, int64_t grid, int64_t* seg, int64_t* units) {
+  double best = 1e30;
+  int64_t best_n = 1;
+  for (int64_t nseg = 1; nseg <= 256 && nseg <= len; ++nseg) {
+    const int64_t sl = (len + nseg - 1) / nseg;
+    const int64_t nseg_eff = (len + sl - 1) / sl;
+    const int64_t U = tiles * nseg_eff;
+    const int64_t waves = (U + grid - 1) / grid;
+    const double cost = (double)waves * grid / (double)U * (1.0 + 2.0 / (double)(sl + 2));
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_n = nseg;
+    }
+  }
+  *seg = (len + best_n - 1) / best_n;
+  *units = tiles * ((len + *seg - 1) / *seg);
+}
+
 bool stencil_tma_able(const ftn_desc_t* d) {
   if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
   for (int k = 1; k < d->rank; ++k)
@@ -357,12 +385,10 @@ ftn_status_t sweep(const ftn_desc_t* src, const ftn_desc_t* dst, const CUtensorM
       p.n2 = n2;
       p.tiles_i = (n1 + S2_W - 1) / S2_W;
       p.nrows = hi - lo + 1;
-      p.total = p.tiles_i * p.nrows;
       p.coeff = coeff;
       int64_t grid = (int64_t)sms * 2;
-      if (grid > p.total) grid = p.total;
-      p.per_cta = (p.total + grid - 1) / grid;
-      grid = (p.total + p.per_cta - 1) / p.per_cta;
+      plan_units(p.tiles_i, p.nrows, grid, &p.seg, &p.units);
+      if (grid > p.units) grid = p.units;
       p.lo = lo;
       jacobi2d_tma<<<(unsigned)grid, S2_THREADS, S2_SMEM, s>>>(*map, p);
       return after_launch("jacobi2d_tma");
@@ -378,12 +404,10 @@ ftn_status_t sweep(const ftn_desc_t* src, const ftn_desc_t* dst, const CUtensorM
       p.tiles_i = (n1 + S3_W - 1) / S3_W;
       p.tiles_j = (n2 + S3_H - 1) / S3_H;
       p.nk = hi - lo + 1;
-      p.total = p.tiles_i * p.tiles_j * p.nk;
       p.coeff = coeff;
       int64_t grid = (int64_t)sms * 2;
-      if (grid > p.total) grid = p.total;
-      p.per_cta = (p.total + grid - 1) / grid;
-      grid = (p.total + p.per_cta - 1) / p.per_cta;
+      plan_units(p.tiles_i * p.tiles_j, p.nk, grid, &p.seg, &p.units);
+      if (grid > p.units) grid = p.units;
       p.lo = lo;
       jacobi3d_tma<<<(unsigned)grid, S3_THREADS, S3_SMEM, s>>>(*map, p);
       return after_launch("jacobi3d_tma");

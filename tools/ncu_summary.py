@@ -1,0 +1,52 @@
+"""Summarise ncu outputs into profiles/ (tracked): per-kernel DRAM traffic vs algorithmic bytes,
+and the launch list's per-kernel share of device time.
+
+    python tools/ncu_summary.py full <rep.ncu-rep> > profiles/<name>.txt
+    python tools/ncu_summary.py launches <launches.csv> > profiles/<name>.txt
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+           "launch__grid_size", "launch__block_size", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum"]
+
+
+def full(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    print("kernel | " + " | ".join(f"{m} [{units[hdr.index(m)]}]" for m in METRICS if m in hdr))
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        print(name[:70] + " | " + " | ".join(d.get(m, "") for m in METRICS if m in hdr))
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[start]
+    ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[start + 1:]:
+        if len(r) <= mi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[mi].replace(",", "")) * scale.get(r[ui], 1.0)
+    tot = sum(a[1] for a in agg.values())
+    print(f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s} {'avg_us':>10s}")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{k[:70]:70s} {n:8d} {t:12.1f} {t / tot * 100:6.1f}% {t / n:10.2f}")
+
+
+if __name__ == "__main__":
+    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])

@@ -1,0 +1,72 @@
+"""Small, ncu-friendly invocations of each hot kernel (one call each after a warm-up call).
+
+    python tools/prof_case.py [jacobi2d,jacobi3d,muladd,sum,transpose,matmul|all]
+
+Working sets are larger than L2 but small enough for ncu's replay save/restore.
+"""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2409_18824_b200 import ftn  # noqa: E402
+
+SEED = 18824
+
+
+def main(which):
+    torch.cuda.set_device(0)
+    if "jacobi2d" in which:
+        n = 8192
+        U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+        ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
+        ftn.assign(W, U)
+        ftn.jacobi(U, W, 2)
+        ftn.jacobi(U, W, 1)
+        del U, W
+    if "jacobi3d" in which:
+        n = 512
+        U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
+        ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
+        ftn.assign(W, U)
+        ftn.jacobi(U, W, 2)
+        ftn.jacobi(U, W, 1)
+        del U, W
+    if "muladd" in which:
+        n = 1 << 27
+        b, c, d, r = (ftn.FArray.empty((n,)) for _ in range(4))
+        for k, a in enumerate((b, c, d)):
+            ftn.gen_fill(a, SEED, k, ftn.GEN_U01)
+        ftn.muladd(r, b, c, d)
+        ftn.muladd(r, b, c, d)
+        del b, c, d, r
+    if "sum" in which:
+        x = ftn.FArray.empty((1 << 28,))
+        ftn.gen_fill(x, SEED, 0, ftn.GEN_U01)
+        ftn.sum(x)
+        ftn.sum(x)
+        del x
+    if "transpose" in which:
+        n = 16384
+        a = ftn.FArray.empty((n, n), dtype=torch.int32)
+        r = ftn.FArray.empty((n, n), dtype=torch.int32)
+        ftn.gen_fill(a, SEED, 0, ftn.GEN_LINEAR)
+        ftn.transpose(r, a)
+        ftn.transpose(r, a)
+        del a, r
+    if "matmul" in which:
+        n = 4096
+        A, B, C = (ftn.FArray.empty((n, n)) for _ in range(3))
+        ftn.gen_fill(A, SEED, 1, ftn.GEN_U11)
+        ftn.gen_fill(B, SEED, 2, ftn.GEN_U11)
+        ftn.matmul(C, A, B)
+        ftn.matmul(C, A, B)
+    torch.cuda.synchronize()
+    print("ok", ftn.launch_count())
+
+
+if __name__ == "__main__":
+    arg = sys.argv[1] if len(sys.argv) > 1 else "all"
+    main(["jacobi2d", "jacobi3d", "muladd", "sum", "transpose", "matmul"] if arg == "all" else arg.split(","))
