@@ -4,31 +4,64 @@
 // int32 32768^2): the strided side of the access kills locality.  Here a
 // 64x64 tile is read with dim-1-contiguous (coalesced) loads into padded shared
 // memory and written back with dim-1-contiguous stores of the result, so both
-// HBM streams are sector-efficient.  Pure data movement: 2 * elem_len bytes per
-// element.
+// HBM streams are sector-efficient.  On full tiles of unit-stride, 16-byte
+// aligned operands every thread moves 16 bytes per global access (4 int32 or
+// 2 fp64); ragged edge tiles and strided sections take the element-wise path.
+// Pure data movement: 2 * elem_len bytes per element.
 #include "ftn_internal.cuh"
 
 namespace ftn {
 namespace {
 
 constexpr int TT = 64;           // tile edge
-constexpr int T_THREADS = 256;   // 64 x 4
+constexpr int T_THREADS = 256;
 
 struct TParams {
   KDesc dst, src;
   int64_t n1, n2;      // src extents
   int64_t tiles1, tiles;
+  int vec;             // operands allow 16-byte accesses
 };
 
 template <typename T>
 __global__ void __launch_bounds__(T_THREADS) transpose_kernel(const __grid_constant__ TParams p) {
+  constexpr int V = 16 / sizeof(T);       // elements per 16-byte vector
+  constexpr int GPR = TT / V;             // vector groups per tile row
   __shared__ T tile[TT][TT + 1];
-  const int tx = threadIdx.x & (TT - 1);
-  const int ty = threadIdx.x / TT;  // 0..3
+  const int tid = threadIdx.x;
   for (int64_t w = blockIdx.x; w < p.tiles; w += gridDim.x) {
     const int64_t i0 = (w % p.tiles1) * TT;
     const int64_t j0 = (w / p.tiles1) * TT;
-    // load src(i0 + tx, j0 + jj): coalesced along src dim 1
+    const bool full = p.vec && i0 + TT <= p.n1 && j0 + TT <= p.n2;
+    if (full) {
+      // load: tile[jj][ii..ii+V) = src(i0+ii.., j0+jj) with one 16-byte load
+#pragma unroll
+      for (int q = 0; q < TT * GPR / T_THREADS; ++q) {
+        const int g = tid + q * T_THREADS;
+        const int jj = g / GPR, ii = (g % GPR) * V;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.src.base + (i0 + ii) * (int64_t)sizeof(T) +
+                                                             (j0 + jj) * p.src.sm[1]));
+        const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) tile[jj][ii + k] = e[k];
+      }
+      __syncthreads();
+      // store: dst(j0+jj.., i0+ii) = tile[jj..jj+V)[ii] with one 16-byte store
+#pragma unroll
+      for (int q = 0; q < TT * GPR / T_THREADS; ++q) {
+        const int g = tid + q * T_THREADS;
+        const int ii = g / GPR, jj = (g % GPR) * V;
+        uint4 v;
+        T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) e[k] = tile[jj + k][ii];
+        *reinterpret_cast<uint4*>(p.dst.base + (j0 + jj) * (int64_t)sizeof(T) + (i0 + ii) * p.dst.sm[1]) = v;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int tx = tid & (TT - 1);
+    const int ty = tid / TT;  // 0..3
     const int64_t i = i0 + tx;
 #pragma unroll 4
     for (int jj = ty; jj < TT; jj += T_THREADS / TT) {
@@ -37,7 +70,6 @@ __global__ void __launch_bounds__(T_THREADS) transpose_kernel(const __grid_const
         tile[jj][tx] = *reinterpret_cast<const T*>(p.src.base + i * p.src.sm[0] + j * p.src.sm[1]);
     }
     __syncthreads();
-    // store dst(j0 + tx, i0 + ii) = src(i0 + ii, j0 + tx): coalesced along dst dim 1
     const int64_t j = j0 + tx;
 #pragma unroll 4
     for (int ii = ty; ii < TT; ii += T_THREADS / TT) {
@@ -57,6 +89,9 @@ ftn_status_t launch(const ftn_desc_t* dst, const ftn_desc_t* src, cudaStream_t s
   p.n2 = src->dim[1].extent;
   p.tiles1 = (p.n1 + TT - 1) / TT;
   p.tiles = p.tiles1 * ((p.n2 + TT - 1) / TT);
+  const int64_t el = src->elem_len;
+  p.vec = p.src.sm[0] == el && p.dst.sm[0] == el && ((uintptr_t)p.src.base % 16) == 0 &&
+          ((uintptr_t)p.dst.base % 16) == 0 && (p.src.sm[1] % 16) == 0 && (p.dst.sm[1] % 16) == 0;
   if (p.tiles == 0) return FTN_OK;
   const int64_t maxb = (int64_t)num_sms() * 8 * 16;
   const unsigned blocks = (unsigned)(p.tiles < maxb ? p.tiles : maxb);
