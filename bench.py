@@ -97,9 +97,13 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- timing helpers
-def timed(torch, fn, steps, warmup, clocks=None, dist=None):
+LAST_LAUNCHES = [0]
+
+
+def timed(torch, fn, steps, warmup, clocks=None, dist=None, counter=None):
     """W untimed runs, then `steps` runs bracketed by barrier + synchronize; CUDA events on the
-    current stream.  Returns seconds for all steps (max over ranks)."""
+    current stream.  Returns seconds for all steps (max over ranks); LAST_LAUNCHES[0] gets the
+    number of libftn kernel launches inside the timed region (when `counter` is given)."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -110,10 +114,12 @@ def timed(torch, fn, steps, warmup, clocks=None, dist=None):
     b = torch.cuda.Event(enable_timing=True)
     if clocks:
         clocks.timing(True)
+    c0 = counter() if counter else 0
     a.record()
     for _ in range(steps):
         fn()
     b.record()
+    LAST_LAUNCHES[0] = (counter() - c0) if counter else 0
     torch.cuda.synchronize()
     if clocks:
         clocks.timing(False)
@@ -159,14 +165,17 @@ def bench_jacobi2d(torch, ftn, args, ctx):
         comm = ctx["comm"]
         step = lambda: comm.jacobi(U, W, sweeps)  # noqa: E731
         interior = (n - 2) * n * N
-    l0 = ftn.launch_count()
-    t = timed(torch, step, args.steps, args.warmup, ctx["clocks"], ctx["dist"])
-    launches = ftn.launch_count() - l0 - args.warmup * (sweeps + (0 if N == 1 else sweeps))
+    t = timed(torch, step, args.steps, args.warmup, ctx["clocks"], ctx["dist"], counter=ftn.launch_count)
+    launches = LAST_LAUNCHES[0]
     glups = interior * sweeps * args.steps / t / 1e9
-    per_launch_bytes = 16 * (n - 2) * (n - 2 if N == 1 else n)       # algorithmic: read u once, write unew once
-    achieved = per_launch_bytes * sweeps * args.steps / t / 1e9      # GB/s, launches back to back
+    # launch plan of ftn_jacobi: F launches of T fused sweeps + S1 single sweeps per step
+    T, F, S1 = ftn.jacobi_launch_plan(sweeps) if N == 1 else (1, 0, sweeps)
+    per_launch_bytes = 16 * (n - 2) * (n - 2 if N == 1 else n)       # algorithmic: read u once, write once
+    stencil_launches = (F + S1) * args.steps
+    achieved = per_launch_bytes * stencil_launches / t / 1e9          # GB/s, launches back to back
     res = {"value": glups, "ms_per_step": t / args.steps * 1e3, "launches": launches,
-           "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes}
+           "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes,
+           "plan": {"sweeps_per_fused_launch": T, "fused_launches_per_step": F, "single_sweep_launches_per_step": S1}}
     # ---- e2e: through the C ABI from pinned host buffers (H2D of u, D2H of the result inside)
     if N == 1:
         # pinned host buffers with the Fortran (column-major) layout: the copies are plain DMAs
@@ -446,11 +455,17 @@ def main():
                            global_grid=f"8192x{8192 * world + (2 if world > 1 else 0)}"),
             "e2e": head.get("e2e"),
             "gpu_launches": head["launches"],
-            "roofline": {"bound": "hbm", "kernel": "jacobi2d_tma", "achieved": head["achieved_gbs"] / world,
+            "roofline": {"bound": "hbm",
+                         "kernel": (f"jacobi2d_wf<{head['plan']['sweeps_per_fused_launch']}>"
+                                    if head["plan"]["fused_launches_per_step"] else "jacobi2d_tma"),
+                         "achieved": head["achieved_gbs"] / world,
                          "peak": hbm_peak, "unit": "GB/s", "frac": frac, "peak_source": peak_src,
                          "traffic": traffic_from_profiles(),
                          "algorithmic_bytes_per_launch": head["per_launch_bytes"],
-                         "note": "16 B per interior point per sweep; time = all launches of the timed region"},
+                         "launch_plan_per_step": head["plan"],
+                         "note": ("16 B per interior point per launch (u read once, result written once); a fused "
+                                  "launch performs T sweeps (temporal blocking), so GLUPS can exceed the "
+                                  "single-sweep roofline 6556/16 = 410 GLUPS; time = all launches of the timed region")},
             "cpu_baseline": cpu,
             "clocks": clk,
             "rows": rows,

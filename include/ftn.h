@@ -198,6 +198,16 @@ ftn_status_t ftn_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
 ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                         int32_t* result_in_unew, ftn_stream_t stream);
 
+/* Tuning (not semantics): rank-2 sweeps are executed T at a time by one kernel that keeps
+ * the T-1 intermediate iterates in shared memory (temporal blocking, SURVEY §8(f) f2,
+ * DESIGN.md §4.3).  Results are bit-identical for every T; the array that does not hold
+ * the result holds an earlier iterate.  T in 1..4 (1 = one sweep per launch); default 3
+ * or the FTN_JACOBI_FUSE environment variable.  Process-wide.  A launch plan for S sweeps:
+ * F = S div T fused launches (F even when T is even, so that the result parity matches
+ * the sweep parity), then S - F*T single sweeps. */
+ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
+int32_t ftn_jacobi_get_fusion(void);
+
 /* ---------------------------------------------------------------- a8
  * Multi-GPU (one process per GPU, NCCL over NVLink).  The id travels between
  * processes through the caller's own channel (torch.distributed store). */

@@ -22,8 +22,33 @@
 #include "ftn_internal.cuh"
 
 #include <cstring>
+#include <cstdlib>
 
 namespace ftn {
+
+// Split `len` rows (planes) of each of `tiles` strips (columns) into segments so that the
+// units (tiles x segments) fill whole waves of `grid` CTAs: minimise
+//   wave-quantisation loss x re-read halo rows (`halo_rows` per segment, they miss L2).
+void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows, int64_t* seg, int64_t* units) {
+  double best = 1e30;
+  int64_t best_n = 1;
+  for (int64_t nseg = 1; nseg <= 512 && nseg <= len; ++nseg) {
+    const int64_t sl = (len + nseg - 1) / nseg;
+    const int64_t nseg_eff = (len + sl - 1) / sl;
+    const int64_t U = tiles * nseg_eff;
+    const int64_t waves = (U + grid - 1) / grid;
+    const double cost = (double)waves * grid / (double)U * (1.0 + (double)halo_rows / (double)(sl + halo_rows));
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_n = nseg;
+    }
+  }
+  *seg = (len + best_n - 1) / best_n;
+  *units = tiles * ((len + *seg - 1) / *seg);
+}
+
+ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
+
 namespace {
 
 // ---------------------------------------------------------------- 2-D
@@ -318,27 +343,6 @@ __global__ void __launch_bounds__(256) jacobi_generic(const __grid_constant__ JG
   }
 }
 
-// Split `len` rows (planes) of each of `tiles` strips (columns) into segments so that the
-// units (tiles x segments) fill whole waves of `grid` CTAs: minimise
-//   wave-quantisation loss x re-read halo rows (2 per segment, they miss L2).
-void plan_units(int64_t tiles, int64_t len, int64_t grid, int64_t* seg, int64_t* units) {
-  double best = 1e30;
-  int64_t best_n = 1;
-  for (int64_t nseg = 1; nseg <= 256 && nseg <= len; ++nseg) {
-    const int64_t sl = (len + nseg - 1) / nseg;
-    const int64_t nseg_eff = (len + sl - 1) / sl;
-    const int64_t U = tiles * nseg_eff;
-    const int64_t waves = (U + grid - 1) / grid;
-    const double cost = (double)waves * grid / (double)U * (1.0 + 2.0 / (double)(sl + 2));
-    if (cost < best - 1e-9) {
-      best = cost;
-      best_n = nseg;
-    }
-  }
-  *seg = (len + best_n - 1) / best_n;
-  *units = tiles * ((len + *seg - 1) / *seg);
-}
-
 bool stencil_tma_able(const ftn_desc_t* d) {
   if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
   for (int k = 1; k < d->rank; ++k)
@@ -387,7 +391,7 @@ ftn_status_t sweep(const ftn_desc_t* src, const ftn_desc_t* dst, const CUtensorM
       p.nrows = hi - lo + 1;
       p.coeff = coeff;
       int64_t grid = (int64_t)sms * 2;
-      plan_units(p.tiles_i, p.nrows, grid, &p.seg, &p.units);
+      plan_units_halo(p.tiles_i, p.nrows, grid, 2, &p.seg, &p.units);
       if (grid > p.units) grid = p.units;
       p.lo = lo;
       jacobi2d_tma<<<(unsigned)grid, S2_THREADS, S2_SMEM, s>>>(*map, p);
@@ -406,7 +410,7 @@ ftn_status_t sweep(const ftn_desc_t* src, const ftn_desc_t* dst, const CUtensorM
       p.nk = hi - lo + 1;
       p.coeff = coeff;
       int64_t grid = (int64_t)sms * 2;
-      plan_units(p.tiles_i * p.tiles_j, p.nk, grid, &p.seg, &p.units);
+      plan_units_halo(p.tiles_i * p.tiles_j, p.nk, grid, 2, &p.seg, &p.units);
       if (grid > p.units) grid = p.units;
       p.lo = lo;
       jacobi3d_tma<<<(unsigned)grid, S3_THREADS, S3_SMEM, s>>>(*map, p);
@@ -455,6 +459,21 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
 
 static bool g_attr_done[64];
 
+// Sweeps fused per launch for 2-D arrays (1 = off, 2..4): ftn_jacobi_set_fusion, else the
+// FTN_JACOBI_FUSE environment variable, else 3 (measured best on B200: 895 GLUPS at 8192^2
+// vs 629 for 2 and 747 for 4, profiles/r1_fusion_sweep.txt).
+static std::atomic<int> g_fuse{0};
+int jacobi_fuse_T() {
+  int t = g_fuse.load();
+  if (t == 0) {
+    const char* e = getenv("FTN_JACOBI_FUSE");
+    t = e ? atoi(e) : 3;
+    t = t < 1 ? 1 : (t > 4 ? 4 : t);
+    g_fuse.store(t);
+  }
+  return t;
+}
+
 ftn_status_t jacobi_prepare() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -470,6 +489,15 @@ ftn_status_t jacobi_prepare() {
 
 using namespace ftn;
 
+extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
+  if (sweeps_per_launch < 1 || sweeps_per_launch > 4)
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..4 sweeps per launch");
+  g_fuse.store(sweeps_per_launch);
+  return FTN_OK;
+}
+
+extern "C" int32_t ftn_jacobi_get_fusion(void) { return jacobi_fuse_T(); }
+
 extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                                    int32_t* result_in_unew, ftn_stream_t stream) {
   FTN_CHECK(jacobi_check(u, unew));
@@ -484,12 +512,30 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     FTN_CHECK(make_stencil_map(&mw, unew));
   }
   const int64_t nlast = u->dim[u->rank - 1].extent;
-  for (int64_t sw = 0; sw < sweeps; ++sw) {
-    const bool even = (sw % 2) == 0;
+  // Temporal blocking: launches of T fused sweeps, then single sweeps.
+  // Every launch swaps u/unew, so the result lands in unew iff the launch count is odd;
+  // the number of fused launches is chosen so that this matches the sweep parity.
+  const int T = jacobi_fuse_T();
+  int64_t fused = 0;
+  if (tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3) {
+    fused = sweeps / T;
+    if (T % 2 == 0 && fused % 2) fused -= 1;
+  }
+  int64_t launches = 0;
+  for (int64_t f = 0; f < fused; ++f, ++launches) {
+    const bool even = (launches % 2) == 0;
+    FTN_CHECK(jacobi2d_fused(even ? u : unew, even ? unew : u, T, coeff, s));
+  }
+  static const bool wf1 = getenv("FTN_JACOBI_WF1") && atoi(getenv("FTN_JACOBI_WF1")) != 0;
+  for (int64_t sw = fused * T; sw < sweeps; ++sw, ++launches) {
+    const bool even = (launches % 2) == 0;
     const ftn_desc_t* src = even ? u : unew;
     const ftn_desc_t* dst = even ? unew : u;
-    FTN_CHECK(sweep(src, dst, tma ? (even ? &mu : &mw) : nullptr, coeff, 1, nlast - 2, s));
+    if (wf1 && tma && u->rank == 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3)
+      FTN_CHECK(jacobi2d_fused(src, dst, 1, coeff, s));
+    else
+      FTN_CHECK(sweep(src, dst, tma ? (even ? &mu : &mw) : nullptr, coeff, 1, nlast - 2, s));
   }
-  if (result_in_unew) *result_in_unew = (int32_t)(sweeps % 2);
+  if (result_in_unew) *result_in_unew = (int32_t)(launches % 2);
   return FTN_OK;
 }

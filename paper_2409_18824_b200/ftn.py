@@ -89,11 +89,14 @@ def _load():
         "ftn_matmul_colsharded": [vp, P, P, P, vp, ctypes.c_size_t, vp],
         "ftn_bcast": [vp, P, ctypes.c_int32, vp],
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
+        "ftn_jacobi_set_fusion": [ctypes.c_int32],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = st
+    L.ftn_jacobi_get_fusion.restype = ctypes.c_int32
+    L.ftn_jacobi_get_fusion.argtypes = []
     L.ftn_launch_count.restype = ctypes.c_uint64
     L.ftn_launch_count.argtypes = []
     L.ftn_status_string.restype = ctypes.c_char_p
@@ -346,6 +349,26 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float | None = None, str
     r = ctypes.c_int32()
     _call("ftn_jacobi", u.ref(), unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
     return bool(r.value)
+
+
+def jacobi_set_fusion(sweeps_per_launch: int):
+    """Temporal-blocking factor of the 2-D Jacobi kernels (1..4, default 3); results are identical."""
+    _call("ftn_jacobi_set_fusion", sweeps_per_launch)
+
+
+def jacobi_fusion() -> int:
+    return int(lib.ftn_jacobi_get_fusion())
+
+
+def jacobi_launch_plan(sweeps: int, rank: int = 2) -> tuple[int, int, int]:
+    """(T, fused launches, single-sweep launches) ftn_jacobi uses for `sweeps` (rank-2 TMA path)."""
+    T = jacobi_fusion() if rank == 2 else 1
+    if T < 2:
+        return 1, 0, sweeps
+    f = sweeps // T
+    if T % 2 == 0 and f % 2:
+        f -= 1
+    return T, f, sweeps - f * T
 
 
 def gen_fill(dst: FArray, seed: int, array_id: int, mode: int, stream=None):

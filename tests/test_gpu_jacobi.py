@@ -127,3 +127,28 @@ def test_c2_full_size_sampled(ftn):
         ref = (b if new else a)[i - i0, j - j0]
         got = res.section((i + 1, i + 1), (j + 1, j + 1)).to_numpy()[0, 0]
         assert got == ref, (i, j)
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4])
+@pytest.mark.parametrize("shape", [(3, 3), (5, 40), (40, 5), (129, 31), (200, 301), (257, 77), (1000, 130)])
+@pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 7, 8, 9])
+def test_2d_temporal_blocking(ftn, T, shape, sweeps):
+    """Fused launches of T sweeps are bit-identical to the oracle's
+    sweep-by-sweep DO nest, and the result lands where the sweep parity says."""
+    ftn.jacobi_set_fusion(T)
+    try:
+        u0 = synth.jacobi_init(shape, array_id=sum(shape) + sweeps)
+        got, ref = _run_both(ftn, u0, sweeps, C2, [1, 0])
+        np.testing.assert_array_equal(got, ref)
+    finally:
+        ftn.jacobi_set_fusion(3)
+
+
+def test_2d_temporal_blocking_long_strip(ftn):
+    """Many units per CTA, uneven segments, 60 sweeps."""
+    for T in (2, 3, 4):
+        ftn.jacobi_set_fusion(T)
+        u0 = synth.jacobi_init((3000, 2000), array_id=T)
+        got, ref = _run_both(ftn, u0, 12, C2)
+        np.testing.assert_array_equal(got, ref)
+    ftn.jacobi_set_fusion(3)
