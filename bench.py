@@ -151,25 +151,28 @@ def bench_jacobi2d(torch, ftn, args, ctx):
         step = lambda: ftn.jacobi(U, W, sweeps)  # noqa: E731
         interior = (n - 2) * (n - 2)
     else:
-        # weak scaling: global grid 8192 x (8192 N + 2); this rank owns planes [1 + r n, (r+1) n]
-        nl = n + 2
+        # weak scaling: global grid 8192 x (8192 N + 2); rank r owns global columns
+        # [1 + r n, (r+1) n] (Fortran dim 2) and keeps `halo` halo planes per side, so
+        # ftn_jacobi_dist exchanges T planes and runs T fused sweeps per step (T = halo)
+        halo = max(1, ftn.jacobi_fusion())
+        nl = n + 2 * halo
         U, W = ftn.FArray.empty((n, nl)), ftn.FArray.empty((n, nl))
         ftn.gen_fill(U, SEED, 1 + rank, ftn.GEN_U01)
         ftn.fill(U.section((1, 1), (1, nl)), 0.0)
         ftn.fill(U.section((n, n), (1, nl)), 0.0)
         if rank == 0:
-            ftn.fill(U.section((1, n), (1, 1)), 1.0)
+            ftn.fill(U.section((1, n), (halo, halo)), 1.0)            # global boundary plane j = 1
         if rank == N - 1:
-            ftn.fill(U.section((1, n), (nl, nl)), 0.0)
+            ftn.fill(U.section((1, n), (nl - halo + 1, nl - halo + 1)), 0.0)   # global plane j = N
         ftn.assign(W, U)
         comm = ctx["comm"]
-        step = lambda: comm.jacobi(U, W, sweeps)  # noqa: E731
+        step = lambda: comm.jacobi(U, W, sweeps, halo=halo)  # noqa: E731
         interior = (n - 2) * n * N
     t = timed(torch, step, args.steps, args.warmup, ctx["clocks"], ctx["dist"], counter=ftn.launch_count)
     launches = LAST_LAUNCHES[0]
     glups = interior * sweeps * args.steps / t / 1e9
     # launch plan of ftn_jacobi: F launches of T fused sweeps + S1 single sweeps per step
-    T, F, S1 = ftn.jacobi_launch_plan(sweeps) if N == 1 else (1, 0, sweeps)
+    T, F, S1 = ftn.jacobi_launch_plan(sweeps)
     per_launch_bytes = 16 * (n - 2) * (n - 2 if N == 1 else n)       # algorithmic: read u once, write once
     stencil_launches = (F + S1) * args.steps
     achieved = per_launch_bytes * stencil_launches / t / 1e9          # GB/s, launches back to back
@@ -326,7 +329,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
             ftn.gen_fill(U, SEED, 7 + rank, ftn.GEN_U01)
             ftn.assign(W, U)
-            t = timed(torch, lambda: comm.jacobi(U, W, sweeps), max(2, steps // 2), 1, ctx["clocks"], dist)
+            t = timed(torch, lambda: comm.jacobi(U, W, sweeps, halo=1), max(2, steps // 2), 1, ctx["clocks"], dist)
             interior = (n - 2) ** 3
             del U, W
         torch.cuda.empty_cache()

@@ -237,16 +237,27 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local,
                                     const ftn_desc_t* y_local, void* result_dev, void* ws,
                                     size_t ws_bytes, ftn_stream_t stream);
 
-/* Distributed Jacobi: u_local / unew_local are this rank's slab of the global
- * array along the last dimension INCLUDING one halo plane on each side
- * (planes 1 and n_last of the local arrays); rank r's first owned plane
- * follows rank r-1's last.  On the first and last rank the outer halo plane
- * is the global boundary plane.  Each sweep exchanges the owned boundary
- * planes with ranks r-1 / r+1 (ncclSend/ncclRecv) and updates the interior.
- * Results are bit-identical to ftn_jacobi on the undivided array. */
+/* Distributed Jacobi: u_local / unew_local are this rank's slab of the global array
+ * along the last dimension with `halo` planes on each side: local planes
+ * [halo, n_last - halo) are owned, rank r's first owned plane follows rank r-1's last,
+ * and on the first (last) rank local plane halo-1 (n_last-halo) is the global boundary
+ * plane.  Per step the k owned planes next to each neighbour are exchanged with
+ * ncclSend/ncclRecv (k = 1, or k = T sweeps fused per step for TMA-able rank-2 slabs,
+ * T = min(halo, ftn_jacobi_get_fusion())) and ftn_jacobi_slab advances the owned planes
+ * by k sweeps.  Results are bit-identical to ftn_jacobi on the undivided array;
+ * *result_in_unew as for ftn_jacobi. */
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const ftn_desc_t* unew_local,
-                             int64_t sweeps, double coeff, int32_t* result_in_unew,
+                             int64_t sweeps, double coeff, int32_t halo, int32_t* result_in_unew,
                              ftn_stream_t stream);
+
+/* One local step of the distributed Jacobi without communication (for callers with their
+ * own exchange, e.g. MPI): `sweeps` (1 <= sweeps <= halo) sweeps of the owned planes of a
+ * slab laid out as for ftn_jacobi_dist whose halo planes are current, src -> dst.  Reads src
+ * planes [halo - sweeps, n_last - halo + sweeps); writes only the owned interior of dst.
+ * first / last: this slab holds the global lower / upper boundary plane.  sweeps > 1 needs
+ * a TMA-able rank-2 slab (FTN_ERR_UNSUPPORTED otherwise). */
+ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
+                             int32_t halo, int32_t first, int32_t last, ftn_stream_t stream);
 
 /* c(:, J_r) = MATMUL(a, b(:, J_r)): b_local / c_local are this rank's column
  * block, a is replicated (see ftn_bcast).  No communication. */

@@ -24,6 +24,8 @@ ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_de
                           cudaStream_t s);
 ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew);
 ftn_status_t jacobi_prepare();
+int jacobi_fuse_T();
+bool stencil_tma_able(const ftn_desc_t* d);
 
 namespace {
 
@@ -146,7 +148,7 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local, 
 }
 
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
-                             double coeff, int32_t* result_in_unew, ftn_stream_t stream) {
+                             double coeff, int32_t halo, int32_t* result_in_unew, ftn_stream_t stream) {
   if (!comm) return fail(FTN_ERR_NULL, "ftn_jacobi_dist: comm NULL");
   FTN_CHECK(jacobi_check(u, unew));
   if (!plane_contiguous(u) || !plane_contiguous(unew))
@@ -154,34 +156,47 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
   if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: negative sweep count");
   const int r = u->rank;
   const int64_t nl = u->dim[r - 1].extent;
-  if (nl < 3) return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: a slab needs 1 owned plane + 2 halo planes");
+  if (halo < 1 || nl - 2 * (int64_t)halo < 1)
+    return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: a slab needs >= 1 owned plane + halo planes on each side");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
+  // temporal blocking: T sweeps per exchange when the slab is rank 2 and TMA-able
+  int T = 1;
+  if (r == 2 && stencil_tma_able(u) && stencil_tma_able(unew)) {
+    T = jacobi_fuse_T();
+    if (T > halo) T = halo;
+  }
+  int64_t fused = T > 1 ? sweeps / T : 0;
+  if (T % 2 == 0 && fused % 2) fused -= 1;  // launch count must match the sweep parity
   const size_t plane = (size_t)(desc_size(u) / nl);
   const int lower = comm->rank - 1, upper = comm->rank + 1;
-  for (int64_t sw = 0; sw < sweeps; ++sw) {
-    const ftn_desc_t* src = (sw % 2 == 0) ? u : unew;
-    const ftn_desc_t* dst = (sw % 2 == 0) ? unew : u;
+  const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
+  int64_t launches = 0;
+  const int64_t total = fused + (sweeps - fused * T);
+  for (; launches < total; ++launches) {
+    const int k = launches < fused ? T : 1;
+    const ftn_desc_t* src = (launches % 2 == 0) ? u : unew;
+    const ftn_desc_t* dst = (launches % 2 == 0) ? unew : u;
     char* b = (char*)src->base_addr;
     const int64_t sm = src->dim[r - 1].sm;
-    // halo exchange of the source: owned boundary planes -> neighbours' halo planes
     if (comm->nranks > 1) {
+      // the k owned planes next to each neighbour -> its k halo planes next to its owned planes
       FTN_NCCL(ncclGroupStart());
       if (lower >= 0) {
-        FTN_NCCL(ncclSend(b + 1 * sm, plane, ncclFloat64, lower, comm->nccl, s));
-        FTN_NCCL(ncclRecv(b + 0 * sm, plane, ncclFloat64, lower, comm->nccl, s));
+        FTN_NCCL(ncclSend(b + halo * sm, plane * k, ncclFloat64, lower, comm->nccl, s));
+        FTN_NCCL(ncclRecv(b + (halo - k) * sm, plane * k, ncclFloat64, lower, comm->nccl, s));
       }
       if (upper < comm->nranks) {
-        FTN_NCCL(ncclSend(b + (nl - 2) * sm, plane, ncclFloat64, upper, comm->nccl, s));
-        FTN_NCCL(ncclRecv(b + (nl - 1) * sm, plane, ncclFloat64, upper, comm->nccl, s));
+        FTN_NCCL(ncclSend(b + (nl - halo - k) * sm, plane * k, ncclFloat64, upper, comm->nccl, s));
+        FTN_NCCL(ncclRecv(b + (nl - halo) * sm, plane * k, ncclFloat64, upper, comm->nccl, s));
       }
       FTN_NCCL(ncclGroupEnd());
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    FTN_CHECK(jacobi_sweep(src, dst, coeff, 1, nl - 2, s));
+    FTN_CHECK(ftn_jacobi_slab(src, dst, k, coeff, halo, first, last, stream));
   }
-  if (result_in_unew) *result_in_unew = (int32_t)(sweeps % 2);
+  if (result_in_unew) *result_in_unew = (int32_t)(launches % 2);
   return FTN_OK;
 }
 

@@ -48,6 +48,17 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 }
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
+ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
+                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
+
+bool stencil_tma_able(const ftn_desc_t* d) {
+  if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
+  for (int k = 1; k < d->rank; ++k)
+    if (d->dim[k].sm <= 0 || (d->dim[k].sm % 16) != 0 || d->dim[k].sm >= (1ll << 40)) return false;
+  for (int k = 0; k < d->rank; ++k)
+    if (d->dim[k].extent >= (1ll << 31)) return false;
+  return true;
+}
 
 namespace {
 
@@ -343,14 +354,6 @@ __global__ void __launch_bounds__(256) jacobi_generic(const __grid_constant__ JG
   }
 }
 
-bool stencil_tma_able(const ftn_desc_t* d) {
-  if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
-  for (int k = 1; k < d->rank; ++k)
-    if (d->dim[k].sm <= 0 || (d->dim[k].sm % 16) != 0 || d->dim[k].sm >= (1ll << 40)) return false;
-  for (int k = 0; k < d->rank; ++k)
-    if (d->dim[k].extent >= (1ll << 31)) return false;
-  return true;
-}
 
 ftn_status_t make_stencil_map(CUtensorMap* m, const ftn_desc_t* d) {
   uint64_t dims[3] = {(uint64_t)d->dim[0].extent, (uint64_t)d->dim[1].extent,
@@ -538,4 +541,36 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
   }
   if (result_in_unew) *result_in_unew = (int32_t)(launches % 2);
   return FTN_OK;
+}
+
+// One local step of the distributed DO nest, no communication: `sweeps`
+// (1 <= sweeps <= halo) sweeps of the owned planes [halo, n_last - halo) of a slab whose
+// halo planes are current; reads src planes [halo - sweeps, n_last - halo + sweeps).
+extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
+                                        int32_t halo, int32_t first, int32_t last, ftn_stream_t stream) {
+  FTN_CHECK(jacobi_check(src, dst));
+  const int r = src->rank;
+  const int64_t nl = src->dim[r - 1].extent;
+  if (halo < 1 || nl - 2 * (int64_t)halo < 1)
+    return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need halo >= 1 and at least one owned plane");
+  if (sweeps < 1 || sweeps > halo) return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need 1 <= sweeps <= halo");
+  const bool tma = stencil_tma_able(src) && stencil_tma_able(dst);
+  if (sweeps > 1 && !(r == 2 && tma))
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_slab: several sweeps per step need a TMA-able rank-2 slab");
+  FTN_CHECK(require_sm100());
+  FTN_CHECK(jacobi_prepare());
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t lo = halo, hi = nl - halo - 1;
+  if (sweeps == 1) {
+    CUtensorMap m;
+    const CUtensorMap* mp = nullptr;
+    if (tma) {
+      FTN_CHECK(make_stencil_map(&m, src));
+      mp = &m;
+    }
+    return sweep(src, dst, mp, coeff, lo, hi, s);
+  }
+  const int64_t fix_lo = first ? lo - 1 : INT64_MIN / 4;
+  const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
+  return jacobi2d_fused_rows(src, dst, sweeps, coeff, lo, hi, fix_lo, fix_hi, s);
 }

@@ -5,23 +5,27 @@
 // instead of 16 B per update.
 //
 // Register wavefront (no shared-memory levels, no block barriers):
-//   * A CTA owns a strip of NW*(32-2T) output columns; one TMA box row per input row
+//   * A CTA owns a strip of NW*(64-2T) output columns; one TMA box row per input row
 //     covers the strip plus an H-column halo on each side (H = T rounded up to even: a
 //     box must start on a 16-byte boundary, tools/microbench/tma_probe.cu).  Rows arrive
 //     through an NS-stage mbarrier ring of {BW x R} boxes issued by one producer lane.
-//   * Warp w reads its own 32-column window of each row (overlapping its neighbours by
-//     2T columns) and runs the T sweeps as a pipeline along j: when input row s arrives,
-//     level 1 (sweep 1) produces row s-1, level 2 row s-2, ..., level T row s-T, which
-//     is stored.  Each level keeps its last three rows in registers; the i-1 / i+1
-//     neighbours come from the adjacent lanes (shfl), so lane l is valid at level t for
-//     t <= l < 32-t (a trapezoid) and lanes T..31-T are the warp's outputs.
+//   * Warp w reads its own 64-column window of each row (two adjacent columns per
+//     lane; windows of neighbouring warps overlap by 2T columns) and runs the T sweeps
+//     as a pipeline along j: when input row s arrives, level 1 (sweep 1) produces row
+//     s-1, level 2 row s-2, ..., level T row s-T, which is stored.  Each level keeps its
+//     last three rows in registers; the i-1 / i+1 neighbours are the lane's other column
+//     or come from the adjacent lane (one shfl each way per level), so column k of the
+//     window is valid at level t for t <= k < 64-t (a trapezoid) and columns T..63-T are
+//     the warp's outputs.
 //   * Global boundary points keep their value at every level (the caller presets the
-//     boundary of both arrays, R#16); values outside the array are never consumed.
+//     boundary of both arrays, R#16); values outside the array are never consumed.  Warps
+//     whose window and unit touch no global boundary take a select-free fast path.
 // Work units (strip, row segment) are taken round-robin with the strip fastest, as in
 // the single-sweep kernels.
 #include "ftn_internal.cuh"
 
 #include <cstring>
+#include <cstdlib>
 
 namespace ftn {
 
@@ -29,18 +33,18 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 
 namespace {
 
-constexpr int WF_NW = 8;   // compute warps per CTA
-constexpr int WF_R = 8;    // rows per TMA box
-constexpr int WF_NS = 4;   // ring stages
-
-template <int T> struct WFCfg {
+template <int T, int WF_NW = 4 /*compute warps per CTA*/, int WF_R = 8 /*rows per TMA box*/,
+          int WF_NS = 4 /*ring stages*/>
+struct WFCfg {
+  static constexpr int NW = WF_NW, R = WF_R, NS = WF_NS;
   static constexpr int H = T + (T & 1);
-  static constexpr int WO = 32 - 2 * T;           // output columns per warp
+  static constexpr int WO = 64 - 2 * T;           // output columns per warp
   static constexpr int OUT = WF_NW * WO;          // output columns per CTA strip
   static constexpr int BW = OUT + 2 * H;          // box width (<= 256, even)
   static constexpr int STAGE = (BW * WF_R * 8 + 127) / 128 * 128;
   static constexpr int SMEM = WF_NS * STAGE + 128 + 64;
   static constexpr int THREADS = (WF_NW + 1) * 32;
+  static constexpr bool ALIGNED = ((H - T) % 2) == 0;  // lane column pairs 16-byte aligned in smem
   static_assert(BW <= 256, "TMA box width");
 };
 
@@ -49,16 +53,19 @@ struct WFParams {
   int64_t d_sm1, d_sm2;
   int64_t n1, n2;
   int64_t strips;
-  int64_t nrows;   // rows to update (interior rows 1 .. n2-2)
+  int64_t row_lo;  // first output row (0-based position in dim 2)
+  int64_t nrows;   // output rows row_lo .. row_lo + nrows - 1
+  int64_t fix_lo;  // rows <= fix_lo and >= fix_hi keep their value at every level
+  int64_t fix_hi;  //   (the global boundary; outside it nothing is consumed)
   int64_t seg;     // output rows per unit
   int64_t units;
   double coeff;
 };
 
-template <int T>
-__global__ void __launch_bounds__(WFCfg<T>::THREADS) jacobi2d_wf(const __grid_constant__ CUtensorMap src_map,
-                                                                 const __grid_constant__ WFParams p) {
-  using C = WFCfg<T>;
+template <int T, class C>
+__global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant__ CUtensorMap src_map,
+                                                          const __grid_constant__ WFParams p) {
+  constexpr int WF_NW = C::NW, WF_R = C::R, WF_NS = C::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + WF_NS * C::STAGE);
@@ -81,8 +88,8 @@ __global__ void __launch_bounds__(WFCfg<T>::THREADS) jacobi2d_wf(const __grid_co
       int64_t k = 0;
       for (int64_t u = blockIdx.x; u < p.units; u += G) {
         const int64_t c = u % p.strips;
-        const int64_t ja = 1 + (u / p.strips) * p.seg;
-        const int64_t jb = min(ja + p.seg, 1 + p.nrows);
+        const int64_t ja = p.row_lo + (u / p.strips) * p.seg;
+        const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
         const int64_t nch = (jb - ja + 2 * T + WF_R - 1) / WF_R;
         for (int64_t q = 0; q < nch; ++q, ++k) {
           const int s = (int)(k % WF_NS);
@@ -98,62 +105,98 @@ __global__ void __launch_bounds__(WFCfg<T>::THREADS) jacobi2d_wf(const __grid_co
     return;
   }
 
-  // ---------------- compute warps
-  const int col = C::H - T + warp * C::WO + lane;  // box column of this lane
-  const bool out_lane = lane >= T && lane < 32 - T;
+  // ---------------- compute warps: lane owns window columns 2*lane, 2*lane+1
+  const int wbase = C::H - T + warp * C::WO;  // box column of window column 0
+  const int col0 = wbase + 2 * lane;          // box column of this lane's first column
   const double coeff = p.coeff;
   int64_t k = 0;
   for (int64_t u = blockIdx.x; u < p.units; u += G) {
     const int64_t c = u % p.strips;
-    const int64_t ja = 1 + (u / p.strips) * p.seg;
-    const int64_t jb = min(ja + p.seg, 1 + p.nrows);
+    const int64_t ja = p.row_lo + (u / p.strips) * p.seg;
+    const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
     const int64_t nr = jb - ja + 2 * T;  // input rows, relative 0 .. nr-1 (global ja - T + r)
-    const int64_t gcol = c * C::OUT - C::H + col;
-    const bool col_fixed = gcol <= 0 || gcol >= p.n1 - 1;
-    const bool store_col = out_lane && gcol >= 1 && gcol <= p.n1 - 2;
-    char* outp = p.dst + gcol * p.d_sm1 + ja * p.d_sm2;  // row ja = relative row T of level T
-    // relative rows r whose global row ja - T + r is interior: r_lo <= r <= r_hi
-    const int r_lo = (int)(1 - (ja - T)), r_hi = (int)(p.n2 - 2 - (ja - T));
-    // level t keeps rows (s-t-1, s-t, s-t+1) = (up, mid, dn) after step s
-    double up[T + 1], mid[T + 1], dn[T + 1];
+    const int64_t gbase = c * C::OUT - C::H;     // global column of box column 0
+    const int64_t g0 = gbase + col0;              // global column of this lane's first column
+    bool fixed[2], store[2];
 #pragma unroll
-    for (int t = 0; t <= T; ++t) up[t] = mid[t] = dn[t] = 0.0;
+    for (int e = 0; e < 2; ++e) {
+      const int kk = 2 * lane + e;  // window column
+      const int64_t g = g0 + e;
+      fixed[e] = g <= 0 || g >= p.n1 - 1;
+      store[e] = kk >= T && kk < 64 - T && g >= 1 && g <= p.n1 - 2;
+    }
+    // warp-uniform fast path: no level-1 point of this window and unit is a boundary point
+    const int64_t wg_lo = gbase + wbase + 1, wg_hi = gbase + wbase + 62;
+    const bool fast = ja - T + 1 > p.fix_lo && jb + T - 2 < p.fix_hi && wg_lo >= 1 && wg_hi <= p.n1 - 2;
+    // relative rows r whose row ja - T + r is updated: r_lo <= r <= r_hi
+    const int64_t rl = p.fix_lo + 1 - (ja - T), rh = p.fix_hi - 1 - (ja - T);
+    const int r_lo = (int)max(rl, (int64_t)-1), r_hi = (int)min(rh, (int64_t)(1 << 30));
+    char* outp = p.dst + g0 * p.d_sm1 + ja * p.d_sm2;  // row ja = relative row T of level T
+    // level t keeps rows (s-t-1, s-t, s-t+1) = (up, mid, dn) after step s, two columns each
+    double up[T + 1][2], mid[T + 1][2], dn[T + 1][2];
+#pragma unroll
+    for (int t = 0; t <= T; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) up[t][e] = mid[t][e] = dn[t][e] = 0.0;
     const int64_t nch = (nr + WF_R - 1) / WF_R;
     int s = 0;
-    // one pipeline step: input row s -> level t rows s - t
-    auto step = [&](const double* row) {
-      up[0] = mid[0];
-      mid[0] = dn[0];
-      dn[0] = *row;
+    auto step = [&](const double* row, bool fastpath) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        up[0][e] = mid[0][e];
+        mid[0][e] = dn[0][e];
+      }
+      if constexpr (C::ALIGNED) {
+        const double2 v = *reinterpret_cast<const double2*>(row);
+        dn[0][0] = v.x;
+        dn[0][1] = v.y;
+      } else {
+        dn[0][0] = row[0];
+        dn[0][1] = row[1];
+      }
 #pragma unroll
       for (int t = 1; t <= T; ++t) {
-        const double lf = __shfl_up_sync(0xffffffffu, mid[t - 1], 1);
-        const double rt = __shfl_down_sync(0xffffffffu, mid[t - 1], 1);
-        const int r = s - t;
-        double v = lf + rt;
-        v = v + up[t - 1];
-        v = v + dn[t - 1];
-        v = coeff * v;
-        const bool upd = !col_fixed && r >= r_lo && r <= r_hi;
-        up[t] = mid[t];
-        mid[t] = dn[t];
-        dn[t] = upd ? v : mid[t - 1];
+        // level t row s - t from level t-1 rows s-t-1, s-t, s-t+1
+        const double left0 = __shfl_up_sync(0xffffffffu, mid[t - 1][1], 1);
+        const double right1 = __shfl_down_sync(0xffffffffu, mid[t - 1][0], 1);
+        double v0 = left0 + mid[t - 1][1];
+        v0 = v0 + up[t - 1][0];
+        v0 = v0 + dn[t - 1][0];
+        v0 = coeff * v0;
+        double v1 = mid[t - 1][0] + right1;
+        v1 = v1 + up[t - 1][1];
+        v1 = v1 + dn[t - 1][1];
+        v1 = coeff * v1;
+        if (!fastpath) {
+          const int r = s - t;
+          const bool rowok = r >= r_lo && r <= r_hi;
+          if (!(rowok && !fixed[0])) v0 = mid[t - 1][0];
+          if (!(rowok && !fixed[1])) v1 = mid[t - 1][1];
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          up[t][e] = mid[t][e];
+          mid[t][e] = dn[t][e];
+        }
+        dn[t][0] = v0;
+        dn[t][1] = v1;
       }
-      if (s >= 2 * T) {
-        if (store_col) *reinterpret_cast<double*>(outp) = dn[T];
+      if (s >= 2 * T) {  // level T row s - T is output row ja + (s - 2T)
+        if (store[0]) *reinterpret_cast<double*>(outp) = dn[T][0];
+        if (store[1]) *reinterpret_cast<double*>(outp + p.d_sm1) = dn[T][1];
         outp += p.d_sm2;
       }
       ++s;
     };
     for (int64_t q = 0; q < nch; ++q, ++k) {
       dev::mbar_wait(&full[k % WF_NS], (uint32_t)((k / WF_NS) & 1));
-      const double* st = reinterpret_cast<const double*>(smem + (k % WF_NS) * C::STAGE) + col;
+      const double* st = reinterpret_cast<const double*>(smem + (k % WF_NS) * C::STAGE) + col0;
       const int rows = (int)min((int64_t)WF_R, nr - q * WF_R);
-      if (rows == WF_R) {
+      if (rows == WF_R && fast) {
 #pragma unroll
-        for (int rr = 0; rr < WF_R; ++rr) step(st + rr * C::BW);
+        for (int rr = 0; rr < WF_R; ++rr) step(st + rr * C::BW, true);
       } else {
-        for (int rr = 0; rr < rows; ++rr) step(st + rr * C::BW);
+        for (int rr = 0; rr < rows; ++rr) step(st + rr * C::BW, false);
       }
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&empty[k % WF_NS]);
@@ -161,14 +204,15 @@ __global__ void __launch_bounds__(WFCfg<T>::THREADS) jacobi2d_wf(const __grid_co
   }
 }
 
-template <int T>
-ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s) {
-  using C = WFCfg<T>;
+template <int T, class C>
+ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t row_lo, int64_t row_hi,
+                       int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
+  constexpr int WF_R = C::R;
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
-    FTN_CUDA(cudaFuncSetAttribute(jacobi2d_wf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    FTN_CUDA(cudaFuncSetAttribute(jacobi2d_wf<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr[dev & 63] = true;
   }
   CUtensorMap m;
@@ -184,29 +228,61 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   p.n1 = src->dim[0].extent;
   p.n2 = src->dim[1].extent;
   p.strips = (p.n1 - 1 + C::OUT - 1) / C::OUT;  // output columns 1 .. n1-2 lie in [0, strips*OUT)
-  p.nrows = p.n2 - 2;
+  p.row_lo = row_lo;
+  p.nrows = row_hi - row_lo + 1;
+  p.fix_lo = fix_lo;
+  p.fix_hi = fix_hi;
   p.coeff = coeff;
+  if (p.nrows <= 0 || p.n1 < 3) return FTN_OK;
   int occ = 0;
-  FTN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi2d_wf<T>, C::THREADS, C::SMEM));
+  FTN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi2d_wf<T, C>, C::THREADS, C::SMEM));
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)num_sms() * occ;
   plan_units_halo(p.strips, p.nrows, grid, 2 * T, &p.seg, &p.units);
   if (grid > p.units) grid = p.units;
-  jacobi2d_wf<T><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, p);
+  jacobi2d_wf<T, C><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, p);
   return after_launch("jacobi2d_wf");
 }
 
 }  // namespace
 
-// T fused sweeps src -> dst (rank 2, TMA-able src): see the header comment.
-ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s) {
-  switch (T) {
-    case 1: return launch_wf<1>(src, dst, coeff, s);
-    case 2: return launch_wf<2>(src, dst, coeff, s);
-    case 3: return launch_wf<3>(src, dst, coeff, s);
-    case 4: return launch_wf<4>(src, dst, coeff, s);
+// T fused sweeps src -> dst (rank 2, TMA-able src) on output rows [row_lo, row_hi], with
+// rows <= fix_lo and >= fix_hi held fixed (the global boundary): see the header comment.
+// Input rows [row_lo - T, row_hi + T] are read.
+ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
+                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
+  static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
+#define WF_ARGS src, dst, coeff, row_lo, row_hi, fix_lo, fix_hi, s
+  switch (cfg < 0 ? T * 10 + 9 : T * 10 + cfg) {
+    // defaults (cfg 9): measured on B200, DESIGN.md §4.3
+    case 19: return launch_wf<1, WFCfg<1, 4, 16, 3>>(WF_ARGS);
+    case 29: return launch_wf<2, WFCfg<2, 4, 16, 3>>(WF_ARGS);
+    case 39: return launch_wf<3, WFCfg<3, 4, 16, 3>>(WF_ARGS);
+    case 49: return launch_wf<4, WFCfg<4, 4, 16, 3>>(WF_ARGS);
+    // tuning variants (FTN_WF_CFG)
+    case 10: return launch_wf<1, WFCfg<1>>(WF_ARGS);
+    case 20: return launch_wf<2, WFCfg<2>>(WF_ARGS);
+    case 30: return launch_wf<3, WFCfg<3>>(WF_ARGS);
+    case 40: return launch_wf<4, WFCfg<4>>(WF_ARGS);
+    case 31: return launch_wf<3, WFCfg<3, 4, 8, 3>>(WF_ARGS);
+    case 41: return launch_wf<4, WFCfg<4, 4, 8, 3>>(WF_ARGS);
+    case 32: return launch_wf<3, WFCfg<3, 2, 8, 4>>(WF_ARGS);
+    case 42: return launch_wf<4, WFCfg<4, 2, 8, 4>>(WF_ARGS);
+    case 35: return launch_wf<3, WFCfg<3, 4, 16, 2>>(WF_ARGS);
+    case 45: return launch_wf<4, WFCfg<4, 4, 16, 2>>(WF_ARGS);
+    case 36: return launch_wf<3, WFCfg<3, 4, 32, 2>>(WF_ARGS);
+    case 46: return launch_wf<4, WFCfg<4, 4, 32, 2>>(WF_ARGS);
+    case 37: return launch_wf<3, WFCfg<3, 2, 32, 2>>(WF_ARGS);
+    case 47: return launch_wf<4, WFCfg<4, 2, 32, 2>>(WF_ARGS);
   }
-  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..4");
+#undef WF_ARGS
+  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..4 (and FTN_WF_CFG a known variant)");
+}
+
+// The whole interior of a single array: rows 1 .. n2-2, boundary rows 0 and n2-1.
+ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s) {
+  const int64_t n2 = src->dim[1].extent;
+  return jacobi2d_fused_rows(src, dst, T, coeff, 1, n2 - 2, 0, n2 - 1, s);
 }
 
 }  // namespace ftn

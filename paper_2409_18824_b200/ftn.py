@@ -85,7 +85,9 @@ def _load():
         "ftn_maxval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_minval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_dot_product_global": [vp, P, P, vp, vp, ctypes.c_size_t, vp],
-        "ftn_jacobi_dist": [vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
+        "ftn_jacobi_dist": [vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                            vp],
+        "ftn_jacobi_slab": [P, P, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp],
         "ftn_matmul_colsharded": [vp, P, P, P, vp, ctypes.c_size_t, vp],
         "ftn_bcast": [vp, P, ctypes.c_int32, vp],
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
@@ -356,6 +358,14 @@ def jacobi_set_fusion(sweeps_per_launch: int):
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
 
 
+def jacobi_slab(src: FArray, dst: FArray, sweeps: int, halo: int, first: bool, last: bool, coeff=None,
+                stream=None):
+    """One communication-free local step of the distributed Jacobi (see include/ftn.h)."""
+    if coeff is None:
+        coeff = JACOBI_C2 if src.rank == 2 else JACOBI_C3
+    _call("ftn_jacobi_slab", src.ref(), dst.ref(), sweeps, coeff, halo, int(first), int(last), _stream(stream))
+
+
 def jacobi_fusion() -> int:
     return int(lib.ftn_jacobi_get_fusion())
 
@@ -434,11 +444,13 @@ class Comm:
               ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
         return res
 
-    def jacobi(self, u: FArray, unew: FArray, sweeps: int, coeff=None, stream=None) -> bool:
+    def jacobi(self, u: FArray, unew: FArray, sweeps: int, coeff=None, halo: int = 1, stream=None) -> bool:
+        """Distributed sweeps of this rank's slab (halo planes per side)."""
         if coeff is None:
             coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
         r = ctypes.c_int32()
-        _call("ftn_jacobi_dist", self.handle, u.ref(), unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
+        _call("ftn_jacobi_dist", self.handle, u.ref(), unew.ref(), sweeps, coeff, halo, ctypes.byref(r),
+              _stream(stream))
         return bool(r.value)
 
     def matmul(self, c_local: FArray, a_full: FArray, b_local: FArray, stream=None):

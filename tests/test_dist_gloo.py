@@ -50,38 +50,54 @@ def _worker(rank, world, port, q, shape2, shape3, sweeps):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         out = {}
-        for shape, coeff in ((shape2, 0.25), (shape3, 1.0 / 6.0)):
+        for shape, coeff, halo in ((shape2, 0.25, 1), (shape2, 0.25, 3), (shape3, 1.0 / 6.0, 1)):
             full = synth.jacobi_init(shape)
             nlast = shape[-1]
-            g0, nl = D.jacobi_slab(nlast, world, rank)
-            # local arrays hold global planes [g0, g0 + nl)
-            sl = [slice(None)] * (len(shape) - 1)
-            u = np.asfortranarray(full[tuple(sl + [slice(g0, g0 + nl)])].copy())
-            w = u.copy(order="F")
-            cur, nxt = u, w
-            for _ in range(sweeps):
-                # halo exchange of the source (the protocol of ftn_jacobi_dist)
+            sl = D.slab(nlast - 2, world, rank)          # owned global planes [sl.lo+1, sl.hi+1)
+            g0 = sl.lo + 1 - halo                       # global plane of local plane 0
+            nl = sl.owned + 2 * halo
+            cur = np.full(shape[:-1] + (nl,), np.nan, order="F")
+            for k in range(nl):
+                if 0 <= g0 + k < nlast:
+                    cur[..., k] = full[..., g0 + k]
+            nxt = cur.copy(order="F")
+            k_sweeps = halo                              # sweeps per exchange (ftn_jacobi_dist's T)
+            steps = [k_sweeps] * (sweeps // k_sweeps) + [1] * (sweeps % k_sweeps)
+            for k in steps:
+                # exchange the k owned planes next to each neighbour into its k innermost halo planes
                 reqs = []
-                recv_lo = torch.empty(cur[..., 0].size, dtype=torch.float64)
-                recv_hi = torch.empty(cur[..., 0].size, dtype=torch.float64)
+                plane_sz = int(np.prod(shape[:-1]))
+                recv_lo = torch.empty(plane_sz * k, dtype=torch.float64)
+                recv_hi = torch.empty(plane_sz * k, dtype=torch.float64)
                 if rank > 0:
-                    reqs.append(dist.isend(torch.from_numpy(cur[..., 1].ravel(order="F").copy()), rank - 1))
+                    reqs.append(dist.isend(torch.from_numpy(cur[..., halo:halo + k].ravel(order="F").copy()), rank - 1))
                     reqs.append(dist.irecv(recv_lo, rank - 1))
                 if rank < world - 1:
-                    reqs.append(dist.isend(torch.from_numpy(cur[..., nl - 2].ravel(order="F").copy()), rank + 1))
+                    reqs.append(dist.isend(torch.from_numpy(cur[..., nl - halo - k:nl - halo].ravel(order="F").copy()),
+                                           rank + 1))
                     reqs.append(dist.irecv(recv_hi, rank + 1))
                 for r in reqs:
                     r.wait()
                 if rank > 0:
-                    cur[..., 0] = recv_lo.numpy().reshape(cur[..., 0].shape, order="F")
+                    cur[..., halo - k:halo] = recv_lo.numpy().reshape(shape[:-1] + (k,), order="F")
                 if rank < world - 1:
-                    cur[..., nl - 1] = recv_hi.numpy().reshape(cur[..., 0].shape, order="F")
-                oracle.jacobi(oracle.FArray(cur), oracle.FArray(nxt), 1, coeff)  # local interior
+                    cur[..., nl - halo:nl - halo + k] = recv_hi.numpy().reshape(shape[:-1] + (k,), order="F")
+                # k local sweeps on the window [halo - k, nl - halo + k): its outer planes are held
+                # fixed by the oracle (the global boundary on the first / last rank), and errors
+                # from holding a halo plane fixed travel one plane per sweep, never reaching the
+                # owned planes.  Only the owned planes are kept.
+                lo = max(halo - k, halo - 1 if rank == 0 else 0)
+                hi = min(nl - halo + k, nl - halo + 1 if rank == world - 1 else nl)
+                a = np.asfortranarray(cur[..., lo:hi])
+                b = a.copy(order="F")
+                new = oracle.jacobi(oracle.FArray(a), oracle.FArray(b), k, coeff)
+                res = b if new else a
+                nxt[..., halo:nl - halo] = res[..., halo - lo:nl - halo - lo]
                 cur, nxt = nxt, cur
-            owned = cur[..., 1:nl - 1]
+            owned = cur[..., halo:nl - halo]
             parts = [None] * world
-            dist.all_gather_object(parts, (g0 + 1, owned))
-            out[len(shape)] = parts
+            dist.all_gather_object(parts, (g0 + halo, owned))
+            out[(len(shape), halo)] = parts
         # global SUM: local order-R value of a chunk-aligned slab, all-gather, fixed tree
         n = 4 * 65536 * world
         v = synth.values(n, mode=synth.U11)
@@ -99,7 +115,7 @@ def _worker(rank, world, port, q, shape2, shape3, sweeps):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_distributed_protocol_matches_undivided(world):
-    shape2, shape3, sweeps = (37, 46), (19, 13, 26), 5
+    shape2, shape3, sweeps = (37, 46), (19, 13, 26), 7
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -110,12 +126,12 @@ def test_distributed_protocol_matches_undivided(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for shape, coeff in ((shape2, 0.25), (shape3, 1.0 / 6.0)):
+    for shape, coeff, halo in ((shape2, 0.25, 1), (shape2, 0.25, 3), (shape3, 1.0 / 6.0, 1)):
         full = synth.jacobi_init(shape)
         a, b = full.copy(order="F"), full.copy(order="F")
         new = oracle.jacobi(oracle.FArray(a), oracle.FArray(b), sweeps, coeff)
         ref = b if new else a
-        for first, owned in out[len(shape)]:
+        for first, owned in out[(len(shape), halo)]:
             np.testing.assert_array_equal(owned, ref[..., first:first + owned.shape[-1]])
     n = 4 * 65536 * world
     v = synth.values(n, mode=synth.U11)

@@ -49,44 +49,88 @@ def test_nccl_single_rank_entry_points(ftn, comm):
     u0 = synth.jacobi_init((77, 50))
     U1, W1 = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
     U2, W2 = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
-    n1 = comm.jacobi(U1, W1, 7)
+    n1 = comm.jacobi(U1, W1, 7, halo=1)
     n2 = ftn.jacobi(U2, W2, 7)
     assert n1 == n2
     assert torch.equal((W1 if n1 else U1).tensor, (W2 if n2 else U2).tensor)
 
 
-@pytest.mark.parametrize("p", [2, 3, 4, 8])
-@pytest.mark.parametrize("shape", [(300, 203), (140, 33, 45)])
-def test_jacobi_decomposition_independence(ftn, p, shape):
+def _slabs(u0, p, halo, rng_fill=True):
+    """Local arrays of p slabs with `halo` planes per side (garbage outside the global array)."""
     from paper_2409_18824_b200 import dist as D
-    sweeps = 6
+    nlast = u0.shape[-1]
+    out = []
+    for r in range(p):
+        s = D.slab(nlast - 2, p, r)                 # owned global planes [s.lo+1, s.hi+1)
+        g0 = s.lo + 1 - halo                        # global plane of local plane 0
+        nl = s.owned + 2 * halo
+        part = np.full(u0.shape[:-1] + (nl,), 7.0e300, order="F")   # garbage outside the array
+        for k in range(nl):
+            g = g0 + k
+            if 0 <= g < nlast:
+                part[..., k] = u0[..., g]
+        out.append((g0, nl, s.owned))
+    return out
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("shape,halo", [((300, 203), 1), ((300, 203), 3), ((140, 33, 45), 1), ((130, 301), 4),
+                                        ((129, 201), 2)])
+def test_jacobi_decomposition_independence(ftn, p, shape, halo):
+    """p slabs with `halo` halo planes; k owned planes exchanged per step (device copies standing
+    in for ncclSend/Recv), ftn_jacobi_slab advancing k sweeps; == the undivided ftn_jacobi."""
+    sweeps = 10
     u0 = synth.jacobi_init(shape)
-    nlast = shape[-1]
     U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
     new = ftn.jacobi(U, W, sweeps)
     ref = (W if new else U).to_numpy()
-    slabs = []
-    for r in range(p):
-        g0, nl = D.jacobi_slab(nlast, p, r)
-        part = np.asfortranarray(u0[..., g0:g0 + nl])
-        slabs.append((g0, nl, [ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)]))
+    meta = _slabs(u0, p, halo)
+    arrs = []
+    for (g0, nl, owned) in meta:
+        part = np.full(u0.shape[:-1] + (nl,), 7.0e300, order="F")
+        for k in range(nl):
+            if 0 <= g0 + k < shape[-1]:
+                part[..., k] = u0[..., g0 + k]
+        arrs.append([ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)])
+    tma_able = len(shape) == 2 and (shape[0] * 8) % 16 == 0       # dim-2 stride a multiple of 16 B
+    T = min(ftn.jacobi_fusion(), halo) if tma_able else 1
+    fused = sweeps // T if T > 1 else 0
+    if T % 2 == 0 and fused % 2:
+        fused -= 1
+    steps = [T] * fused + [1] * (sweeps - fused * T)
     cur = 0
-    for _ in range(sweeps):
-        # halo exchange of the current source arrays (ftn_jacobi_dist's protocol)
+    for k in steps:
         for r in range(p):
-            g0, nl, arr = slabs[r]
-            src = arr[cur].tensor
+            g0, nl, owned = meta[r]
+            src = arrs[r][cur].tensor
             if r > 0:
-                src[..., 0].copy_(slabs[r - 1][2][cur].tensor[..., slabs[r - 1][1] - 2])
+                lnl = meta[r - 1][1]
+                src[..., halo - k:halo].copy_(arrs[r - 1][cur].tensor[..., lnl - halo - k:lnl - halo])
             if r < p - 1:
-                src[..., nl - 1].copy_(slabs[r + 1][2][cur].tensor[..., 1])
+                src[..., nl - halo:nl - halo + k].copy_(arrs[r + 1][cur].tensor[..., halo:halo + k])
         for r in range(p):
-            arr = slabs[r][2]
-            ftn.jacobi(arr[cur], arr[1 - cur], 1)
+            ftn.jacobi_slab(arrs[r][cur], arrs[r][1 - cur], k, halo, r == 0, r == p - 1)
         cur = 1 - cur
-    for g0, nl, arr in slabs:
-        got = arr[cur].to_numpy()[..., 1:nl - 1]
-        np.testing.assert_array_equal(got, ref[..., g0 + 1:g0 + nl - 1])
+    assert (cur == 1) == new                       # same result parity as the undivided run
+    for (g0, nl, owned), a in zip(meta, arrs):
+        got = a[cur].to_numpy()[..., halo:halo + owned]
+        np.testing.assert_array_equal(got, ref[..., g0 + halo:g0 + halo + owned])
+
+
+def test_jacobi_dist_single_rank_deep_halo(ftn, comm):
+    """ftn_jacobi_dist at nranks = 1 with halo 3: the global boundary sits at local planes 2 and
+    n_last-3, the planes outside it are garbage that must never be consumed."""
+    u0 = synth.jacobi_init((250, 120))
+    halo = 3
+    part = np.full((250, 120 + 2 * (halo - 1)), 7.0e300, order="F")
+    part[:, halo - 1:halo - 1 + 120] = u0
+    U, W = ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)
+    n1 = comm.jacobi(U, W, 11, halo=halo)
+    R, S = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+    n2 = ftn.jacobi(R, S, 11)
+    assert n1 == n2
+    got = (W if n1 else U).to_numpy()[:, halo - 1:halo - 1 + 120]
+    np.testing.assert_array_equal(got, (S if n2 else R).to_numpy())
 
 
 @pytest.mark.parametrize("p", [2, 4, 8])
