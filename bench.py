@@ -235,6 +235,13 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             fx = ftn.FArray(b.tensor.permute(2, 1, 0).reshape(-1))
             fy = ftn.FArray(c.tensor.permute(2, 1, 0).reshape(-1))
             gbs_row("c4_dot_product", 16 * n_el, lambda: ftn.dot_product(fx, fy, out))
+            # PRODUCT and DIM= reductions (results are 8 MiB: not counted)
+            gbs_row("f1_product", 8 * n_el, lambda: ftn.product(b, out))
+            rd = [ftn.FArray.empty((1024, 1024)) for _ in range(3)]
+            for dd in (1, 2, 3):
+                gbs_row(f"f1_sum_dim{dd}", 8 * n_el, lambda dd=dd: ftn.sum_dim(b, dd, rd[dd - 1]))
+            gbs_row("f1_maxval_dim3", 8 * n_el, lambda: ftn.maxval_dim(b, 3, rd[2]))
+            del rd
         else:
             gbs_row("c4_sum_global", 8 * n_el, lambda: comm.sum(b, out))
             gbs_row("c4_maxval_global", 8 * n_el, lambda: comm.maxval(b, out))

@@ -156,6 +156,23 @@ ftn_status_t ftn_maxval(const ftn_desc_t* x, void* result_dev, void* ws, size_t 
                         ftn_stream_t stream);
 ftn_status_t ftn_minval(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes,
                         ftn_stream_t stream);
+/* PRODUCT(x) ("product ... also implemented"): order R with
+ * multiplication, neutral 1 (empty -> 1); reals within (n-1)*2^-53 relative of the exact
+ * product (each multiply rounds once); integers modulo 2^w.  Workspace as for ftn_sum. */
+ftn_status_t ftn_product(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes,
+                         ftn_stream_t stream);
+
+/* SUM / PRODUCT / MAXVAL / MINVAL (x, DIM=dim) (linalg.reduce with `dimensions`;
+ * SURVEY §8(f) f1).  x: rank 1..3, any strides; dim 1-based.  result: rank(x)-1 descriptor
+ * (rank 0 = one element at base_addr) whose extents are x's without dimension dim, same
+ * type, not overlapping x.  Each result element is the sequential fold over the reduced
+ * subscript in ascending order from the neutral element (R#24), so results are exact
+ * replicas of the paper's loop; MAXVAL/MINVAL NaN and empty rules as above.  No workspace. */
+ftn_status_t ftn_sum_dim(const ftn_desc_t* x, int32_t dim, const ftn_desc_t* result, ftn_stream_t stream);
+ftn_status_t ftn_product_dim(const ftn_desc_t* x, int32_t dim, const ftn_desc_t* result, ftn_stream_t stream);
+ftn_status_t ftn_maxval_dim(const ftn_desc_t* x, int32_t dim, const ftn_desc_t* result, ftn_stream_t stream);
+ftn_status_t ftn_minval_dim(const ftn_desc_t* x, int32_t dim, const ftn_desc_t* result, ftn_stream_t stream);
+
 /* DOT_PRODUCT(x, y) = SUM(x*y) for rank-1 real vectors of equal size (P:298,
  * R#12); each product is rounded, then summed in order R, so the result is
  * bit-identical to ftn_sum of the packed product vector.  Workspace as for

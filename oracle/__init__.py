@@ -24,7 +24,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 I32, I64, F32, F64 = 1, 2, 3, 4
 ADD, SUB, MUL, DIV, MULADD = 1, 2, 3, 4, 5
-SUM, MAX, MIN = 0, 1, 2
+SUM, MAX, MIN, PROD = 0, 1, 2, 3
 R_CHUNK = 65536  # DESIGN.md section 4.2, step 2
 
 _NP2TYPE = {np.dtype(np.int32): I32, np.dtype(np.int64): I64,
@@ -89,6 +89,9 @@ def lib():
             "orc_matmul_element_f64": (ctypes.c_double, [P, P, ctypes.c_int64, ctypes.c_int64, dp]),
             "orc_jacobi_f64": (ctypes.c_int, [P, P, ctypes.c_int64, ctypes.c_double,
                                               ctypes.POINTER(ctypes.c_int32)]),
+            "orc_product_seq_f64": (ctypes.c_double, [P]),
+            "orc_product_int": (ctypes.c_int64, [P]),
+            "orc_reduce_dim": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -304,3 +307,19 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float) -> bool:
 
 JACOBI_C2 = 0.25
 JACOBI_C3 = 1.0 / 6.0  # fl(1/6) = 0x1.5555555555555p-3 (R#23)
+
+
+def product_seq(x: FArray) -> float:
+    return lib().orc_product_seq_f64(x.ref())
+
+
+def product_int(x: FArray) -> int:
+    return lib().orc_product_int(x.ref())
+
+
+def reduce_dim(x: FArray, dim: int, kind: int) -> np.ndarray:
+    """SUM/MAXVAL/MINVAL/PRODUCT(x, DIM=dim) as a new Fortran-ordered array (0-d for rank 1)."""
+    shape = tuple(e for d, e in enumerate(x.shape) if d != dim - 1)
+    out = np.zeros(shape, dtype=x.owner.dtype, order="F")
+    _check(lib().orc_reduce_dim(x.ref(), dim, kind, FArray(out).ref()), "reduce_dim")
+    return out

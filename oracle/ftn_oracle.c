@@ -383,6 +383,15 @@ static double add_f(double a, double b) { return a + b; }
 /* maxNum/minNum: a NaN operand is ignored unless both are NaN (R#11). */
 static double max_f(double a, double b) { if (isnan(a)) return b; if (isnan(b)) return a; return a > b ? a : b; }
 static double min_f(double a, double b) { if (isnan(a)) return b; if (isnan(b)) return a; return a < b ? a : b; }
+static double mul_f(double a, double b) { return a * b; }
+
+/* kind: 0 SUM, 1 MAXVAL, 2 MINVAL, 3 PRODUCT */
+static combine_fn kind_fn(int32_t kind) {
+  return kind == 0 ? add_f : (kind == 1 ? max_f : (kind == 2 ? min_f : mul_f));
+}
+static double kind_neutral(int32_t kind) {
+  return kind == 0 ? 0.0 : (kind == 1 ? -INFINITY : (kind == 2 ? INFINITY : 1.0));
+}
 
 static double chunk_partial(const double* v, int64_t n, int64_t c, combine_fn f, double neutral) {
   double thread_val[R_THREADS];
@@ -415,8 +424,8 @@ static double chunk_partial(const double* v, int64_t n, int64_t c, combine_fn f,
 
 /* Balanced adjacent-pair tree over p[0..n-1], padded with pad to a power of two. */
 double orc_tree_combine(const double* p, int64_t n, int32_t kind) {
-  combine_fn f = kind == 0 ? add_f : (kind == 1 ? max_f : min_f);
-  const double pad = kind == 0 ? 0.0 : (kind == 1 ? -INFINITY : INFINITY);
+  combine_fn f = kind_fn(kind);
+  const double pad = kind_neutral(kind);
   if (n <= 0) return pad;
   int64_t m = 1;
   while (m < n) m *= 2;
@@ -433,8 +442,8 @@ double orc_tree_combine(const double* p, int64_t n, int32_t kind) {
 
 /* Chunk partials of order R (steps 1-5) over a packed vector. */
 void orc_orderR_partials(const double* v, int64_t n, int32_t kind, double* partials) {
-  combine_fn f = kind == 0 ? add_f : (kind == 1 ? max_f : min_f);
-  const double neutral = kind == 0 ? 0.0 : (kind == 1 ? -INFINITY : INFINITY);
+  combine_fn f = kind_fn(kind);
+  const double neutral = kind_neutral(kind);
   const int64_t nc = (n + R_CHUNK - 1) / R_CHUNK;
   for (int64_t c = 0; c < nc; ++c) partials[c] = chunk_partial(v, n, c, f, neutral);
 }
@@ -447,7 +456,8 @@ static double* pack_f64(const orc_array* x, int64_t* n_out) {
   return v;
 }
 
-/* kind: 0 = SUM, 1 = MAXVAL, 2 = MINVAL */
+/* kind: 0 = SUM, 1 = MAXVAL, 2 = MINVAL, 3 = PRODUCT ("a range of other Fortran
+ * array intrinsics such as maxval and product are also implemented" the same way) */
 double orc_reduce_orderR_f64(const orc_array* x, int32_t kind) {
   int64_t n;
   double* v = pack_f64(x, &n);
@@ -658,5 +668,93 @@ int orc_jacobi_f64(const orc_array* u0, const orc_array* unew0, int64_t sweeps, 
     const orc_array* tmp = u; u = w; w = tmp;   /* u = unew */
   }
   *result_in_unew = (int32_t)(sweeps % 2 == 1);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* PRODUCT by definition: the sequential fold p = 1; p = p * x(t) in element */
+/* order (reals); integers modulo 2^w.                                      */
+/* ------------------------------------------------------------------------ */
+double orc_product_seq_f64(const orc_array* x) {
+  const int64_t n = total_size(x);
+  double p = 1.0;
+  for (int64_t t = 0; t < n; ++t) p = p * *(const double*)addr_linear(x, t);
+  return p;
+}
+int64_t orc_product_int(const orc_array* x) {
+  const int64_t n = total_size(x);
+  if (x->type == ORC_I32) {
+    uint32_t p = 1;
+    for (int64_t t = 0; t < n; ++t) p *= *(const uint32_t*)addr_linear(x, t);
+    return (int64_t)(int32_t)p;
+  }
+  uint64_t p = 1;
+  for (int64_t t = 0; t < n; ++t) p *= *(const uint64_t*)addr_linear(x, t);
+  return (int64_t)p;
+}
+
+/* ------------------------------------------------------------------------ */
+/* SUM / MAXVAL / MINVAL / PRODUCT (x, DIM=dim)  (linalg.reduce with a    */
+/* `dimensions` attribute).  The result has x's shape with       */
+/* dimension dim (1-based) removed; result element o is the sequential fold over   */
+/* the reduced subscript in ascending order, starting from the neutral element     */
+/* (R#24).  MAXVAL/MINVAL: NaN ignored unless all are NaN; an empty reduced        */
+/* dimension gives the R#10 value.  result: rank(x)-1 (rank 0 = one element).      */
+/* ------------------------------------------------------------------------ */
+int orc_reduce_dim(const orc_array* x, int32_t dim, int32_t kind, const orc_array* result) {
+  if (x->rank < 1 || dim < 1 || dim > x->rank) return ORC_ERANK;
+  if (result->rank != x->rank - 1 || result->type != x->type) return ORC_ESHAPE;
+  int64_t kept_ext[ORC_MAXRANK] = {1, 1, 1}, kept_sm[ORC_MAXRANK] = {0, 0, 0};
+  int nk = 0;
+  for (int d = 0; d < x->rank; ++d) {
+    if (d == dim - 1) continue;
+    if (result->dim[nk].ext != x->dim[d].ext) return ORC_ESHAPE;
+    kept_ext[nk] = x->dim[d].ext;
+    kept_sm[nk] = x->dim[d].sm;
+    ++nk;
+  }
+  const int64_t n = x->dim[dim - 1].ext, step = x->dim[dim - 1].sm;
+  int64_t nout = 1;
+  for (int d = 0; d < nk; ++d) nout *= kept_ext[d];
+  int64_t k[ORC_MAXRANK] = {0, 0, 0};
+  for (int64_t o = 0; o < nout; ++o) {
+    const char* xp = x->base;
+    char* rp = result->base;
+    for (int d = 0; d < nk; ++d) { xp += k[d] * kept_sm[d]; rp += k[d] * result->dim[d].sm; }
+    if (x->type == ORC_F64) {
+      double acc;
+      if (kind == 1 || kind == 2) {
+        if (n == 0) acc = kind == 1 ? -INFINITY : INFINITY;
+        else {
+          acc = NAN;
+          combine_fn f = kind_fn(kind);
+          for (int64_t j = 0; j < n; ++j) acc = f(acc, *(const double*)(xp + j * step));
+        }
+      } else {
+        acc = kind_neutral(kind);
+        combine_fn f = kind_fn(kind);
+        for (int64_t j = 0; j < n; ++j) acc = f(acc, *(const double*)(xp + j * step));
+      }
+      *(double*)rp = acc;
+    } else if (x->type == ORC_I32 || x->type == ORC_I64) {
+      const int w32 = x->type == ORC_I32;
+      uint64_t acc = kind == 0 ? 0 : (kind == 3 ? 1 : 0);
+      int64_t best = kind == 1 ? (w32 ? INT32_MIN : INT64_MIN) : (w32 ? INT32_MAX : INT64_MAX);
+      for (int64_t j = 0; j < n; ++j) {
+        const char* e = xp + j * step;
+        const int64_t v = w32 ? (int64_t)*(const int32_t*)e : *(const int64_t*)e;
+        if (kind == 0) acc += (uint64_t)v;
+        else if (kind == 3) acc *= (uint64_t)v;
+        else if (kind == 1) { if (v > best) best = v; }
+        else { if (v < best) best = v; }
+      }
+      const int64_t r = (kind == 0 || kind == 3) ? (int64_t)acc : best;
+      if (w32) *(int32_t*)rp = (int32_t)(uint32_t)(uint64_t)r;
+      else *(int64_t*)rp = r;
+    } else {
+      return ORC_ETYPE;
+    }
+    for (int d = 0; d < nk; ++d) { if (++k[d] < kept_ext[d]) break; k[d] = 0; }
+  }
   return ORC_OK;
 }

@@ -43,6 +43,8 @@ __device__ __forceinline__ typename Acc<T>::type neutral() {
   typedef typename Acc<T>::type A;
   if constexpr (KIND == RK_SUM || KIND == RK_DOT) {
     return A(0);
+  } else if constexpr (KIND == RK_PROD) {
+    return A(1);
   } else if constexpr (std::is_floating_point<T>::value) {
     return NAN;  // maxNum/minNum ignore NaN: an all-NaN (or empty) combine stays NaN (R#11)
   } else {
@@ -63,6 +65,8 @@ template <typename T, int KIND>
 __device__ __forceinline__ typename Acc<T>::type combine(typename Acc<T>::type a, typename Acc<T>::type b) {
   if constexpr (KIND == RK_SUM || KIND == RK_DOT) {
     return a + b;  // fp: one IEEE add (RN); ints: modulo 2^w
+  } else if constexpr (KIND == RK_PROD) {
+    return a * b;  // fp: one IEEE multiply (RN); ints: modulo 2^w
   } else if constexpr (std::is_floating_point<T>::value) {
     return KIND == RK_MAX ? fmax(a, b) : fmin(a, b);  // maxNum: NaN ignored (R#11)
   } else {
@@ -289,6 +293,7 @@ ftn_status_t by_kind(int kind, const RParams& p, bool flat, bool vec, void* resu
     case RK_SUM: return launch_reduce<T, RK_SUM>(p, flat, vec, result, ws, s);
     case RK_MAX: return launch_reduce<T, RK_MAX>(p, flat, vec, result, ws, s);
     case RK_MIN: return launch_reduce<T, RK_MIN>(p, flat, vec, result, ws, s);
+    case RK_PROD: return launch_reduce<T, RK_PROD>(p, flat, vec, result, ws, s);
   }
   return fail(FTN_ERR_UNSUPPORTED, "reduce kind");
 }
@@ -374,6 +379,10 @@ static ftn_status_t reduce_entry(int kind, const char* name, const ftn_desc_t* x
 }
 
 extern "C" {
+
+ftn_status_t ftn_product(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes, ftn_stream_t stream) {
+  return reduce_entry(RK_PROD, "ftn_product", x, result_dev, ws, ws_bytes, stream);
+}
 
 ftn_status_t ftn_reduce_workspace_size(const ftn_desc_t* x, size_t* bytes) {
   FTN_CHECK(check_desc(x, "ftn_reduce_workspace_size", 1, FTN_MAX_RANK));

@@ -73,6 +73,11 @@ def _load():
         "ftn_maxval": [P, vp, vp, ctypes.c_size_t, vp],
         "ftn_minval": [P, vp, vp, ctypes.c_size_t, vp],
         "ftn_dot_product": [P, P, vp, vp, ctypes.c_size_t, vp],
+        "ftn_product": [P, vp, vp, ctypes.c_size_t, vp],
+        "ftn_sum_dim": [P, ctypes.c_int32, P, vp],
+        "ftn_product_dim": [P, ctypes.c_int32, P, vp],
+        "ftn_maxval_dim": [P, ctypes.c_int32, P, vp],
+        "ftn_minval_dim": [P, ctypes.c_int32, P, vp],
         "ftn_transpose": [P, P, vp],
         "ftn_matmul_workspace_size": [P, P, P, szp],
         "ftn_matmul": [P, P, P, vp, ctypes.c_size_t, vp],
@@ -318,6 +323,36 @@ def maxval(x: FArray, out=None, stream=None) -> torch.Tensor:
 
 def minval(x: FArray, out=None, stream=None) -> torch.Tensor:
     return _reduce("ftn_minval", x, out, stream)
+
+
+def product(x: FArray, out=None, stream=None) -> torch.Tensor:
+    return _reduce("ftn_product", x, out, stream)
+
+
+def _reduce_dim(name, x: FArray, dim: int, out: FArray | None = None, stream=None) -> FArray:
+    if out is None:
+        shape = tuple(e for d, e in enumerate(x.shape) if d != dim - 1)
+        out = FArray.empty(shape, dtype=x.dtype, device=x.tensor.device) if shape else \
+            FArray(torch.empty((), dtype=x.dtype, device=x.tensor.device))
+    _call(name, x.ref(), dim, out.ref(), _stream(stream))
+    return out
+
+
+def sum_dim(x: FArray, dim: int, out=None, stream=None) -> FArray:
+    """SUM(x, DIM=dim): sequential fold along dim (R#24)."""
+    return _reduce_dim("ftn_sum_dim", x, dim, out, stream)
+
+
+def product_dim(x: FArray, dim: int, out=None, stream=None) -> FArray:
+    return _reduce_dim("ftn_product_dim", x, dim, out, stream)
+
+
+def maxval_dim(x: FArray, dim: int, out=None, stream=None) -> FArray:
+    return _reduce_dim("ftn_maxval_dim", x, dim, out, stream)
+
+
+def minval_dim(x: FArray, dim: int, out=None, stream=None) -> FArray:
+    return _reduce_dim("ftn_minval_dim", x, dim, out, stream)
 
 
 def dot_product(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:
