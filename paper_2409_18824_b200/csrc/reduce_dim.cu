@@ -97,26 +97,35 @@ constexpr int RB_WARPS = 4;  // 4 x 32 x 33 x 8 B = 33.8 KB static shared memory
 template <typename T, int KIND>
 __global__ void __launch_bounds__(RB_WARPS * 32) reduce_dim_leading(const __grid_constant__ RDParams p) {
   __shared__ T tile[RB_WARPS][32][33];
+  __shared__ const char* rowbase[RB_WARPS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ngroups = (p.nout + 31) / 32;
   for (int64_t g = blockIdx.x * (int64_t)RB_WARPS + warp; g < ngroups; g += (int64_t)gridDim.x * RB_WARPS) {
     const int64_t o0 = g * 32;
     const int64_t my = o0 + lane;  // this lane's result element
     const int64_t mk0 = my % p.ke[0], mk1 = my / p.ke[0];
-    const char* mybase = p.x + mk0 * p.ks[0] + mk1 * p.ks[1];
     const int rows = (int)min((int64_t)32, p.nout - o0);
+    __syncwarp();
+    rowbase[warp][lane] = p.x + mk0 * p.ks[0] + mk1 * p.ks[1];
+    __syncwarp();
     T acc = init_val<T, KIND>();
     for (int64_t j0 = 0; j0 < p.n; j0 += 32) {
       const int64_t j = j0 + lane;
-#pragma unroll 4
-      for (int rr = 0; rr < 32; ++rr) {
-        const char* rb = reinterpret_cast<const char*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mybase), rr));
-        if (rr < rows && j < p.n) tile[warp][rr][lane] = *reinterpret_cast<const T*>(rb + j * p.step);
-      }
+      const bool jok = j < p.n;
+      T v[32];
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr)  // 32 independent coalesced row loads in flight
+        v[rr] = (rr < rows && jok) ? *reinterpret_cast<const T*>(rowbase[warp][rr] + j * p.step) : T(0);
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) tile[warp][rr][lane] = v[rr];
       __syncwarp();
       const int cnt = (int)min((int64_t)32, p.n - j0);
-      for (int jj = 0; jj < cnt; ++jj) acc = fold<T, KIND>(acc, tile[warp][lane][jj]);
+      if (cnt == 32) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) acc = fold<T, KIND>(acc, tile[warp][lane][jj]);
+      } else {
+        for (int jj = 0; jj < cnt; ++jj) acc = fold<T, KIND>(acc, tile[warp][lane][jj]);
+      }
       __syncwarp();
     }
     if (my < p.nout) *reinterpret_cast<T*>(p.r + mk0 * p.rs[0] + mk1 * p.rs[1]) = finish<T, KIND>(acc, p.n);
