@@ -280,6 +280,18 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             Ac, Bc = A.tensor, B.tensor
             tc = timed(torch, lambda: torch.matmul(Ac, Bc), 3, 1, None, None)
             rows["c3_matmul_8192"]["cublas_dgemm_tflops_context"] = 2.0 * n ** 3 * 3 / tc / 1e12
+            # MATMUL(TRANSPOSE(a), b) without forming the transpose, and the
+            # rank-1 forms (HBM-bound: 8 B per matrix element)
+            t = timed(torch, lambda: ftn.matmul(C, A, B, transpose_a=True), steps, warm, None, None)
+            tf = 2.0 * n ** 3 * steps / t / 1e12
+            rows["f3_matmul_transpose_a_8192"] = {"value": tf, "unit": "TFLOP/s", "ms": t / steps * 1e3,
+                                                  "roofline": {"bound": "fp64 tensor (DMMA)",
+                                                               "frac": tf / FP64_PEAK_TFLOPS}}
+            xv, yv = ftn.FArray.empty((n,)), ftn.FArray.empty((n,))
+            ftn.gen_fill(xv, SEED, 9, ftn.GEN_U11)
+            gbs_row("f3_matvec_8192", 8 * n * n, lambda: ftn.matmul(yv, A, xv))
+            gbs_row("f3_vecmat_8192", 8 * n * n, lambda: ftn.matmul(yv, xv, A))
+            del xv, yv
         del A, B, C
         torch.cuda.empty_cache()
 

@@ -187,19 +187,30 @@ ftn_status_t ftn_dot_product(const ftn_desc_t* x, const ftn_desc_t* y, void* res
 ftn_status_t ftn_transpose(const ftn_desc_t* dst, const ftn_desc_t* src, ftn_stream_t stream);
 
 /* ---------------------------------------------------------------- a6
- * c = MATMUL(a, b) for real(8) rank-2 operands:
- * c(i,j) = sum_l a(i,l) b(l,j); a (m,k), b (k,n), c (m,n).  Computed on the
- * fp64 tensor cores (DMMA); the per-element summation order inside a tensor
- * core step is the hardware's, so the result is within 4*k*2^-53*sum|a||b|
- * of the exact value (R#8, R#14), and exact when all partial sums are
- * representable (integer-valued data).  Operands that are not TMA-able
- * (dim-1 stride != 8 bytes, a column stride that is not a multiple of 16
- * bytes, a base that is not 16-byte aligned) are first packed into ws.
- * c must not overlap a or b.  Rank-1 forms: FTN_ERR_UNSUPPORTED. */
+ * c = MATMUL(a, b) for real(8) operands (F2018 16.9.124):
+ *   rank 2 x rank 2: c(i,j) = sum_l a(i,l) b(l,j), a (m,k), b (k,n), c (m,n), computed on the
+ *     fp64 tensor cores (DMMA); the per-element summation order inside a tensor-core step is
+ *     the hardware's, so c is within 4*k*2^-53*sum|a||b| of the exact value (R#8, R#14) and
+ *     exact when all partial sums are representable (integer-valued data);
+ *   rank 2 x rank 1: c(i) = sum_l a(i,l) b(l) (m);  rank 1 x rank 2: c(j) = sum_l a(l) b(l,j)
+ *     (n) -- HBM-bound kernels, same bound.
+ * Rank-2 operands that are not TMA-able (dim-1 stride != 8 bytes, a column stride that is
+ * not a multiple of 16 bytes, a base that is not 16-byte aligned) are first packed into ws.
+ * An overlapping c is computed through a temporary (R#5). */
 ftn_status_t ftn_matmul_workspace_size(const ftn_desc_t* c, const ftn_desc_t* a,
                                        const ftn_desc_t* b, size_t* bytes);
 ftn_status_t ftn_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws,
                         size_t ws_bytes, ftn_stream_t stream);
+
+/* c = MATMUL(op(a), op(b)) with op = TRANSPOSE when the flag is set, for rank-2 operands,
+ * without materialising the transpose (the TMA boxes and fragment addressing swap roles;
+ * SURVEY §8(f) f3).  Workspace: ftn_matmul_ex_workspace_size. */
+#define FTN_MATMUL_TRANSPOSE_A 1u
+#define FTN_MATMUL_TRANSPOSE_B 2u
+ftn_status_t ftn_matmul_ex_workspace_size(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b,
+                                          uint32_t flags, size_t* bytes);
+ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags,
+                           void* ws, size_t ws_bytes, ftn_stream_t stream);
 
 /* ---------------------------------------------------------------- a7
  * Jacobi sweeps ("a Jacobi iteration solving Laplace's equation"; the

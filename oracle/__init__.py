@@ -92,6 +92,8 @@ def lib():
             "orc_product_seq_f64": (ctypes.c_double, [P]),
             "orc_product_int": (ctypes.c_int64, [P]),
             "orc_reduce_dim": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int32, P]),
+            "orc_matvec_f64": (ctypes.c_int, [P, P, P, P]),
+            "orc_vecmat_f64": (ctypes.c_int, [P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -323,3 +325,19 @@ def reduce_dim(x: FArray, dim: int, kind: int) -> np.ndarray:
     out = np.zeros(shape, dtype=x.owner.dtype, order="F")
     _check(lib().orc_reduce_dim(x.ref(), dim, kind, FArray(out).ref()), "reduce_dim")
     return out
+
+
+def matvec(a: FArray, x: FArray) -> tuple[np.ndarray, np.ndarray]:
+    """MATMUL(a(m,k), x(k)) and sum |a(i,l) x(l)| per element."""
+    m = a.shape[0]
+    y, t = np.zeros(m), np.zeros(m)
+    _check(lib().orc_matvec_f64(FArray(y).ref(), a.ref(), x.ref(), FArray(t).ref()), "matvec")
+    return y, t
+
+
+def vecmat(x: FArray, b: FArray) -> tuple[np.ndarray, np.ndarray]:
+    """MATMUL(x(k), b(k,n)) and sum |x(l) b(l,j)| per element."""
+    n = b.shape[1]
+    y, t = np.zeros(n), np.zeros(n)
+    _check(lib().orc_vecmat_f64(FArray(y).ref(), x.ref(), b.ref(), FArray(t).ref()), "vecmat")
+    return y, t

@@ -758,3 +758,43 @@ int orc_reduce_dim(const orc_array* x, int32_t dim, int32_t kind, const orc_arra
   }
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* MATMUL rank-1 forms (F2018: MATMUL(matrix_a(m,k), vector_b(k)) has shape  */
+/* (m) and MATMUL(vector_a(k), matrix_b(k,n)) has shape (n)):      */
+/*   y(i) = sum_{l=1..k} a(i,l) x(l)      y(j) = sum_{l=1..k} x(l) b(l,j)            */
+/* l ascending from 0, each product rounded then added; absum = sum |products|.     */
+/* ------------------------------------------------------------------------ */
+int orc_matvec_f64(const orc_array* y, const orc_array* a, const orc_array* x, const orc_array* absum) {
+  if (a->rank != 2 || x->rank != 1 || y->rank != 1) return ORC_ERANK;
+  const int64_t m = a->dim[0].ext, k = a->dim[1].ext;
+  if (x->dim[0].ext != k || y->dim[0].ext != m) return ORC_ESHAPE;
+  for (int64_t i = 0; i < m; ++i) {
+    double s = 0.0, t = 0.0;
+    for (int64_t l = 0; l < k; ++l) {
+      const double p = AT(a, i, l) * *(const double*)(x->base + l * x->dim[0].sm);
+      s = s + p;
+      t = t + fabs(p);
+    }
+    *(double*)(y->base + i * y->dim[0].sm) = s;
+    if (absum) *(double*)(absum->base + i * absum->dim[0].sm) = t;
+  }
+  return ORC_OK;
+}
+
+int orc_vecmat_f64(const orc_array* y, const orc_array* x, const orc_array* b, const orc_array* absum) {
+  if (b->rank != 2 || x->rank != 1 || y->rank != 1) return ORC_ERANK;
+  const int64_t k = b->dim[0].ext, n = b->dim[1].ext;
+  if (x->dim[0].ext != k || y->dim[0].ext != n) return ORC_ESHAPE;
+  for (int64_t j = 0; j < n; ++j) {
+    double s = 0.0, t = 0.0;
+    for (int64_t l = 0; l < k; ++l) {
+      const double p = *(const double*)(x->base + l * x->dim[0].sm) * AT(b, l, j);
+      s = s + p;
+      t = t + fabs(p);
+    }
+    *(double*)(y->base + j * y->dim[0].sm) = s;
+    if (absum) *(double*)(absum->base + j * absum->dim[0].sm) = t;
+  }
+  return ORC_OK;
+}

@@ -59,6 +59,10 @@ __device__ __forceinline__ void dmma(double* d, double a0, double a1, double b0)
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// TA: the A operand is TRANSPOSE(a) with a (k, m) column-major (k fastest); TB: the B operand
+// is TRANSPOSE(b) with b (n, k).  The boxes then carry the k index along their 16-element
+// rows instead of across them, and the fragment addresses swap roles (same bank analysis).
+template <bool TA, bool TB>
 __global__ void __launch_bounds__(THREADS, 1)
     dmma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ MParams p) {
@@ -95,11 +99,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* st = smem + s * STAGE_BYTES;
     dev::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
     const int k0 = kt * BK;
+    if constexpr (!TA) {
 #pragma unroll
-    for (int a = 0; a < BM / 16; ++a) dev::tma_load_2d(st + a * A_BOX_BYTES, &map_a, &full[s], m0 + 16 * a, k0);
+      for (int a = 0; a < BM / 16; ++a) dev::tma_load_2d(st + a * A_BOX_BYTES, &map_a, &full[s], m0 + 16 * a, k0);
+    } else {
 #pragma unroll
-    for (int h = 0; h < BK / 16; ++h)
-      dev::tma_load_2d(st + A_STAGE + h * B_BOX_BYTES, &map_b, &full[s], k0 + 16 * h, n0);
+      for (int h = 0; h < BK / 16; ++h) dev::tma_load_2d(st + h * B_BOX_BYTES, &map_a, &full[s], k0 + 16 * h, m0);
+    }
+    if constexpr (!TB) {
+#pragma unroll
+      for (int h = 0; h < BK / 16; ++h)
+        dev::tma_load_2d(st + A_STAGE + h * B_BOX_BYTES, &map_b, &full[s], k0 + 16 * h, n0);
+    } else {
+#pragma unroll
+      for (int a = 0; a < BN / 16; ++a)
+        dev::tma_load_2d(st + A_STAGE + a * A_BOX_BYTES, &map_b, &full[s], n0 + 16 * a, k0);
+    }
   };
   const bool producer = (warp == 0 && lane == 0);
   if (producer) {
@@ -133,12 +148,25 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t l = tphys + 2 * q;  // row within an 8-block
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
-      const uint32_t box = wm * 4 + mt;
-      a_off[q][mt][0] = box * A_BOX_BYTES + swz(l, g);
-      a_off[q][mt][1] = box * A_BOX_BYTES + swz(l, g + 8);
+      if constexpr (!TA) {  // boxes of 16 rows (i) x 32 (l): row = l, element = i
+        const uint32_t box = wm * 4 + mt;
+        a_off[q][mt][0] = box * A_BOX_BYTES + swz(l, g);
+        a_off[q][mt][1] = box * A_BOX_BYTES + swz(l, g + 8);
+      } else {              // boxes of 16 (l) x 128 (i): row = i, element = l
+        const uint32_t i = wm * 64 + mt * 16 + g;
+        a_off[q][mt][0] = swz(i, l);
+        a_off[q][mt][1] = swz(i + 8, l);
+      }
     }
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) b_off[q][nt] = A_STAGE + swz(wn * 32 + nt * 8 + g, l);
+    for (int nt = 0; nt < 4; ++nt) {
+      if constexpr (!TB) {  // boxes of 16 (l) x 128 (j): row = j, element = l
+        b_off[q][nt] = A_STAGE + swz(wn * 32 + nt * 8 + g, l);
+      } else {              // boxes of 16 (j) x 32 (l): row = l, element = j
+        const uint32_t box = wn * 2 + (nt >> 1);
+        b_off[q][nt] = A_STAGE + box * A_BOX_BYTES + swz(l, (nt & 1) * 8 + g);
+      }
+    }
   }
 
   for (int kt = 0; kt < p.kt; ++kt) {
@@ -151,16 +179,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kb = 0; kb < BK / 8; ++kb) {
       // A: row l = kb*8 + phys -> +kb*8 rows (the swizzle phase (row & 7) is unchanged)
       // B: x = (kb & 1) * 8 + phys in box kb >> 1 -> +8 doubles = +4 chunks: XOR by 4 commutes
-      const uint32_t a_kb = kb * 8 * 128;
-      const uint32_t b_kb = (kb >> 1) * B_BOX_BYTES;
-      const uint32_t b_x = (kb & 1) ? 64u : 0u;  // chunk index ^ 4 == byte offset ^ 64
+      // rows carry l (MK / NK layouts): +kb*8 rows; elements carry l (KM / KN): box kb>>1, chunk ^ 4
+      const uint32_t a_kb = TA ? (kb >> 1) * B_BOX_BYTES : kb * 8 * 128;
+      const uint32_t a_x = TA ? ((kb & 1) ? 64u : 0u) : 0u;
+      const uint32_t b_kb = TB ? kb * 8 * 128 : (kb >> 1) * B_BOX_BYTES;
+      const uint32_t b_x = TB ? 0u : ((kb & 1) ? 64u : 0u);  // chunk index ^ 4 == byte offset ^ 64
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         double af[4][2], bf[4];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
-          af[mt][0] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + a_off[q][mt][0]);
-          af[mt][1] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + a_off[q][mt][1]);
+          af[mt][0] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][0] ^ a_x));
+          af[mt][1] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][1] ^ a_x));
         }
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
@@ -219,8 +249,27 @@ ftn_status_t make_map(CUtensorMap* map, const ftn_desc_t* d, uint32_t box0, uint
                     CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, char* ws, cudaStream_t s) {
-  const int64_t M = a->dim[0].extent, K = a->dim[1].extent, N = b->dim[1].extent;
+template <bool TA, bool TB>
+ftn_status_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const MParams& p, cudaStream_t s) {
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    FTN_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SMEM_BYTES));
+    attr_set[dev & 63] = true;
+  }
+  const int64_t tiles = p.tiles_m * p.tiles_n;
+  dmma_gemm_kernel<TA, TB><<<(unsigned)tiles, THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  return after_launch("dmma_gemm_kernel");
+}
+
+// c = MATMUL(op(a), op(b)), op = TRANSPOSE when ta / tb.  op(a) is (M, K), op(b) is (K, N).
+ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
+                        cudaStream_t s) {
+  const int64_t M = ta ? a->dim[1].extent : a->dim[0].extent;
+  const int64_t K = ta ? a->dim[0].extent : a->dim[1].extent;
+  const int64_t N = tb ? b->dim[0].extent : b->dim[1].extent;
   if (M == 0 || N == 0) return FTN_OK;
   if (K == 0) {
     const double zero = 0.0;
@@ -237,9 +286,11 @@ ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
     w = (char*)(((uintptr_t)w + 255) & ~uintptr_t(255));
     FTN_CHECK(pack(b, w, &bp, s));
   }
+  // boxes: A (M,K) {16 (i), BK}; TRANSPOSE(a) from a (K,M) {16 (l), BM};
+  //        B (K,N) {16 (l), BN}; TRANSPOSE(b) from b (N,K) {16 (j), BK}
   CUtensorMap ma, mb;
-  FTN_CHECK(make_map(&ma, &ap, 16, BK));
-  FTN_CHECK(make_map(&mb, &bp, 16, BN));
+  FTN_CHECK(make_map(&ma, &ap, 16, ta ? BM : BK));
+  FTN_CHECK(make_map(&mb, &bp, 16, tb ? BK : BN));
   MParams p;
   p.c = (char*)c->base_addr;
   p.c_sm0 = c->dim[0].sm;
@@ -250,47 +301,241 @@ ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
   p.tiles_m = (M + BM - 1) / BM;
   p.tiles_n = (N + BN - 1) / BN;
   p.kt = (int)((K + BK - 1) / BK);
-  static bool attr_set[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!attr_set[dev & 63]) {
-    FTN_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set[dev & 63] = true;
+  if (!ta && !tb) return launch_gemm<false, false>(ma, mb, p, s);
+  if (ta && !tb) return launch_gemm<true, false>(ma, mb, p, s);
+  if (!ta && tb) return launch_gemm<false, true>(ma, mb, p, s);
+  return launch_gemm<true, true>(ma, mb, p, s);
+}
+
+// ---------------------------------------------------------------- rank-1 forms
+// y(i) = sum_l a(i,l) x(l): blocks of 256 rows x LC columns; each thread folds its row
+// over the column chunk in l order (coalesced over i), partials per chunk go to ws and are
+// added in chunk order by a second kernel.  HBM-bound on a: 8 B per element.
+constexpr int MV_ROWS = 256;
+constexpr int MV_MAXLC = 2048;
+
+struct MVParams {
+  const char* a;
+  int64_t a_sm0, a_sm1;
+  const char* x;
+  int64_t x_sm;
+  char* y;
+  int64_t y_sm;
+  double* part;  // [nch][m]
+  int64_t m, k, lc, nch;
+};
+
+__global__ void __launch_bounds__(MV_ROWS) matvec_kernel(const __grid_constant__ MVParams p) {
+  __shared__ double xs[MV_MAXLC];
+  const int64_t rb = blockIdx.x, ch = blockIdx.y;
+  const int64_t l0 = ch * p.lc, l1 = min(l0 + p.lc, p.k);
+  for (int64_t l = l0 + threadIdx.x; l < l1; l += blockDim.x) xs[l - l0] = *reinterpret_cast<const double*>(p.x + l * p.x_sm);
+  __syncthreads();
+  const int64_t i = rb * MV_ROWS + threadIdx.x;
+  if (i >= p.m) return;
+  const char* ap = p.a + i * p.a_sm0;
+  double acc = 0.0;
+  int64_t l = l0;
+  for (; l + 8 <= l1; l += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double*>(ap + (l + u) * p.a_sm1);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double prod = v[u] * xs[l + u - l0];
+      acc = acc + prod;
+    }
   }
-  const int64_t tiles = p.tiles_m * p.tiles_n;
-  dmma_gemm_kernel<<<(unsigned)tiles, THREADS, SMEM_BYTES, s>>>(ma, mb, p);
-  return after_launch("dmma_gemm_kernel");
+  for (; l < l1; ++l) {
+    const double prod = *reinterpret_cast<const double*>(ap + l * p.a_sm1) * xs[l - l0];
+    acc = acc + prod;
+  }
+  if (p.nch == 1) *reinterpret_cast<double*>(p.y + i * p.y_sm) = acc;
+  else p.part[ch * p.m + i] = acc;
+}
+
+__global__ void matvec_combine(const __grid_constant__ MVParams p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.m; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t c = 0; c < p.nch; ++c) acc = acc + p.part[c * p.m + i];
+    *reinterpret_cast<double*>(p.y + i * p.y_sm) = acc;
+  }
+}
+
+int64_t matvec_chunks(int64_t m, int64_t k) {
+  const int64_t rblocks = (m + MV_ROWS - 1) / MV_ROWS;
+  int64_t nch = (148 * 8 + rblocks - 1) / rblocks;        // >= 8 blocks per SM
+  if (nch < (k + MV_MAXLC - 1) / MV_MAXLC) nch = (k + MV_MAXLC - 1) / MV_MAXLC;
+  int64_t lc = (k + nch - 1) / nch;
+  if (lc < 64) lc = 64;
+  return (k + lc - 1) / lc;
+}
+
+ftn_status_t run_matvec(const ftn_desc_t* y, const ftn_desc_t* a, const ftn_desc_t* x, char* ws, cudaStream_t s) {
+  MVParams p;
+  p.a = (const char*)a->base_addr;
+  p.a_sm0 = a->dim[0].sm;
+  p.a_sm1 = a->dim[1].sm;
+  p.x = (const char*)x->base_addr;
+  p.x_sm = x->dim[0].sm;
+  p.y = (char*)y->base_addr;
+  p.y_sm = y->dim[0].sm;
+  p.m = a->dim[0].extent;
+  p.k = a->dim[1].extent;
+  if (p.m == 0) return FTN_OK;
+  if (p.k == 0) {
+    const double zero = 0.0;
+    return ftn_fill(y, &zero, s);
+  }
+  p.nch = matvec_chunks(p.m, p.k);
+  p.lc = (p.k + p.nch - 1) / p.nch;
+  p.nch = (p.k + p.lc - 1) / p.lc;
+  p.part = reinterpret_cast<double*>(((uintptr_t)ws + 255) & ~uintptr_t(255));
+  dim3 grid((unsigned)((p.m + MV_ROWS - 1) / MV_ROWS), (unsigned)p.nch);
+  matvec_kernel<<<grid, MV_ROWS, 0, s>>>(p);
+  FTN_CHECK(after_launch("matvec_kernel"));
+  if (p.nch > 1) {
+    matvec_combine<<<(unsigned)((p.m + 255) / 256), 256, 0, s>>>(p);
+    FTN_CHECK(after_launch("matvec_combine"));
+  }
+  return FTN_OK;
+}
+
+// y(j) = sum_l x(l) b(l,j): one warp per column of b (contiguous in l), lanes stride over l,
+// then a fixed shfl.xor butterfly.
+struct VMParams {
+  const char* x;
+  int64_t x_sm;
+  const char* b;
+  int64_t b_sm0, b_sm1;
+  char* y;
+  int64_t y_sm;
+  int64_t k, n;
+};
+
+__global__ void __launch_bounds__(256) vecmat_kernel(const __grid_constant__ VMParams p) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < p.n;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const char* bp = p.b + j * p.b_sm1;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t l = lane;
+    for (; l + 96 < p.k; l += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double prod = *reinterpret_cast<const double*>(p.x + (l + 32 * u) * p.x_sm) *
+                            *reinterpret_cast<const double*>(bp + (l + 32 * u) * p.b_sm0);
+        acc[u] = acc[u] + prod;
+      }
+    }
+    for (; l < p.k; l += 32) {
+      const double prod = *reinterpret_cast<const double*>(p.x + l * p.x_sm) *
+                          *reinterpret_cast<const double*>(bp + l * p.b_sm0);
+      acc[0] = acc[0] + prod;
+    }
+    double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int mask = 16; mask >= 1; mask >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, mask);
+    if (lane == 0) *reinterpret_cast<double*>(p.y + j * p.y_sm) = v;
+  }
+}
+
+ftn_status_t run_vecmat(const ftn_desc_t* y, const ftn_desc_t* x, const ftn_desc_t* b, cudaStream_t s) {
+  VMParams p;
+  p.x = (const char*)x->base_addr;
+  p.x_sm = x->dim[0].sm;
+  p.b = (const char*)b->base_addr;
+  p.b_sm0 = b->dim[0].sm;
+  p.b_sm1 = b->dim[1].sm;
+  p.y = (char*)y->base_addr;
+  p.y_sm = y->dim[0].sm;
+  p.k = b->dim[0].extent;
+  p.n = b->dim[1].extent;
+  if (p.n == 0) return FTN_OK;
+  int64_t blocks = (p.n * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  vecmat_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+  return after_launch("vecmat_kernel");
+}
+
+// forms: 0 = matrix x matrix, 1 = matrix x vector, 2 = vector x matrix
+int form_of(const ftn_desc_t* a, const ftn_desc_t* b) {
+  if (a->rank == 2 && b->rank == 2) return 0;
+  if (a->rank == 2 && b->rank == 1) return 1;
+  return 2;
+}
+
+size_t ws_bytes_for(const ftn_desc_t* a, const ftn_desc_t* b) {
+  switch (form_of(a, b)) {
+    case 1: {
+      const int64_t m = a->dim[0].extent, k = a->dim[1].extent;
+      return (size_t)(matvec_chunks(m > 0 ? m : 1, k > 0 ? k : 1) * (m > 0 ? m : 1) * 8 + 512);
+    }
+    case 2: return 0;
+  }
+  return pack_bytes(a) + pack_bytes(b) + 512;
+}
+
+ftn_status_t dispatch(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
+                      cudaStream_t s) {
+  switch (form_of(a, b)) {
+    case 1: return run_matvec(c, a, b, ws, s);
+    case 2: return run_vecmat(c, a, b, s);
+  }
+  return run_matmul(c, a, b, ta, tb, ws, s);
 }
 
 }  // namespace
 
-size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b) { return pack_bytes(a) + pack_bytes(b) + 512; }
+size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b) { return ws_bytes_for(a, b); }
 
-ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws, size_t ws_bytes,
-                          cudaStream_t s) {
-  const size_t need = pack_bytes(a) + pack_bytes(b);
-  if (need && (!ws || ws_bytes < matmul_ws(a, b)))
+ftn_status_t matmul_local_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags, void* ws,
+                             size_t ws_bytes, cudaStream_t s) {
+  const bool ta = flags & FTN_MATMUL_TRANSPOSE_A, tb = flags & FTN_MATMUL_TRANSPOSE_B;
+  const size_t need = ws_bytes_for(a, b);
+  if (need > 512 && (!ws || ws_bytes < need))
     return fail(FTN_ERR_WORKSPACE, "ftn_matmul: workspace too small (see ftn_matmul_workspace_size)");
-  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return run_matmul(c, a, b, (char*)ws, s);
+  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return dispatch(c, a, b, ta, tb, (char*)ws, s);
   StreamTemp tmp;  // R#5: the product is formed before c is defined
   FTN_CHECK(tmp.alloc((size_t)desc_size(c) * 8, s));
   ftn_desc_t t;
   FTN_CHECK(make_packed(&t, tmp.ptr, c));
-  FTN_CHECK(run_matmul(&t, a, b, (char*)ws, s));
+  FTN_CHECK(dispatch(&t, a, b, ta, tb, (char*)ws, s));
   return launch_copy(c, &t, s);
 }
 
-ftn_status_t check_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b) {
+ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws, size_t ws_bytes,
+                          cudaStream_t s) {
+  return matmul_local_ex(c, a, b, 0, ws, ws_bytes, s);
+}
+
+// F2018 16.9.124: MATMUL(matrix(m,k), matrix(k,n)) -> (m,n); (m,k) x vector(k) -> (m);
+// vector(k) x (k,n) -> (n).  TRANSPOSE flags apply to rank-2 operands only.
+ftn_status_t check_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags = 0) {
   FTN_CHECK(check_desc(c, "ftn_matmul(c)", 1, 2));
   FTN_CHECK(check_desc(a, "ftn_matmul(a)", 1, 2));
   FTN_CHECK(check_desc(b, "ftn_matmul(b)", 1, 2));
-  if (a->rank != 2 || b->rank != 2 || c->rank != 2)
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_matmul: rank-1 (matrix-vector) forms are not implemented yet");
   if (a->type != FTN_F64 || b->type != FTN_F64 || c->type != FTN_F64)
     return fail(FTN_ERR_TYPE, "ftn_matmul: real(8) operands only");
-  if (b->dim[0].extent != a->dim[1].extent || c->dim[0].extent != a->dim[0].extent ||
-      c->dim[1].extent != b->dim[1].extent)
-    return fail(FTN_ERR_SHAPE, "ftn_matmul: shapes (m,k) x (k,n) -> (m,n) do not match");
+  if (flags & ~(uint32_t)(FTN_MATMUL_TRANSPOSE_A | FTN_MATMUL_TRANSPOSE_B))
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_matmul: unknown flags");
+  const bool ta = flags & FTN_MATMUL_TRANSPOSE_A, tb = flags & FTN_MATMUL_TRANSPOSE_B;
+  if ((ta && a->rank != 2) || (tb && b->rank != 2))
+    return fail(FTN_ERR_RANK, "ftn_matmul: TRANSPOSE needs a rank-2 operand");
+  if (a->rank == 1 && b->rank == 1) return fail(FTN_ERR_RANK, "ftn_matmul: at least one operand must be rank 2");
+  const int64_t am = a->rank == 2 ? (ta ? a->dim[1].extent : a->dim[0].extent) : -1;
+  const int64_t ak = a->rank == 2 ? (ta ? a->dim[0].extent : a->dim[1].extent) : a->dim[0].extent;
+  const int64_t bk = b->rank == 2 ? (tb ? b->dim[1].extent : b->dim[0].extent) : b->dim[0].extent;
+  const int64_t bn = b->rank == 2 ? (tb ? b->dim[0].extent : b->dim[1].extent) : -1;
+  if (ak != bk) return fail(FTN_ERR_SHAPE, "ftn_matmul: inner extents differ");
+  if (a->rank == 2 && b->rank == 2) {
+    if (c->rank != 2 || c->dim[0].extent != am || c->dim[1].extent != bn)
+      return fail(FTN_ERR_SHAPE, "ftn_matmul: c must be (m, n)");
+  } else if (a->rank == 2) {
+    if (c->rank != 1 || c->dim[0].extent != am) return fail(FTN_ERR_SHAPE, "ftn_matmul: c must be (m)");
+  } else {
+    if (c->rank != 1 || c->dim[0].extent != bn) return fail(FTN_ERR_SHAPE, "ftn_matmul: c must be (n)");
+  }
   return FTN_OK;
 }
 
@@ -313,6 +558,21 @@ ftn_status_t ftn_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
   FTN_CHECK(check_matmul(c, a, b));
   FTN_CHECK(require_sm100());
   return matmul_local(c, a, b, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+ftn_status_t ftn_matmul_ex_workspace_size(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b,
+                                          uint32_t flags, size_t* bytes) {
+  FTN_CHECK(check_matmul(c, a, b, flags));
+  if (!bytes) return fail(FTN_ERR_NULL, "ftn_matmul_ex_workspace_size: bytes NULL");
+  *bytes = matmul_ws(a, b);
+  return FTN_OK;
+}
+
+ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags, void* ws,
+                           size_t ws_bytes, ftn_stream_t stream) {
+  FTN_CHECK(check_matmul(c, a, b, flags));
+  FTN_CHECK(require_sm100());
+  return matmul_local_ex(c, a, b, flags, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -81,6 +81,8 @@ def _load():
         "ftn_transpose": [P, P, vp],
         "ftn_matmul_workspace_size": [P, P, P, szp],
         "ftn_matmul": [P, P, P, vp, ctypes.c_size_t, vp],
+        "ftn_matmul_ex_workspace_size": [P, P, P, ctypes.c_uint32, szp],
+        "ftn_matmul_ex": [P, P, P, ctypes.c_uint32, vp, ctypes.c_size_t, vp],
         "ftn_jacobi": [P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
         "ftn_comm_init": [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8),
@@ -374,7 +376,17 @@ def matmul_workspace_size(c: FArray, a: FArray, b: FArray) -> int:
     return n.value
 
 
-def matmul(c: FArray, a: FArray, b: FArray, stream=None):
+def matmul(c: FArray, a: FArray, b: FArray, transpose_a: bool = False, transpose_b: bool = False, stream=None):
+    """c = MATMUL(a, b); with transpose_a / transpose_b: MATMUL(TRANSPOSE(a), ...) without a copy.
+    Rank-1 operands give the matrix-vector / vector-matrix forms."""
+    flags = (1 if transpose_a else 0) | (2 if transpose_b else 0)
+    if flags:
+        n = ctypes.c_size_t()
+        _call("ftn_matmul_ex_workspace_size", c.ref(), a.ref(), b.ref(), flags, ctypes.byref(n))
+        ws = workspace(n.value, c.tensor.device, "matmul")
+        _call("ftn_matmul_ex", c.ref(), a.ref(), b.ref(), flags, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+              _stream(stream))
+        return
     ws = workspace(matmul_workspace_size(c, a, b), c.tensor.device, "matmul")
     _call("ftn_matmul", c.ref(), a.ref(), b.ref(), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
 

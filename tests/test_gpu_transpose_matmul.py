@@ -154,9 +154,12 @@ def test_matmul_errors(ftn):
     with pytest.raises(ftn.FtnError) as e:
         ftn.matmul(ftn.FArray.empty((3, 3)), ftn.FArray.empty((3, 4)), ftn.FArray.empty((3, 3)))
     assert e.value.name == "FTN_ERR_SHAPE"
-    with pytest.raises(ftn.FtnError) as e:
-        ftn.matmul(ftn.FArray.empty((3,)), ftn.FArray.empty((3, 4)), ftn.FArray.empty((4,)))
-    assert e.value.name == "FTN_ERR_UNSUPPORTED"
+    with pytest.raises(ftn.FtnError) as e:      # vector x vector is not a MATMUL form
+        ftn.matmul(ftn.FArray.empty((3,)), ftn.FArray.empty((3,)), ftn.FArray.empty((3,)))
+    assert e.value.name == "FTN_ERR_RANK"
+    with pytest.raises(ftn.FtnError) as e:      # TRANSPOSE of a vector
+        ftn.matmul(ftn.FArray.empty((4,)), ftn.FArray.empty((3,)), ftn.FArray.empty((3, 4)), transpose_a=True)
+    assert e.value.name == "FTN_ERR_RANK"
 
 
 @pytest.mark.slow

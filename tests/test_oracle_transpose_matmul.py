@@ -112,3 +112,35 @@ def test_matmul_shape_errors(orc):
         orc.matmul(FArray(np.zeros((3, 3), order="F")), FArray(np.zeros((3, 4), order="F")),
                    FArray(np.zeros((3, 3), order="F")))
     assert e.value.code == 4
+
+
+# ---- rank-1 forms ---------------------------------------------------------
+
+@pytest.mark.parametrize("mk", [(1, 1), (7, 3), (65, 130), (300, 17)])
+def test_matvec_vecmat_vs_blas_and_exact(orc, mk):
+    m, k = mk
+    a = synth.farray((m, k), array_id=1, mode=synth.U11)
+    x = synth.values(k, array_id=2, mode=synth.U11)
+    y, t = orc.matvec(FArray(a, [0, 3]), FArray(x, [-2]))
+    assert np.all(np.abs(y - a @ x) <= 2 * 4 * k * U * t)
+    b = synth.farray((k, m), array_id=3, mode=synth.U11)
+    z, s = orc.vecmat(FArray(x), FArray(b))
+    assert np.all(np.abs(z - x @ b) <= 2 * 4 * k * U * s)
+    ia = synth.farray((m, k), array_id=4, mode=synth.INT8)
+    ix = synth.values(k, array_id=5, mode=synth.INT8)
+    yi, _ = orc.matvec(FArray(ia), FArray(ix))
+    np.testing.assert_array_equal(yi, (ia.astype(np.int64) @ ix.astype(np.int64)).astype(np.float64))
+    ib = synth.farray((k, m), array_id=6, mode=synth.INT8)
+    zi, _ = orc.vecmat(FArray(ix), FArray(ib))
+    np.testing.assert_array_equal(zi, (ix.astype(np.int64) @ ib.astype(np.int64)).astype(np.float64))
+
+
+def test_matvec_identity_and_sections(orc):
+    x = synth.values(40, mode=synth.U11)
+    y, _ = orc.matvec(FArray(np.eye(40, order="F")), FArray(x))
+    np.testing.assert_array_equal(y, x)
+    a = synth.farray((50, 30), mode=synth.U11)
+    s = FArray(a).section((49, 1, -2), (2, 30, 2))        # 25 x 15 strided, reversed
+    xs = synth.values(15, array_id=9, mode=synth.U11)
+    y, t = orc.matvec(s, FArray(xs))
+    assert np.all(np.abs(y - s.to_numpy() @ xs) <= 2 * 4 * 15 * U * t)
