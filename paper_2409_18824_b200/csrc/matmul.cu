@@ -420,12 +420,17 @@ __global__ void __launch_bounds__(256) vecmat_kernel(const __grid_constant__ VMP
     const char* bp = p.b + j * p.b_sm1;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int64_t l = lane;
-    for (; l + 96 < p.k; l += 128) {
+    for (; l + 224 < p.k; l += 256) {  // 8 independent loads of b in flight per lane
+      double bv[8], xv[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double prod = *reinterpret_cast<const double*>(p.x + (l + 32 * u) * p.x_sm) *
-                            *reinterpret_cast<const double*>(bp + (l + 32 * u) * p.b_sm0);
-        acc[u] = acc[u] + prod;
+      for (int u = 0; u < 8; ++u) {
+        bv[u] = *reinterpret_cast<const double*>(bp + (l + 32 * u) * p.b_sm0);
+        xv[u] = __ldg(reinterpret_cast<const double*>(p.x + (l + 32 * u) * p.x_sm));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double prod = xv[u] * bv[u];
+        acc[u & 3] = acc[u & 3] + prod;
       }
     }
     for (; l < p.k; l += 32) {
