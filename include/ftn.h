@@ -236,6 +236,22 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
 
+/* Jacobi iteration to convergence (R#25): sweeps in blocks of
+ * check_every (the last block may be shorter); after each block the residual
+ * res = MAXVAL(ABS(u_s - u_{s-1})) of the last two iterates is computed on the device and
+ * read back (one stream synchronisation per block); stop when res <= tol or after
+ * max_sweeps.  *sweeps_done, *residual (0 when no sweep ran) and *result_in_unew are
+ * written on the host.  ws: ftn_reduce_workspace_size(u) + 16 bytes, 8-byte aligned. */
+ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
+                              int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
+                              int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
+                              ftn_stream_t stream);
+
+/* MAXVAL(ABS(x - y)) of conformable real(8) arrays without forming x - y (a fused
+ * reduction of an element-wise expression; exact).  Workspace as for ftn_sum(x). */
+ftn_status_t ftn_maxval_absdiff(const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev, void* ws,
+                                size_t ws_bytes, ftn_stream_t stream);
+
 /* ---------------------------------------------------------------- a8
  * Multi-GPU (one process per GPU, NCCL over NVLink).  The id travels between
  * processes through the caller's own channel (torch.distributed store). */

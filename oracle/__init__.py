@@ -93,6 +93,10 @@ def lib():
             "orc_product_int": (ctypes.c_int64, [P]),
             "orc_reduce_dim": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int32, P]),
             "orc_matvec_f64": (ctypes.c_int, [P, P, P, P]),
+            "orc_maxabsdiff_f64": (ctypes.c_double, [P, P]),
+            "orc_jacobi_solve_f64": (ctypes.c_int, [P, P, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                                    ctypes.c_double, ctypes.POINTER(ctypes.c_int64),
+                                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]),
             "orc_vecmat_f64": (ctypes.c_int, [P, P, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -341,3 +345,15 @@ def vecmat(x: FArray, b: FArray) -> tuple[np.ndarray, np.ndarray]:
     y, t = np.zeros(n), np.zeros(n)
     _check(lib().orc_vecmat_f64(FArray(y).ref(), x.ref(), b.ref(), FArray(t).ref()), "vecmat")
     return y, t
+
+
+def maxabsdiff(x: FArray, y: FArray) -> float:
+    return lib().orc_maxabsdiff_f64(x.ref(), y.ref())
+
+
+def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol: float, coeff: float):
+    """(sweeps done, last residual, result in unew) -- DESIGN.md R#25."""
+    d, r, n = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
+    _check(lib().orc_jacobi_solve_f64(u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff, ctypes.byref(d),
+                                      ctypes.byref(r), ctypes.byref(n)), "jacobi_solve")
+    return d.value, r.value, bool(n.value)

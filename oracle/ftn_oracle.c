@@ -798,3 +798,45 @@ int orc_vecmat_f64(const orc_array* y, const orc_array* x, const orc_array* b, c
   }
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* MAXVAL(ABS(x - y)) by the definition (R#10/R#11 rules; empty -> -inf).          */
+/* ------------------------------------------------------------------------ */
+double orc_maxabsdiff_f64(const orc_array* x, const orc_array* y) {
+  const int64_t n = total_size(x);
+  double r = -INFINITY;
+  int seen = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    const double d = fabs(*(const double*)addr_linear(x, t) - *(const double*)addr_linear(y, t));
+    if (isnan(d)) { if (!seen) r = d; continue; }
+    if (!seen || isnan(r) || d > r) r = d;
+    seen = 1;
+  }
+  return r;
+}
+
+/* Jacobi to convergence (R#25): the DO nest of orc_jacobi_f64 one sweep at a time; after
+ * every check_every-th sweep (and after max_sweeps) res = max |u_s - u_{s-1}| over all points;
+ * stop when res <= tol. */
+int orc_jacobi_solve_f64(const orc_array* u, const orc_array* unew, int64_t max_sweeps, int64_t check_every,
+                         double tol, double coeff, int64_t* sweeps_done, double* residual, int32_t* in_unew) {
+  const orc_array* a = u;
+  const orc_array* b = unew;
+  int64_t s = 0;
+  double res = 0.0;
+  int32_t dummy;
+  while (s < max_sweeps) {
+    int rc = orc_jacobi_f64(a, b, 1, coeff, &dummy);
+    if (rc) return rc;
+    const orc_array* t = a; a = b; b = t;   /* a holds u_s */
+    ++s;
+    if (s % check_every == 0 || s == max_sweeps) {
+      res = orc_maxabsdiff_f64(a, b);
+      if (res <= tol) break;
+    }
+  }
+  *sweeps_done = s;
+  *residual = res;
+  *in_unew = (int32_t)(a == unew);
+  return ORC_OK;
+}

@@ -83,7 +83,7 @@ ftn_status_t launch_copy(const ftn_desc_t* dst, const ftn_desc_t* src, cudaStrea
 ftn_status_t reduce_local(int kind, const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev,
                           void* ws, size_t ws_bytes, cudaStream_t stream);
 size_t reduce_ws_bytes(int64_t n);
-enum { RK_SUM = 0, RK_MAX = 1, RK_MIN = 2, RK_DOT = 3, RK_PROD = 4 };
+enum { RK_SUM = 0, RK_MAX = 1, RK_MIN = 2, RK_DOT = 3, RK_PROD = 4, RK_MAXABSDIFF = 5 };
 ftn_status_t tree_combine_launch(int kind, int32_t type, const void* partials, int64_t n,
                                  void* result, cudaStream_t stream);
 

@@ -46,7 +46,7 @@ __device__ __forceinline__ typename Acc<T>::type neutral() {
   } else if constexpr (KIND == RK_PROD) {
     return A(1);
   } else if constexpr (std::is_floating_point<T>::value) {
-    return NAN;  // maxNum/minNum ignore NaN: an all-NaN (or empty) combine stays NaN (R#11)
+    return NAN;  // maxNum/minNum ignore NaN (MAXABSDIFF too): an all-NaN (or empty) combine stays NaN (R#11)
   } else {
     if constexpr (sizeof(T) == 4) return (A)(KIND == RK_MAX ? INT32_MIN : INT32_MAX);
     else return (A)(KIND == RK_MAX ? INT64_MIN : INT64_MAX);
@@ -56,8 +56,8 @@ __device__ __forceinline__ typename Acc<T>::type neutral() {
 // MAXVAL / MINVAL of an empty array: -inf / +inf (R#10)
 template <typename T, int KIND>
 __device__ __forceinline__ typename Acc<T>::type empty_value() {
-  if constexpr (std::is_floating_point<T>::value && (KIND == RK_MAX || KIND == RK_MIN))
-    return KIND == RK_MAX ? -INFINITY : INFINITY;
+  if constexpr (std::is_floating_point<T>::value && (KIND == RK_MAX || KIND == RK_MIN || KIND == RK_MAXABSDIFF))
+    return KIND == RK_MIN ? INFINITY : -INFINITY;
   return neutral<T, KIND>();
 }
 
@@ -68,7 +68,7 @@ __device__ __forceinline__ typename Acc<T>::type combine(typename Acc<T>::type a
   } else if constexpr (KIND == RK_PROD) {
     return a * b;  // fp: one IEEE multiply (RN); ints: modulo 2^w
   } else if constexpr (std::is_floating_point<T>::value) {
-    return KIND == RK_MAX ? fmax(a, b) : fmin(a, b);  // maxNum: NaN ignored (R#11)
+    return (KIND == RK_MAX || KIND == RK_MAXABSDIFF) ? fmax(a, b) : fmin(a, b);  // maxNum: NaN ignored (R#11)
   } else {
     T x = (T)a, y = (T)b;
     return (typename Acc<T>::type)(KIND == RK_MAX ? (x > y ? x : y) : (x < y ? x : y));
@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           ld_group<T>(reinterpret_cast<const char*>(xp + g0 + 1024 * (m0 + u)), xv[u]);
-          if constexpr (KIND == RK_DOT) ld_group<T>(reinterpret_cast<const char*>(yp + g0 + 1024 * (m0 + u)), yv[u]);
+          if constexpr (KIND == RK_DOT || KIND == RK_MAXABSDIFF)
+            ld_group<T>(reinterpret_cast<const char*>(yp + g0 + 1024 * (m0 + u)), yv[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
           for (int v = 0; v < R_GROUP; ++v) {
             A e;
             if constexpr (KIND == RK_DOT) e = __dmul_rn(xv[u][v], yv[u][v]);
+            else if constexpr (KIND == RK_MAXABSDIFF) e = fabs(__dsub_rn(xv[u][v], yv[u][v]));
             else e = (A)xv[u][v];
             acc[v] = combine<T, KIND>(acc[v], e);
           }
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
           if (g + v < end) {
             A e;
             if constexpr (KIND == RK_DOT) e = __dmul_rn(xp[g + v], yp[g + v]);
+            else if constexpr (KIND == RK_MAXABSDIFF) e = fabs(__dsub_rn(xp[g + v], yp[g + v]));
             else e = (A)xp[g + v];
             acc[v] = combine<T, KIND>(acc[v], e);
           }
@@ -172,14 +175,14 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
     }
   } else {
     // general descriptor: walk positions incrementally (one division per row crossing)
-    int64_t i0 = 0, i1 = 0, i2 = 0, j0 = 0, j1 = 0, j2 = 0;
+    int64_t i0 = 0, i1 = 0, i2 = 0;
     if (g0 < end) {
       int64_t t = g0;
       i0 = t % p.x.ext[0];
       t /= p.x.ext[0];
       i1 = t % p.x.ext[1];
       i2 = t / p.x.ext[1];
-      if constexpr (KIND == RK_DOT) { j0 = g0; }
+
     }
     for (int m = 0; m < R_STEPS; ++m) {
       const int64_t g = g0 + 1024 * m;
@@ -195,10 +198,12 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
         for (int v = 0; v < R_GROUP; ++v) {
           if (g + v < end) {
             A e;
-            if constexpr (KIND == RK_DOT) {
-              const T xv = *reinterpret_cast<const T*>(p.x.base + (j0 + v) * p.x.sm[0]);
-              const T yv = *reinterpret_cast<const T*>(p.y.base + (j0 + v) * p.y.sm[0]);
-              e = __dmul_rn(xv, yv);
+            if constexpr (KIND == RK_DOT || KIND == RK_MAXABSDIFF) {
+              // the second operand has the same (collapsed) shape: same position, own strides
+              const T xv = *reinterpret_cast<const T*>(addr(p.x, a0, a1, a2));
+              const T yv = *reinterpret_cast<const T*>(addr(p.y, a0, a1, a2));
+              if constexpr (KIND == RK_DOT) e = __dmul_rn(xv, yv);
+              else e = fabs(__dsub_rn(xv, yv));
             } else {
               e = (A)*reinterpret_cast<const T*>(addr(p.x, a0, a1, a2));
             }
@@ -208,7 +213,6 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
         }
       }
       advance(p.x, i0, i1, i2, 1024);
-      if constexpr (KIND == RK_DOT) j0 += 1024;
     }
   }
 
@@ -315,20 +319,27 @@ ftn_status_t reduce_local(int kind, const ftn_desc_t* x, const ftn_desc_t* y, vo
     return fail(FTN_ERR_WORKSPACE, "reduction workspace too small (need " + std::to_string(reduce_ws_bytes(p.n)) + " bytes)");
   if (p.nc > 1 && ((uintptr_t)ws % 8)) return fail(FTN_ERR_ALIGN, "reduction workspace must be 8-byte aligned");
   const int64_t el = x->elem_len;
-  if (kind == RK_DOT) {
-    p.x = to_kdesc(x);
-    p.y = to_kdesc(y);
-    const bool flat = p.x.sm[0] == el && p.y.sm[0] == el && ((uintptr_t)p.x.base % 32) == 0 &&
+  if (kind == RK_DOT || kind == RK_MAXABSDIFF) {
+    const ftn_desc_t* arr2[2] = {x, y};
+    KDesc kd[2];
+    const int r2 = collapse(arr2, 2, kd);
+    p.x = kd[0];
+    p.y = kd[1];
+    const bool flat = r2 == 1 && p.x.sm[0] == el && p.y.sm[0] == el && ((uintptr_t)p.x.base % 32) == 0 &&
                       ((uintptr_t)p.y.base % 32) == 0;
     const unsigned blocks = (unsigned)(p.nc > 0 ? p.nc : 1);
     void* out = p.nc > 1 ? ws : result;
-    if (flat)
-      reduce_chunks<double, RK_DOT, true, true><<<blocks, R_THREADS, 0, stream>>>(p, out);
-    else
-      reduce_chunks<double, RK_DOT, false, false><<<blocks, R_THREADS, 0, stream>>>(p, out);
-    FTN_CHECK(after_launch("reduce_chunks(dot)"));
+    if (kind == RK_DOT) {
+      if (flat) reduce_chunks<double, RK_DOT, true, true><<<blocks, R_THREADS, 0, stream>>>(p, out);
+      else reduce_chunks<double, RK_DOT, false, false><<<blocks, R_THREADS, 0, stream>>>(p, out);
+    } else {
+      if (flat) reduce_chunks<double, RK_MAXABSDIFF, true, true><<<blocks, R_THREADS, 0, stream>>>(p, out);
+      else reduce_chunks<double, RK_MAXABSDIFF, false, false><<<blocks, R_THREADS, 0, stream>>>(p, out);
+    }
+    FTN_CHECK(after_launch("reduce_chunks(2 operands)"));
     if (p.nc > 1) {
-      tree_kernel<double, RK_SUM><<<1, TREE_THREADS, 0, stream>>>(ws, p.nc, result);
+      if (kind == RK_DOT) tree_kernel<double, RK_SUM><<<1, TREE_THREADS, 0, stream>>>(ws, p.nc, result);
+      else tree_kernel<double, RK_MAXABSDIFF><<<1, TREE_THREADS, 0, stream>>>(ws, p.nc, result);
       FTN_CHECK(after_launch("reduce_tree"));
     }
     return FTN_OK;
@@ -353,7 +364,8 @@ ftn_status_t tree_combine_launch(int kind, int32_t type, const void* partials, i
                                  cudaStream_t s) {
   if (type == FTN_F64) {
     if (kind == RK_SUM || kind == RK_DOT) tree_kernel<double, RK_SUM><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
-    else if (kind == RK_MAX) tree_kernel<double, RK_MAX><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
+    else if (kind == RK_MAX || kind == RK_MAXABSDIFF) tree_kernel<double, RK_MAX><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
+    else if (kind == RK_PROD) tree_kernel<double, RK_PROD><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
     else tree_kernel<double, RK_MIN><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
   } else if (type == FTN_I64) {
     if (kind == RK_SUM) tree_kernel<int64_t, RK_SUM><<<1, TREE_THREADS, 0, s>>>(partials, n, result);
@@ -399,6 +411,17 @@ ftn_status_t ftn_maxval(const ftn_desc_t* x, void* result_dev, void* ws, size_t 
 }
 ftn_status_t ftn_minval(const ftn_desc_t* x, void* result_dev, void* ws, size_t ws_bytes, ftn_stream_t stream) {
   return reduce_entry(RK_MIN, "ftn_minval", x, result_dev, ws, ws_bytes, stream);
+}
+
+ftn_status_t ftn_maxval_absdiff(const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev, void* ws,
+                                size_t ws_bytes, ftn_stream_t stream) {
+  FTN_CHECK(check_desc(x, "ftn_maxval_absdiff(x)", 1, FTN_MAX_RANK));
+  FTN_CHECK(check_desc(y, "ftn_maxval_absdiff(y)", 1, FTN_MAX_RANK));
+  if (x->type != FTN_F64 || y->type != FTN_F64) return fail(FTN_ERR_TYPE, "ftn_maxval_absdiff: real(8) only");
+  if (!same_shape(x, y)) return fail(FTN_ERR_SHAPE, "ftn_maxval_absdiff: x and y are not conformable");
+  if (!result_dev) return fail(FTN_ERR_NULL, "ftn_maxval_absdiff: result_dev NULL");
+  FTN_CHECK(require_sm100());
+  return reduce_local(RK_MAXABSDIFF, x, y, result_dev, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 ftn_status_t ftn_dot_product(const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev, void* ws, size_t ws_bytes,

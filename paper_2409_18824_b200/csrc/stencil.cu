@@ -574,3 +574,62 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
   const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
   return jacobi2d_fused_rows(src, dst, sweeps, coeff, lo, hi, fix_lo, fix_hi, s);
 }
+
+// Jacobi iteration to convergence (R#25): blocks of check_every
+// sweeps, the last sweep of each block a single sweep so that the two arrays hold
+// consecutive iterates, then res = MAXVAL(ABS(u_s - u_{s-1})) (exact: a max of exactly
+// rounded differences); stop when res <= tol or after max_sweeps.  Synchronises the stream
+// once per block to read res.
+extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
+                                         int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
+                                         int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
+                                         ftn_stream_t stream) {
+  FTN_CHECK(jacobi_check(u, unew));
+  if (max_sweeps < 0 || check_every < 1) return fail(FTN_ERR_SHAPE, "ftn_jacobi_solve: need max_sweeps >= 0, check_every >= 1");
+  size_t rws = 0;
+  FTN_CHECK(ftn_reduce_workspace_size(u, &rws));
+  if (!ws || ws_bytes < rws + 16 || ((uintptr_t)ws % 8))
+    return fail(FTN_ERR_WORKSPACE, "ftn_jacobi_solve: workspace must hold ftn_reduce_workspace_size(u) + 16 bytes");
+  FTN_CHECK(require_sm100());
+  FTN_CHECK(jacobi_prepare());
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
+  const int T = jacobi_fuse_T();
+  const bool can_fuse = tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3;
+  double* res_dev = reinterpret_cast<double*>(ws);
+  char* rw = reinterpret_cast<char*>(ws) + 16;
+  int cur = 0;  // 0: u holds the newest iterate
+  int64_t done = 0;
+  double res = INFINITY;
+  const int64_t nlast = u->dim[u->rank - 1].extent;
+  while (done < max_sweeps) {
+    const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
+    int64_t left = k;
+    while (left > 1 + (can_fuse ? T - 1 : 0) && can_fuse) {   // fused launches, keeping the last sweep single
+      FTN_CHECK(jacobi2d_fused(cur ? unew : u, cur ? u : unew, T, coeff, s));
+      cur ^= 1;
+      left -= T;
+    }
+    for (; left > 0; --left) {
+      const ftn_desc_t* src = cur ? unew : u;
+      const ftn_desc_t* dst = cur ? u : unew;
+      CUtensorMap m;
+      const CUtensorMap* mp = nullptr;
+      if (tma) {
+        FTN_CHECK(make_stencil_map(&m, src));
+        mp = &m;
+      }
+      FTN_CHECK(sweep(src, dst, mp, coeff, 1, nlast - 2, s));
+      cur ^= 1;
+    }
+    done += k;
+    FTN_CHECK(ftn_maxval_absdiff(u, unew, res_dev, rw, ws_bytes - 16, stream));
+    FTN_CUDA(cudaMemcpyAsync(&res, res_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    FTN_CUDA(cudaStreamSynchronize(s));
+    if (res <= tol) break;
+  }
+  if (sweeps_done) *sweeps_done = done;
+  if (residual) *residual = done ? res : 0.0;
+  if (result_in_unew) *result_in_unew = cur;
+  return FTN_OK;
+}

@@ -74,6 +74,10 @@ def _load():
         "ftn_minval": [P, vp, vp, ctypes.c_size_t, vp],
         "ftn_dot_product": [P, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_product": [P, vp, vp, ctypes.c_size_t, vp],
+        "ftn_maxval_absdiff": [P, P, vp, vp, ctypes.c_size_t, vp],
+        "ftn_jacobi_solve": [P, P, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double, vp,
+                             ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_sum_dim": [P, ctypes.c_int32, P, vp],
         "ftn_product_dim": [P, ctypes.c_int32, P, vp],
         "ftn_maxval_dim": [P, ctypes.c_int32, P, vp],
@@ -403,6 +407,28 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float | None = None, str
 def jacobi_set_fusion(sweeps_per_launch: int):
     """Temporal-blocking factor of the 2-D Jacobi kernels (1..4, default 3); results are identical."""
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
+
+
+def maxval_absdiff(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:
+    """MAXVAL(ABS(x - y)) without forming x - y."""
+    res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
+    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce")
+    _call("ftn_maxval_absdiff", x.ref(), y.ref(), ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+          ws.numel(), _stream(stream))
+    return res
+
+
+def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol: float, coeff=None,
+                 stream=None) -> tuple[int, float, bool]:
+    """Jacobi to convergence (R#25): (sweeps done, last residual, result in unew)."""
+    if coeff is None:
+        coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
+    ws = workspace(reduce_workspace_size(u) + 64, u.tensor.device, "solve")
+    done, res, new = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
+    _call("ftn_jacobi_solve", u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff,
+          ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(done), ctypes.byref(res), ctypes.byref(new),
+          _stream(stream))
+    return done.value, res.value, bool(new.value)
 
 
 def jacobi_slab(src: FArray, dst: FArray, sweeps: int, halo: int, first: bool, last: bool, coeff=None,

@@ -1,0 +1,47 @@
+"""GPU parity for SURVEY §8(f) f2: MAXVAL(ABS(x-y)) and Jacobi to convergence (R#25) vs the
+oracle -- sweeps done, residual and result bit-exact, for every temporal-blocking factor."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import FArray as OA
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ftn():
+    from paper_2409_18824_b200 import ftn
+    return ftn
+
+
+def test_maxval_absdiff(ftn):
+    for shape in ((1,), (1000,), (65537,), (300, 301), (40, 30, 20)):
+        a = synth.farray(shape, array_id=1, mode=synth.U11)
+        b = synth.farray(shape, array_id=2, mode=synth.U11)
+        got = ftn.maxval_absdiff(ftn.FArray.from_numpy(a), ftn.FArray.from_numpy(b)).item()
+        assert got == oracle.maxabsdiff(OA(a), OA(b)) == np.max(np.abs(a - b))
+    a = synth.farray((90, 80), array_id=3, mode=synth.U11)
+    b = synth.farray((90, 80), array_id=4, mode=synth.U11)
+    A, B = ftn.FArray.from_numpy(a), ftn.FArray.from_numpy(b)
+    got = ftn.maxval_absdiff(A.section((89, 1, -2), (1, 80, 3)), B.section((1, 89, 2), (80, 1, -3))).item()
+    assert got == np.max(np.abs(a[88::-2, ::3] - b[0:89:2, ::-3]))
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4])
+@pytest.mark.parametrize("shape,check,tol", [((130, 97), 5, 1e-3), ((130, 97), 7, -1.0), ((300, 200), 10, 1e-4),
+                                             ((60, 50, 40), 4, 1e-3)])
+def test_jacobi_solve(ftn, T, shape, check, tol):
+    ftn.jacobi_set_fusion(T)
+    try:
+        u0 = synth.jacobi_init(shape)
+        U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+        coeff = 0.25 if len(shape) == 2 else 1.0 / 6.0
+        done, res, new = ftn.jacobi_solve(U, W, 60, check, tol, coeff)
+        a, b = u0.copy(order="F"), u0.copy(order="F")
+        d2, r2, n2 = oracle.jacobi_solve(OA(a), OA(b), 60, check, tol, coeff)
+        assert (done, res, new) == (d2, r2, n2)
+        np.testing.assert_array_equal((W if new else U).to_numpy(), b if n2 else a)
+    finally:
+        ftn.jacobi_set_fusion(3)

@@ -146,3 +146,43 @@ def test_strided_descriptors(orc):
     res_sec = s.to_numpy()
     res_p, _ = _run(orc, packed, 4, C2)
     np.testing.assert_array_equal(res_sec, res_p)
+
+
+# ---- convergence (R#25) ------------------------------------------
+
+def test_maxabsdiff_vs_numpy(orc):
+    a = synth.farray((40, 30), array_id=1, mode=synth.U11)
+    b = synth.farray((40, 30), array_id=2, mode=synth.U11)
+    assert orc.maxabsdiff(FArray(a), FArray(b)) == np.max(np.abs(a - b))
+    assert orc.maxabsdiff(FArray(a), FArray(a)) == 0.0
+    assert orc.maxabsdiff(FArray(np.zeros(0)), FArray(np.zeros(0))) == -np.inf
+
+
+def test_solve_equals_fixed_sweeps_when_not_converging(orc):
+    u = synth.jacobi_init((37, 29))
+    a, b = u.copy(order="F"), u.copy(order="F")
+    done, res, new = orc.jacobi_solve(FArray(a), FArray(b), 13, 4, -1.0, C2)
+    assert done == 13 and new
+    c, d = u.copy(order="F"), u.copy(order="F")
+    orc.jacobi(FArray(c), FArray(d), 13, C2)
+    np.testing.assert_array_equal(b, d)
+    assert res == np.max(np.abs(b - a))                 # last two iterates
+
+
+def test_solve_harmonic_stops_at_first_check(orc):
+    i, j = np.meshgrid(np.arange(20.0), np.arange(15.0), indexing="ij")
+    u = np.asfortranarray(i + 2 * j)
+    done, res, _ = orc.jacobi_solve(FArray(u.copy(order="F")), FArray(u.copy(order="F")), 100, 5, 0.0, C2)
+    assert done == 5 and res == 0.0
+
+
+def test_solve_residual_monotone_on_dyadic_data(orc):
+    """||u_{s+1} - u_s||_inf <= ||u_s - u_{s-1}||_inf (Jacobi is an averaging map); dyadic data keep
+    every sum exact for the first sweeps, so the inequality holds bit for bit."""
+    u = np.asfortranarray(synth.farray((16, 16), mode=synth.INT8) * 2.0 ** -4)
+    res = []
+    for s in range(1, 12):
+        a, b = u.copy(order="F"), u.copy(order="F")
+        _, r, _ = orc.jacobi_solve(FArray(a), FArray(b), s, s, -1.0, C2)
+        res.append(r)
+    assert all(x >= y for x, y in zip(res, res[1:]))
