@@ -241,7 +241,8 @@ int32_t ftn_jacobi_get_fusion(void);
  * res = MAXVAL(ABS(u_s - u_{s-1})) of the last two iterates is computed on the device and
  * read back (one stream synchronisation per block); stop when res <= tol or after
  * max_sweeps.  *sweeps_done, *residual (0 when no sweep ran) and *result_in_unew are
- * written on the host.  ws: ftn_reduce_workspace_size(u) + 16 bytes, 8-byte aligned. */
+ * written on the host; the result is in unew iff sweeps_done is odd (as for ftn_jacobi).
+ * ws: ftn_reduce_workspace_size(u) + 16 bytes, 8-byte aligned. */
 ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
                               int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
                               int64_t* sweeps_done, double* residual, int32_t* result_in_unew,

@@ -604,11 +604,14 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   const int64_t nlast = u->dim[u->rank - 1].extent;
   while (done < max_sweeps) {
     const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
-    int64_t left = k;
-    while (left > 1 + (can_fuse ? T - 1 : 0) && can_fuse) {   // fused launches, keeping the last sweep single
+    // fused launches for the first k-1 sweeps (an even number of them when T is even, so
+    // that the launch count keeps the sweep parity, as in ftn_jacobi); the last sweep single
+    int64_t fused = can_fuse ? (k - 1) / T : 0;
+    if (T % 2 == 0 && fused % 2) fused -= 1;
+    int64_t left = k - fused * T;
+    for (int64_t f = 0; f < fused; ++f) {
       FTN_CHECK(jacobi2d_fused(cur ? unew : u, cur ? u : unew, T, coeff, s));
       cur ^= 1;
-      left -= T;
     }
     for (; left > 0; --left) {
       const ftn_desc_t* src = cur ? unew : u;
