@@ -226,15 +226,19 @@ ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_d
 ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                         int32_t* result_in_unew, ftn_stream_t stream);
 
-/* Tuning (not semantics): rank-2 sweeps are executed T at a time by one kernel that keeps
- * the T-1 intermediate iterates in shared memory (temporal blocking, SURVEY §8(f) f2,
+/* Tuning (not semantics): rank-2 sweeps are executed up to T at a time by one kernel that
+ * keeps the intermediate iterates in registers (temporal blocking, SURVEY §8(f) f2,
  * DESIGN.md §4.3).  Results are bit-identical for every T; the array that does not hold
- * the result holds an earlier iterate.  T in 1..4 (1 = one sweep per launch); default 3
- * or the FTN_JACOBI_FUSE environment variable.  Process-wide.  A launch plan for S sweeps:
- * F = S div T fused launches (F even when T is even, so that the result parity matches
- * the sweep parity), then S - F*T single sweeps. */
+ * the result holds an earlier iterate.  T in 1..4 (1 = one sweep per launch); default 4
+ * or the FTN_JACOBI_FUSE environment variable.  Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
+
+/* The launch plan ftn_jacobi / ftn_jacobi_dist use for `sweeps` sweeps with at most T per
+ * launch: floor(S/T) launches of T and one of S mod T, with one launch split k -> (k-1)+1
+ * when needed so that the launch count has the parity of S (the result then lands in unew
+ * iff S is odd).  Writes up to cap sweep counts to sizes (may be NULL); returns the count. */
+int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, int64_t cap);
 
 /* Jacobi iteration to convergence (R#25): sweeps in blocks of
  * check_every (the last block may be shorter); after each block the residual

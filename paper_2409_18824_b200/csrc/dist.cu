@@ -12,6 +12,7 @@
 
 #include <nccl.h>
 #include <cstring>
+#include <vector>
 
 struct ftn_comm_s {
   ncclComm_t nccl;
@@ -167,15 +168,15 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
     T = jacobi_fuse_T();
     if (T > halo) T = halo;
   }
-  int64_t fused = T > 1 ? sweeps / T : 0;
-  if (T % 2 == 0 && fused % 2) fused -= 1;  // launch count must match the sweep parity
+  const int64_t nplan = ftn_jacobi_plan(sweeps, T, nullptr, 0);
+  std::vector<int32_t> plan((size_t)nplan);
+  ftn_jacobi_plan(sweeps, T, plan.data(), nplan);
   const size_t plane = (size_t)(desc_size(u) / nl);
   const int lower = comm->rank - 1, upper = comm->rank + 1;
   const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
   int64_t launches = 0;
-  const int64_t total = fused + (sweeps - fused * T);
-  for (; launches < total; ++launches) {
-    const int k = launches < fused ? T : 1;
+  for (; launches < nplan; ++launches) {
+    const int k = plan[(size_t)launches];
     const ftn_desc_t* src = (launches % 2 == 0) ? u : unew;
     const ftn_desc_t* dst = (launches % 2 == 0) ? unew : u;
     char* b = (char*)src->base_addr;

@@ -23,6 +23,7 @@
 
 #include <cstring>
 #include <cstdlib>
+#include <vector>
 
 namespace ftn {
 
@@ -463,14 +464,14 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
 static bool g_attr_done[64];
 
 // Sweeps fused per launch for 2-D arrays (1 = off, 2..4): ftn_jacobi_set_fusion, else the
-// FTN_JACOBI_FUSE environment variable, else 3 (measured best on B200: 895 GLUPS at 8192^2
-// vs 629 for 2 and 747 for 4, profiles/r1_fusion_sweep.txt).
+// FTN_JACOBI_FUSE environment variable, else 4 (measured on B200 at 8192^2 x 100 with the
+// register-ring kernel: T=2 ~640, T=3 955-975, T=4 1036-1039 GLUPS).
 static std::atomic<int> g_fuse{0};
 int jacobi_fuse_T() {
   int t = g_fuse.load();
   if (t == 0) {
     const char* e = getenv("FTN_JACOBI_FUSE");
-    t = e ? atoi(e) : 3;
+    t = e ? atoi(e) : 4;
     t = t < 1 ? 1 : (t > 4 ? 4 : t);
     g_fuse.store(t);
   }
@@ -501,6 +502,29 @@ extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
 
 extern "C" int32_t ftn_jacobi_get_fusion(void) { return jacobi_fuse_T(); }
 
+// Launch plan for S sweeps with at most T per launch: floor(S/T) launches of
+// T and one of S mod T; every launch swaps u/unew, so when the launch count does not have the
+// parity of S one T-launch is split into T-1 and 1 (or, for S < T, the single launch into
+// S-1 and 1).  Each entry is the number of sweeps of one launch.
+extern "C" int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, int64_t cap) {
+  std::vector<int32_t> v;
+  if (T < 1) T = 1;
+  for (int64_t i = 0; i < sweeps / T; ++i) v.push_back(T);
+  if (sweeps % T) v.push_back((int32_t)(sweeps % T));
+  if ((int64_t)(v.size() % 2) != sweeps % 2) {
+    // split the first launch with >= 2 sweeps: k -> (k - 1) + 1
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i] >= 2) {
+        v[i] -= 1;
+        v.insert(v.begin() + i + 1, 1);
+        break;
+      }
+  }
+  const int64_t n = (int64_t)v.size();
+  for (int64_t i = 0; i < n && i < cap; ++i) sizes[i] = v[i];
+  return n;
+}
+
 extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                                    int32_t* result_in_unew, ftn_stream_t stream) {
   FTN_CHECK(jacobi_check(u, unew));
@@ -515,27 +539,23 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     FTN_CHECK(make_stencil_map(&mw, unew));
   }
   const int64_t nlast = u->dim[u->rank - 1].extent;
-  // Temporal blocking: launches of T fused sweeps, then single sweeps.
-  // Every launch swaps u/unew, so the result lands in unew iff the launch count is odd;
-  // the number of fused launches is chosen so that this matches the sweep parity.
+  // Temporal blocking: launches of up to T fused sweeps (ftn_jacobi_plan).
+  // Every launch swaps u/unew; the plan's launch count has the parity of `sweeps`, so the
+  // result lands in unew iff sweeps is odd.
   const int T = jacobi_fuse_T();
-  int64_t fused = 0;
-  if (tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3) {
-    fused = sweeps / T;
-    if (T % 2 == 0 && fused % 2) fused -= 1;
-  }
-  int64_t launches = 0;
-  for (int64_t f = 0; f < fused; ++f, ++launches) {
-    const bool even = (launches % 2) == 0;
-    FTN_CHECK(jacobi2d_fused(even ? u : unew, even ? unew : u, T, coeff, s));
-  }
+  const bool can_fuse = tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3;
   static const bool wf1 = getenv("FTN_JACOBI_WF1") && atoi(getenv("FTN_JACOBI_WF1")) != 0;
-  for (int64_t sw = fused * T; sw < sweeps; ++sw, ++launches) {
+  const int64_t nplan = ftn_jacobi_plan(sweeps, can_fuse ? T : 1, nullptr, 0);
+  std::vector<int32_t> plan((size_t)nplan);
+  ftn_jacobi_plan(sweeps, can_fuse ? T : 1, plan.data(), nplan);
+  int64_t launches = 0;
+  for (; launches < nplan; ++launches) {
     const bool even = (launches % 2) == 0;
     const ftn_desc_t* src = even ? u : unew;
     const ftn_desc_t* dst = even ? unew : u;
-    if (wf1 && tma && u->rank == 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3)
-      FTN_CHECK(jacobi2d_fused(src, dst, 1, coeff, s));
+    const int k = plan[(size_t)launches];
+    if (k >= 2 || (wf1 && can_fuse))
+      FTN_CHECK(jacobi2d_fused(src, dst, k, coeff, s));
     else
       FTN_CHECK(sweep(src, dst, tma ? (even ? &mu : &mw) : nullptr, coeff, 1, nlast - 2, s));
   }
@@ -604,14 +624,19 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   const int64_t nlast = u->dim[u->rank - 1].extent;
   while (done < max_sweeps) {
     const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
-    // fused launches for the first k-1 sweeps (an even number of them when T is even, so
-    // that the launch count keeps the sweep parity, as in ftn_jacobi); the last sweep single
-    int64_t fused = can_fuse ? (k - 1) / T : 0;
-    if (T % 2 == 0 && fused % 2) fused -= 1;
-    int64_t left = k - fused * T;
-    for (int64_t f = 0; f < fused; ++f) {
-      FTN_CHECK(jacobi2d_fused(cur ? unew : u, cur ? u : unew, T, coeff, s));
-      cur ^= 1;
+    // the first k-1 sweeps by the plan of ftn_jacobi (launch count of their parity), then
+    // one single sweep, so the two arrays end up holding consecutive iterates
+    const int64_t np = ftn_jacobi_plan(k - 1, can_fuse ? T : 1, nullptr, 0);
+    std::vector<int32_t> plan((size_t)np);
+    ftn_jacobi_plan(k - 1, can_fuse ? T : 1, plan.data(), np);
+    int64_t left = 1;
+    for (int32_t kk : plan) {
+      if (kk >= 2) {
+        FTN_CHECK(jacobi2d_fused(cur ? unew : u, cur ? u : unew, kk, coeff, s));
+        cur ^= 1;
+      } else {
+        left += 1;
+      }
     }
     for (; left > 0; --left) {
       const ftn_desc_t* src = cur ? unew : u;

@@ -46,6 +46,7 @@ struct WFCfg {
   static constexpr int THREADS = (WF_NW + 1) * 32;
   static constexpr bool ALIGNED = ((H - T) % 2) == 0;  // lane column pairs 16-byte aligned in smem
   static_assert(BW <= 256, "TMA box width");
+  static_assert(WF_R % 3 == 0, "rows per box: a multiple of 3 (register ring slots are compile-time)");
 };
 
 struct WFParams {
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
   }
 
   // ---------------- compute warps: lane owns window columns 2*lane, 2*lane+1
+  const uint32_t smem_off = (uint32_t)(smem - smem_raw);
   const int wbase = C::H - T + warp * C::WO;  // box column of window column 0
   const int col0 = wbase + 2 * lane;          // box column of this lane's first column
   const double coeff = p.coeff;
@@ -132,72 +134,70 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
     const int64_t rl = p.fix_lo + 1 - (ja - T), rh = p.fix_hi - 1 - (ja - T);
     const int r_lo = (int)max(rl, (int64_t)-1), r_hi = (int)min(rh, (int64_t)(1 << 30));
     char* outp = p.dst + g0 * p.d_sm1 + ja * p.d_sm2;  // row ja = relative row T of level T
-    // level t keeps rows (s-t-1, s-t, s-t+1) = (up, mid, dn) after step s, two columns each
-    double up[T + 1][2], mid[T + 1][2], dn[T + 1][2];
+    // Level t keeps its last three rows in a register ring: row r in slot r mod 3.  Every
+    // chunk starts at a row s0 = 0 mod 3 (R is a multiple of 3) and is processed fully
+    // unrolled, so every slot index is a compile-time constant (no register moves); rows of
+    // the last chunk beyond nr compute garbage that is never stored or consumed.
+    double L[T + 1][3][2];
 #pragma unroll
     for (int t = 0; t <= T; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) up[t][e] = mid[t][e] = dn[t][e] = 0.0;
+      for (int q3 = 0; q3 < 3; ++q3) L[t][q3][0] = L[t][q3][1] = 0.0;
     const int64_t nch = (nr + WF_R - 1) / WF_R;
-    int s = 0;
-    auto step = [&](const double* row, bool fastpath) {
+    const int nri = (int)nr;
+    auto chunk = [&](const double* st, int s0, bool fastpath) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        up[0][e] = mid[0][e];
-        mid[0][e] = dn[0][e];
-      }
-      if constexpr (C::ALIGNED) {
-        const double2 v = *reinterpret_cast<const double2*>(row);
-        dn[0][0] = v.x;
-        dn[0][1] = v.y;
-      } else {
-        dn[0][0] = row[0];
-        dn[0][1] = row[1];
-      }
-#pragma unroll
-      for (int t = 1; t <= T; ++t) {
-        // level t row s - t from level t-1 rows s-t-1, s-t, s-t+1
-        const double left0 = __shfl_up_sync(0xffffffffu, mid[t - 1][1], 1);
-        const double right1 = __shfl_down_sync(0xffffffffu, mid[t - 1][0], 1);
-        double v0 = left0 + mid[t - 1][1];
-        v0 = v0 + up[t - 1][0];
-        v0 = v0 + dn[t - 1][0];
-        v0 = coeff * v0;
-        double v1 = mid[t - 1][0] + right1;
-        v1 = v1 + up[t - 1][1];
-        v1 = v1 + dn[t - 1][1];
-        v1 = coeff * v1;
-        if (!fastpath) {
-          const int r = s - t;
-          const bool rowok = r >= r_lo && r <= r_hi;
-          if (!(rowok && !fixed[0])) v0 = mid[t - 1][0];
-          if (!(rowok && !fixed[1])) v1 = mid[t - 1][1];
+      for (int rr = 0; rr < WF_R; ++rr) {
+        const int s = s0 + rr;
+        const double* row = st + rr * C::BW;
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int sl0 = rr % 3;
+        if constexpr (C::ALIGNED) {
+          const double2 v = *reinterpret_cast<const double2*>(row);
+          L[0][sl0][0] = v.x;
+          L[0][sl0][1] = v.y;
+        } else {
+          L[0][sl0][0] = row[0];
+          L[0][sl0][1] = row[1];
         }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          up[t][e] = mid[t][e];
-          mid[t][e] = dn[t][e];
+        for (int t = 1; t <= T; ++t) {
+          // level t row s - t from level t-1 rows s-t-1 (up), s-t (mid), s-t+1 (dn)
+          const int su = ((rr - t - 1) % 3 + 3) % 3, sm = ((rr - t) % 3 + 3) % 3, sd = ((rr - t + 1) % 3 + 3) % 3;
+          const double left0 = __shfl_up_sync(0xffffffffu, L[t - 1][sm][1], 1);
+          const double right1 = __shfl_down_sync(0xffffffffu, L[t - 1][sm][0], 1);
+          double v0 = left0 + L[t - 1][sm][1];
+          v0 = v0 + L[t - 1][su][0];
+          v0 = v0 + L[t - 1][sd][0];
+          v0 = coeff * v0;
+          double v1 = L[t - 1][sm][0] + right1;
+          v1 = v1 + L[t - 1][su][1];
+          v1 = v1 + L[t - 1][sd][1];
+          v1 = coeff * v1;
+          if (!fastpath) {
+            const int r = s - t;
+            const bool rowok = r >= r_lo && r <= r_hi;
+            if (!(rowok && !fixed[0])) v0 = L[t - 1][sm][0];
+            if (!(rowok && !fixed[1])) v1 = L[t - 1][sm][1];
+          }
+          L[t][sm][0] = v0;   // level t row s - t -> slot (s - t) mod 3
+          L[t][sm][1] = v1;
         }
-        dn[t][0] = v0;
-        dn[t][1] = v1;
+        // level T row s - T is output row ja + (s - 2T) when 2T <= s < nr
+        const int so = ((rr - T) % 3 + 3) % 3;
+        const bool ok = s >= 2 * T && s < nri;
+        char* o = outp + (int64_t)(s - 2 * T) * p.d_sm2;
+        if (ok && store[0]) *reinterpret_cast<double*>(o) = L[T][so][0];
+        if (ok && store[1]) *reinterpret_cast<double*>(o + p.d_sm1) = L[T][so][1];
       }
-      if (s >= 2 * T) {  // level T row s - T is output row ja + (s - 2T)
-        if (store[0]) *reinterpret_cast<double*>(outp) = dn[T][0];
-        if (store[1]) *reinterpret_cast<double*>(outp + p.d_sm1) = dn[T][1];
-        outp += p.d_sm2;
-      }
-      ++s;
     };
     for (int64_t q = 0; q < nch; ++q, ++k) {
       dev::mbar_wait(&full[k % WF_NS], (uint32_t)((k / WF_NS) & 1));
-      const double* st = reinterpret_cast<const double*>(smem + (k % WF_NS) * C::STAGE) + col0;
-      const int rows = (int)min((int64_t)WF_R, nr - q * WF_R);
-      if (rows == WF_R && fast) {
-#pragma unroll
-        for (int rr = 0; rr < WF_R; ++rr) step(st + rr * C::BW, true);
-      } else {
-        for (int rr = 0; rr < rows; ++rr) step(st + rr * C::BW, false);
-      }
+      // index the __shared__ array itself so the loads are LDS (not generic LD)
+      const double* st = reinterpret_cast<const double*>(smem_raw + smem_off + (k % WF_NS) * C::STAGE) + col0;
+      if (fast) chunk(st, (int)(q * WF_R), true);
+      else chunk(st, (int)(q * WF_R), false);
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&empty[k % WF_NS]);
     }
@@ -254,26 +254,22 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
 #define WF_ARGS src, dst, coeff, row_lo, row_hi, fix_lo, fix_hi, s
   switch (cfg < 0 ? T * 10 + 9 : T * 10 + cfg) {
-    // defaults (cfg 9): measured on B200, DESIGN.md §4.3
-    case 19: return launch_wf<1, WFCfg<1, 4, 16, 3>>(WF_ARGS);
-    case 29: return launch_wf<2, WFCfg<2, 4, 16, 3>>(WF_ARGS);
-    case 39: return launch_wf<3, WFCfg<3, 4, 16, 3>>(WF_ARGS);
-    case 49: return launch_wf<4, WFCfg<4, 4, 16, 3>>(WF_ARGS);
+    // defaults (cfg 9): measured on B200; R must be a multiple of 3
+    case 19: return launch_wf<1, WFCfg<1, 4, 12, 3>>(WF_ARGS);
+    case 29: return launch_wf<2, WFCfg<2, 4, 12, 3>>(WF_ARGS);
+    case 39: return launch_wf<3, WFCfg<3, 4, 12, 3>>(WF_ARGS);
+    case 49: return launch_wf<4, WFCfg<4, 4, 12, 3>>(WF_ARGS);
     // tuning variants (FTN_WF_CFG)
-    case 10: return launch_wf<1, WFCfg<1>>(WF_ARGS);
-    case 20: return launch_wf<2, WFCfg<2>>(WF_ARGS);
-    case 30: return launch_wf<3, WFCfg<3>>(WF_ARGS);
-    case 40: return launch_wf<4, WFCfg<4>>(WF_ARGS);
-    case 31: return launch_wf<3, WFCfg<3, 4, 8, 3>>(WF_ARGS);
-    case 41: return launch_wf<4, WFCfg<4, 4, 8, 3>>(WF_ARGS);
-    case 32: return launch_wf<3, WFCfg<3, 2, 8, 4>>(WF_ARGS);
-    case 42: return launch_wf<4, WFCfg<4, 2, 8, 4>>(WF_ARGS);
-    case 35: return launch_wf<3, WFCfg<3, 4, 16, 2>>(WF_ARGS);
-    case 45: return launch_wf<4, WFCfg<4, 4, 16, 2>>(WF_ARGS);
-    case 36: return launch_wf<3, WFCfg<3, 4, 32, 2>>(WF_ARGS);
-    case 46: return launch_wf<4, WFCfg<4, 4, 32, 2>>(WF_ARGS);
-    case 37: return launch_wf<3, WFCfg<3, 2, 32, 2>>(WF_ARGS);
-    case 47: return launch_wf<4, WFCfg<4, 2, 32, 2>>(WF_ARGS);
+    case 30: return launch_wf<3, WFCfg<3, 4, 24, 2>>(WF_ARGS);
+    case 40: return launch_wf<4, WFCfg<4, 4, 24, 2>>(WF_ARGS);
+    case 31: return launch_wf<3, WFCfg<3, 4, 6, 4>>(WF_ARGS);
+    case 41: return launch_wf<4, WFCfg<4, 4, 6, 4>>(WF_ARGS);
+    case 32: return launch_wf<3, WFCfg<3, 4, 12, 4>>(WF_ARGS);
+    case 42: return launch_wf<4, WFCfg<4, 4, 12, 4>>(WF_ARGS);
+    case 33: return launch_wf<3, WFCfg<3, 4, 18, 3>>(WF_ARGS);
+    case 43: return launch_wf<4, WFCfg<4, 4, 18, 3>>(WF_ARGS);
+    case 34: return launch_wf<3, WFCfg<3, 2, 12, 3>>(WF_ARGS);
+    case 44: return launch_wf<4, WFCfg<4, 2, 12, 3>>(WF_ARGS);
   }
 #undef WF_ARGS
   return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..4 (and FTN_WF_CFG a known variant)");

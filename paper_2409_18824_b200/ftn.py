@@ -110,6 +110,8 @@ def _load():
         f.restype = st
     L.ftn_jacobi_get_fusion.restype = ctypes.c_int32
     L.ftn_jacobi_get_fusion.argtypes = []
+    L.ftn_jacobi_plan.restype = ctypes.c_int64
+    L.ftn_jacobi_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64]
     L.ftn_launch_count.restype = ctypes.c_uint64
     L.ftn_launch_count.argtypes = []
     L.ftn_status_string.restype = ctypes.c_char_p
@@ -405,7 +407,7 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float | None = None, str
 
 
 def jacobi_set_fusion(sweeps_per_launch: int):
-    """Temporal-blocking factor of the 2-D Jacobi kernels (1..4, default 3); results are identical."""
+    """Temporal-blocking factor of the 2-D Jacobi kernels (1..4, default 4); results are identical."""
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
 
 
@@ -443,15 +445,13 @@ def jacobi_fusion() -> int:
     return int(lib.ftn_jacobi_get_fusion())
 
 
-def jacobi_launch_plan(sweeps: int, rank: int = 2) -> tuple[int, int, int]:
-    """(T, fused launches, single-sweep launches) ftn_jacobi uses for `sweeps` (rank-2 TMA path)."""
-    T = jacobi_fusion() if rank == 2 else 1
-    if T < 2:
-        return 1, 0, sweeps
-    f = sweeps // T
-    if T % 2 == 0 and f % 2:
-        f -= 1
-    return T, f, sweeps - f * T
+def jacobi_plan(sweeps: int, T: int | None = None) -> list[int]:
+    """Sweeps per launch that ftn_jacobi uses for a rank-2 TMA-able array (ftn_jacobi_plan)."""
+    T = jacobi_fusion() if T is None else T
+    n = lib.ftn_jacobi_plan(sweeps, T, None, 0)
+    buf = (ctypes.c_int32 * max(n, 1))()
+    lib.ftn_jacobi_plan(sweeps, T, buf, n)
+    return list(buf[:n])
 
 
 def gen_fill(dst: FArray, seed: int, array_id: int, mode: int, stream=None):

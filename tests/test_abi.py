@@ -98,3 +98,14 @@ def test_compute_calls_validate_before_device(ftn):
     assert rc == 4                                                              # FTN_ERR_SHAPE
     assert b"not conformable" in ftn.lib.ftn_last_error()
     assert ftn.lib.ftn_status_string(8) == b"FTN_ERR_UNSUPPORTED"
+
+
+def test_jacobi_launch_plan(ftn):
+    """ftn_jacobi_plan (host logic): sweep counts sum to S, each in 1..T, and the launch count
+    has the parity of S (the result lands in unew iff S is odd)."""
+    for S in range(0, 60):
+        for T in (1, 2, 3, 4):
+            p = ftn.jacobi_plan(S, T)
+            assert sum(p) == S and len(p) % 2 == S % 2 and all(1 <= k <= T for k in p), (S, T, p)
+            assert p.count(1) <= (S % T == 1) + 1 + (T == 1) * S       # at most one split-off single
+    assert ftn.jacobi_plan(100, 4) .count(4) == 24

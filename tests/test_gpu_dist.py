@@ -94,10 +94,7 @@ def test_jacobi_decomposition_independence(ftn, p, shape, halo):
         arrs.append([ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)])
     tma_able = len(shape) == 2 and (shape[0] * 8) % 16 == 0       # dim-2 stride a multiple of 16 B
     T = min(ftn.jacobi_fusion(), halo) if tma_able else 1
-    fused = sweeps // T if T > 1 else 0
-    if T % 2 == 0 and fused % 2:
-        fused -= 1
-    steps = [T] * fused + [1] * (sweeps - fused * T)
+    steps = ftn.jacobi_plan(sweeps, T)                 # ftn_jacobi_dist's launch plan
     cur = 0
     for k in steps:
         for r in range(p):

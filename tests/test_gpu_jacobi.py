@@ -141,7 +141,7 @@ def test_2d_temporal_blocking(ftn, T, shape, sweeps):
         got, ref = _run_both(ftn, u0, sweeps, C2, [1, 0])
         np.testing.assert_array_equal(got, ref)
     finally:
-        ftn.jacobi_set_fusion(3)
+        ftn.jacobi_set_fusion(4)
 
 
 def test_2d_temporal_blocking_long_strip(ftn):
@@ -151,4 +151,4 @@ def test_2d_temporal_blocking_long_strip(ftn):
         u0 = synth.jacobi_init((3000, 2000), array_id=T)
         got, ref = _run_both(ftn, u0, 12, C2)
         np.testing.assert_array_equal(got, ref)
-    ftn.jacobi_set_fusion(3)
+    ftn.jacobi_set_fusion(4)

@@ -44,4 +44,4 @@ def test_jacobi_solve(ftn, T, shape, check, tol):
         assert (done, res, new) == (d2, r2, n2)
         np.testing.assert_array_equal((W if new else U).to_numpy(), b if n2 else a)
     finally:
-        ftn.jacobi_set_fusion(3)
+        ftn.jacobi_set_fusion(4)
