@@ -144,7 +144,7 @@ def jacobi_faces(ftn, U, n1, n2):
 def bench_jacobi2d(torch, ftn, args, ctx):
     n, sweeps = 8192, 100
     N, rank = ctx["world"], ctx["rank"]
-    if N == 1:
+    if N == 1 and not ctx.get("force_dist"):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
         jacobi_faces(ftn, U, n, n)
         ftn.assign(W, U)
@@ -211,6 +211,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
     steps, warm = max(3, args.steps // 2), 2
     dist = ctx["dist"]
     comm = ctx.get("comm")
+    distmode = N > 1 or bool(ctx.get("force_dist"))   # the NCCL code paths (also at N = 1 with --dist)
 
     def gbs_row(name, nbytes, fn, units=None):
         t = timed(torch, fn, steps, warm, None, dist)
@@ -230,7 +231,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         n_el = 1024 * 1024 * nk
         gbs_row("c4_muladd_r=b*c+d", 32 * n_el, lambda: ftn.muladd(r, b, c, d))
         out = torch.empty((), dtype=torch.float64, device="cuda")
-        if N == 1:
+        if not distmode:
             gbs_row("c4_sum", 8 * n_el, lambda: ftn.sum(b, out))
             gbs_row("c4_maxval", 8 * n_el, lambda: ftn.maxval(b, out))
             gbs_row("c4_minval", 8 * n_el, lambda: ftn.minval(b, out))
@@ -272,7 +273,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         C = ftn.FArray.empty((n, nc))
         ftn.gen_fill(A, SEED, 1, ftn.GEN_U11)
         ftn.gen_fill(B, SEED, 2 + rank, ftn.GEN_U11)
-        fn = (lambda: ftn.matmul(C, A, B)) if N == 1 else (lambda: comm.matmul(C, A, B))
+        fn = (lambda: ftn.matmul(C, A, B)) if not distmode else (lambda: comm.matmul(C, A, B))
         t = timed(torch, fn, steps, warm, ctx["clocks"], dist)
         tf = 2.0 * n * n * n * steps / t / 1e12
         rows["c3_matmul_8192"] = {"value": tf, "unit": "TFLOP/s", "ms": t / steps * 1e3,
@@ -333,7 +334,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
     if "c5" in args.rows:
         n, sweeps = 2048, 10
         free = torch.cuda.mem_get_info()[0]
-        if N == 1:
+        if not distmode:
             need = 2 * n ** 3 * 8
             if free > need + (2 << 30):
                 U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
@@ -441,6 +442,8 @@ def main():
     ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
     ap.add_argument("--rows", default="c4,c3,paper,c5", help="comma list of extra rows, or 'none'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")
     args = ap.parse_args()
     args.rows = [] if args.rows == "none" else args.rows.split(",")
     if args.impl == "reference":
@@ -452,10 +455,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    ctx = {"world": world, "rank": rank, "dist": None}
+    ctx = {"world": world, "rank": rank, "dist": None, "force_dist": args.dist}
     from paper_2409_18824_b200 import ftn
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         ctx["dist"] = dist
         ctx["comm"] = ftn.Comm.from_torch_distributed(local)
@@ -495,7 +503,7 @@ def main():
             "rows": rows,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if ctx.get("comm") is not None:
         ctx["comm"].destroy()
         dist.destroy_process_group()
     return 0

@@ -23,11 +23,11 @@ def main(which):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
-        ftn.jacobi(U, W, 3)      # one fused launch (3 sweeps, jacobi2d_wf<3>)
-        ftn.jacobi(U, W, 3)
+        ftn.jacobi(U, W, 4)      # one fused launch (4 sweeps, jacobi2d_wf<4>), the default
+        ftn.jacobi(U, W, 4)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi2d_tma)
-        ftn.jacobi_set_fusion(3)
+        ftn.jacobi_set_fusion(4)
         del U, W
     if "jacobi3d" in which:
         n = 512
