@@ -181,24 +181,29 @@ def bench_jacobi2d(torch, ftn, args, ctx):
            "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes,
            "plan": {"max_sweeps_per_launch": halo_T, "launches_per_step": len(plan),
                     "sweeps_per_launch": {str(k): plan.count(k) for k in sorted(set(plan))}}}
-    # ---- e2e: through the C ABI from pinned host buffers (H2D of u, D2H of the result inside)
-    if N == 1:
-        # pinned host buffers with the Fortran (column-major) layout: the copies are plain DMAs
-        host_u = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
-        host_u.copy_(U.tensor)
-        host_out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
-        U2, W2 = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+    # ---- e2e: through the C ABI from pinned host buffers (H2D of u, D2H of the result inside);
+    # at N > 1 every rank moves its own slab, timed as the max over ranks
+    shape = tuple(U.shape)
+    host_u = torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True).t()   # Fortran layout
+    host_u.copy_(U.tensor)
+    host_out = torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True).t()
+    U2, W2 = ftn.FArray.empty(shape), ftn.FArray.empty(shape)
+    dist_path = not (N == 1 and not ctx.get("force_dist"))
+    halo_e2e = max(1, ftn.jacobi_fusion())
 
-        def e2e_step():
-            U2.tensor.copy_(host_u, non_blocking=True)
-            ftn.assign(W2, U2)
-            new = ftn.jacobi(U2, W2, sweeps)
-            host_out.copy_((W2 if new else U2).tensor, non_blocking=True)
+    def e2e_step():
+        U2.tensor.copy_(host_u, non_blocking=True)
+        ftn.assign(W2, U2)
+        new = ctx["comm"].jacobi(U2, W2, sweeps, halo=halo_e2e) if dist_path else ftn.jacobi(U2, W2, sweeps)
+        host_out.copy_((W2 if new else U2).tensor, non_blocking=True)
 
-        te = timed(torch, e2e_step, max(3, args.steps // 2), 1, None, None)
-        res["e2e"] = {"value": interior * sweeps * max(3, args.steps // 2) / te / 1e9, "unit": "GLUPS",
-                      "h2d_bytes_per_step": host_u.numel() * 8, "d2h_bytes_per_step": host_out.numel() * 8}
-        del host_u, host_out, U2, W2
+    ne = max(3, args.steps // 2)
+    te = timed(torch, e2e_step, ne, 1, None, ctx["dist"])
+    res["e2e"] = {"value": interior * sweeps * ne / te / 1e9, "unit": "GLUPS",
+                  "h2d_bytes_per_step": host_u.numel() * 8 * N, "d2h_bytes_per_step": host_out.numel() * 8 * N,
+                  "note": "per step: H2D of u from pinned host memory, device copy u -> unew (boundary), "
+                          "the 100 sweeps, D2H of the result; bytes summed over ranks"}
+    del host_u, host_out, U2, W2
     del U, W
     torch.cuda.empty_cache()
     return res
