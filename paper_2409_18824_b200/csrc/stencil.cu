@@ -49,6 +49,7 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 }
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
+ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s);
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                                  int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 
@@ -478,6 +479,21 @@ int jacobi_fuse_T() {
   return t;
 }
 
+// Sweeps per launch for this array: T (<= 4) for TMA-able rank-2 arrays, min(T, 2) for
+// TMA-able rank-3 arrays (jacobi3d_tb2), 1 otherwise.
+int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
+  const int T = jacobi_fuse_T();
+  if (T < 2 || !stencil_tma_able(u) || !stencil_tma_able(unew)) return 1;
+  for (int d = 0; d < u->rank; ++d)
+    if (u->dim[d].extent < 3) return 1;
+  return u->rank == 2 ? T : 2;
+}
+
+// k >= 2 fused sweeps src -> dst
+ftn_status_t jacobi_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int k, double coeff, cudaStream_t s) {
+  return src->rank == 2 ? jacobi2d_fused(src, dst, k, coeff, s) : jacobi3d_fused2(src, dst, coeff, s);
+}
+
 ftn_status_t jacobi_prepare() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -542,12 +558,12 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
   // Temporal blocking: launches of up to T fused sweeps (ftn_jacobi_plan).
   // Every launch swaps u/unew; the plan's launch count has the parity of `sweeps`, so the
   // result lands in unew iff sweeps is odd.
-  const int T = jacobi_fuse_T();
-  const bool can_fuse = tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3;
+  const int T = jacobi_fuse_for(u, unew);
+  const bool can_fuse = T >= 2 && u->rank == 2;
   static const bool wf1 = getenv("FTN_JACOBI_WF1") && atoi(getenv("FTN_JACOBI_WF1")) != 0;
-  const int64_t nplan = ftn_jacobi_plan(sweeps, can_fuse ? T : 1, nullptr, 0);
+  const int64_t nplan = ftn_jacobi_plan(sweeps, T, nullptr, 0);
   std::vector<int32_t> plan((size_t)nplan);
-  ftn_jacobi_plan(sweeps, can_fuse ? T : 1, plan.data(), nplan);
+  ftn_jacobi_plan(sweeps, T, plan.data(), nplan);
   int64_t launches = 0;
   for (; launches < nplan; ++launches) {
     const bool even = (launches % 2) == 0;
@@ -555,7 +571,7 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     const ftn_desc_t* dst = even ? unew : u;
     const int k = plan[(size_t)launches];
     if (k >= 2 || (wf1 && can_fuse))
-      FTN_CHECK(jacobi2d_fused(src, dst, k, coeff, s));
+      FTN_CHECK(jacobi_fused(src, dst, k, coeff, s));
     else
       FTN_CHECK(sweep(src, dst, tma ? (even ? &mu : &mw) : nullptr, coeff, 1, nlast - 2, s));
   }
@@ -614,8 +630,7 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
   const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
-  const int T = jacobi_fuse_T();
-  const bool can_fuse = tma && u->rank == 2 && T >= 2 && u->dim[0].extent >= 3 && u->dim[1].extent >= 3;
+  const int T = jacobi_fuse_for(u, unew);
   double* res_dev = reinterpret_cast<double*>(ws);
   char* rw = reinterpret_cast<char*>(ws) + 16;
   int cur = 0;  // 0: u holds the newest iterate
@@ -626,13 +641,13 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
     const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
     // the first k-1 sweeps by the plan of ftn_jacobi (launch count of their parity), then
     // one single sweep, so the two arrays end up holding consecutive iterates
-    const int64_t np = ftn_jacobi_plan(k - 1, can_fuse ? T : 1, nullptr, 0);
+    const int64_t np = ftn_jacobi_plan(k - 1, T, nullptr, 0);
     std::vector<int32_t> plan((size_t)np);
-    ftn_jacobi_plan(k - 1, can_fuse ? T : 1, plan.data(), np);
+    ftn_jacobi_plan(k - 1, T, plan.data(), np);
     int64_t left = 1;
     for (int32_t kk : plan) {
       if (kk >= 2) {
-        FTN_CHECK(jacobi2d_fused(cur ? unew : u, cur ? u : unew, kk, coeff, s));
+        FTN_CHECK(jacobi_fused(cur ? unew : u, cur ? u : unew, kk, coeff, s));
         cur ^= 1;
       } else {
         left += 1;

@@ -152,3 +152,59 @@ def test_2d_temporal_blocking_long_strip(ftn):
         got, ref = _run_both(ftn, u0, 12, C2)
         np.testing.assert_array_equal(got, ref)
     ftn.jacobi_set_fusion(4)
+
+
+@pytest.mark.parametrize("T", [1, 2])
+@pytest.mark.parametrize("shape", [(3, 3, 3), (4, 5, 6), (61, 29, 5), (62, 30, 6), (63, 31, 4), (121, 57, 9),
+                                   (130, 18, 7), (64, 64, 64), (200, 90, 40), (17, 100, 33)])
+@pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 5])
+def test_3d_temporal_blocking(ftn, T, shape, sweeps):
+    """Rank-3 launches of two fused sweeps (jacobi3d_tb2) are bit-identical to
+    the oracle's DO nest; tiles of 60 x 28 outputs, so these shapes cover one tile, exact
+    multiples and ragged tails in i and j."""
+    ftn.jacobi_set_fusion(T)
+    try:
+        u0 = synth.jacobi_init(shape, array_id=sum(shape) + sweeps)
+        got, ref = _run_both(ftn, u0, sweeps, C3, [0, 2, -1])
+        np.testing.assert_array_equal(got, ref)
+    finally:
+        ftn.jacobi_set_fusion(4)
+
+
+def test_3d_temporal_blocking_many_units(ftn):
+    """More units than CTAs (several k segments per tile column), random data, 6 sweeps."""
+    u0 = np.asfortranarray(synth.farray((250, 180, 150), array_id=9, mode=synth.U11))
+    got, ref = _run_both(ftn, u0, 6, C3)
+    np.testing.assert_array_equal(got, ref)
+    i, j, k = np.meshgrid(np.arange(130.0), np.arange(60.0), np.arange(50.0), indexing="ij")
+    u3 = np.asfortranarray(i - 2 * j + 3 * k)
+    got, _ = _run_both(ftn, u3, 4, C3)
+    np.testing.assert_array_equal(got, u3)
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(ftn):
+    """C5 at full size (2048^3, 10 sweeps, the bench's launch configuration): sampled points
+    recomputed by the oracle on their dependence cone (a 23^3 window), bit-exact."""
+    n, sweeps = 2048, 10
+    U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
+    ftn.gen_fill(U, synth.SEED, 0, ftn.GEN_U01)
+    ftn.assign(W, U)
+    rng = np.random.default_rng(5)
+    pts = [(1, 1, 1), (n - 2, n - 2, n - 2), (0, 7, 9), (1000, 1, 1000), (59, 27, 300), (60, 28, 301)] + \
+          [tuple(int(v) for v in rng.integers(0, n, 3)) for _ in range(8)]
+    R = sweeps + 1
+    wins = []
+    for p in pts:
+        lo = [max(0, c - R) for c in p]
+        hi = [min(n, c + R + 1) for c in p]
+        sec = U.section(*[(a + 1, b) for a, b in zip(lo, hi)])
+        wins.append((p, lo, np.asfortranarray(sec.to_numpy())))
+    in_new = ftn.jacobi(U, W, sweeps)
+    res = W if in_new else U
+    for p, lo, win in wins:
+        a, b = win.copy(order="F"), win.copy(order="F")
+        new = oracle.jacobi(OA(a), OA(b), sweeps, C3)
+        ref = (b if new else a)[tuple(c - l for c, l in zip(p, lo))]
+        got = res.section(*[(c + 1, c + 1) for c in p]).to_numpy().ravel()[0]
+        assert got == ref, p
