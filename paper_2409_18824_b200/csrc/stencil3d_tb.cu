@@ -3,16 +3,27 @@
 //
 // A CTA owns a (64-4) x (32-4) column of output points and streams it along k:
 //   * level 0 (the input u) arrives plane by plane as TMA boxes {64 x 32 x 1} (start 2
-//     columns/rows before the tile: halo 2 for two sweeps; dim-0 start 16-byte aligned) into
-//     a 6-slot mbarrier ring filled by one producer lane;
-//   * when input plane q has landed, every thread computes level 1 (sweep 1) of plane q-1 on
-//     the box interior [1,63) x [1,31) into a 4-slot shared-memory ring, then (one block
-//     barrier) level 2 (sweep 2) of plane q-2 on [2,62) x [2,30), which is stored;
-//   * thread (x, jb) owns box column x and rows 8 jb .. 8 jb + 7 of every plane.
-// The 4-slot level-1 ring makes one barrier per plane sufficient: the slot written by
-// level 1 of plane q+1 was last read by level 2 of plane q-2, which every thread finished
-// before the barrier of step q+1.  Global boundary points keep their value at every level.
+//     columns/rows before the tile: halo 2 for two sweeps; dim-0 start 16-byte aligned, the
+//     output rows 32-byte aligned) into an 8-slot mbarrier ring; thread 0 refills the slot of
+//     plane q-1 right after the block barrier of step q (every warp has finished reading it
+//     by then), so there is no producer warp and no empty barrier: 16 warps = 4 per SM
+//     sub-partition share the register file evenly;
+//   * thread (x, y0) owns box column x, rows y0 .. y0+R-1 of every plane and keeps its own
+//     values of three consecutive planes of level 0 and of level 1 in register rings
+//     (slot = plane mod 3, compile-time after unrolling the plane loop by 3);
+//   * at step q (input plane q landed) it computes level 1 (sweep 1) of plane q-1: the k and
+//     own-row j neighbours come from registers, the i neighbours and the two halo rows from
+//     shared memory; level 1 is also written to a 3-slot shared ring for the neighbours'
+//     benefit; then, after one block barrier, level 2 (sweep 2) of plane q-2 the same way,
+//     stored to HBM.
+// The 3-slot level-1 ring is safe with one barrier per step: the slot written at step q was
+// last read at step q-2, before the barrier of step q-1.  Global boundary points keep their
+// value at every level.
 #include "ftn_internal.cuh"
+
+#ifndef FTN_J3_ROWS
+#define FTN_J3_ROWS 4
+#endif
 
 namespace ftn {
 
@@ -22,12 +33,12 @@ namespace {
 
 constexpr int B3_X = 64, B3_Y = 32;                  // box (level 0) extent in i, j
 constexpr int B3_OX = B3_X - 4, B3_OY = B3_Y - 4;    // output tile 60 x 28
-constexpr int B3_PLANE = B3_X * B3_Y * 8;            // 16 KB
-constexpr int B3_NS0 = 6, B3_NS1 = 4;        // level-0 TMA ring, level-1 ring
-constexpr int B3_ROWS = 8;                           // j rows per thread
-constexpr int B3_CT = B3_X * (B3_Y / B3_ROWS);       // 256 compute threads
-constexpr int B3_THREADS = B3_CT + 32;
-constexpr int B3_SMEM = (B3_NS0 + B3_NS1) * B3_PLANE + 128 + 64;
+constexpr int B3_PE = B3_X * B3_Y;                   // elements per plane
+constexpr int B3_PLANE = B3_PE * 8;                  // 16 KB
+constexpr int B3_NS0 = 8, B3_NS1 = 3;                // level-0 TMA ring, level-1 ring
+constexpr int B3_ROWS = FTN_J3_ROWS;                 // j rows per thread
+constexpr int B3_THREADS = B3_X * (B3_Y / B3_ROWS);  // 512 at 4 rows
+constexpr int B3_SMEM = (B3_NS0 + B3_NS1) * B3_PLANE + 128 + 8 * B3_NS0;
 
 struct J3TParams {
   char* dst;
@@ -38,7 +49,120 @@ struct J3TParams {
   double coeff;
 };
 
-__device__ __forceinline__ void bar_compute3() { asm volatile("bar.sync 1, %0;" ::"n"(B3_CT) : "memory"); }
+// Unit u -> (tile origin, output planes [ka, kb)); 32-bit (units, tiles < 2^31).
+struct J3Geom {
+  int32_t ntile, tiles_i, seg, n3;
+  __device__ __forceinline__ void unit(uint32_t u, int32_t& i0, int32_t& j0, int32_t& ka, int32_t& kb) const {
+    const uint32_t t = u % (uint32_t)ntile, sgi = u / (uint32_t)ntile;
+    i0 = (int32_t)(t % (uint32_t)tiles_i) * B3_OX - 2;
+    j0 = (int32_t)(t / (uint32_t)tiles_i) * B3_OY - 2;
+    ka = 1 + (int32_t)sgi * seg;
+    kb = min(ka + seg, n3 - 1);
+  }
+};
+
+// Plane cursor of the TMA issuer (thread 0): walks (unit, k) in consumption order.
+struct J3Cursor {
+  uint32_t u;
+  int32_t kk, kend, ci, cj;
+};
+
+__device__ __forceinline__ void cursor_unit(J3Cursor& c, const J3Geom& G) {
+  int32_t ka, kb;
+  G.unit(c.u, c.ci, c.cj, ka, kb);
+  c.kk = ka - 2;
+  c.kend = kb + 2;
+}
+
+// Issues the next plane (if any) into slot g % NS0.
+__device__ __forceinline__ void cursor_issue(J3Cursor& c, const J3Geom& G, uint32_t units, const CUtensorMap* map,
+                                             uint8_t* smem, uint64_t* full, uint32_t g) {
+  if (c.u >= units) return;
+  const int s = (int)(g % B3_NS0);
+  dev::mbar_arrive_expect_tx(&full[s], B3_PLANE);
+  dev::tma_load_3d(smem + s * B3_PLANE, map, &full[s], c.ci, c.cj, c.kk);
+  if (++c.kk == c.kend) {
+    c.u += gridDim.x;
+    if (c.u < units) cursor_unit(c, G);
+  }
+}
+
+// Per-thread state of the compute warps (smem offsets in elements).
+struct J3Unit {
+  const double* L0;   // level-0 ring base
+  double* L1;         // level-1 ring base
+  uint64_t* full;
+  char* out;          // &dst(gi, gj0 + y0, 0)
+  int64_t d_sm2, d_sm3;
+  double c;
+  int own, xm, xp, ylo, yhi;  // element offsets in a plane: own (y0, x), x-1, x+1, rows y0-1, y0+R (clamped)
+  int qlo, qhi;       // level 1 keeps plane q-1 when q <= qlo or q >= qhi (global boundary planes)
+  int ka;
+  uint32_t fix_rows;  // bit r: level 1 keeps row r (boundary row or boundary column)
+  uint32_t st_rows;   // bit r: level 2 stores row r (0 for a column that is not stored)
+};
+
+template <int PH>
+__device__ __forceinline__ void tb3_step(const J3Unit& U, int q, uint32_t gq, double (&a)[3][B3_ROWS],
+                                         double (&b)[3][B3_ROWS]) {
+  constexpr int P0 = PH, P1 = (PH + 2) % 3, P2 = (PH + 1) % 3;  // ring slots of planes q, q-1, q-2
+  dev::mbar_wait(&U.full[gq % B3_NS0], (uint32_t)((gq / B3_NS0) & 1));
+  {
+    const double* Lq = U.L0 + (gq % B3_NS0) * B3_PE + U.own;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) a[P0][r] = Lq[r * B3_X];
+  }
+  if (q >= 2) {  // level 1 of plane q-1 (ring slot P1 of the 3-slot shared level-1 ring too)
+    const double* Lp = U.L0 + ((gq - 1) % B3_NS0) * B3_PE;
+    double xl[B3_ROWS], xr[B3_ROWS];
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      xl[r] = Lp[U.xm + r * B3_X];
+      xr[r] = Lp[U.xp + r * B3_X];
+    }
+    const double ylo = Lp[U.ylo], yhi = Lp[U.yhi];
+    const uint32_t keep = (q <= U.qlo || q >= U.qhi) ? 0xffffffffu : U.fix_rows;
+    double* W = U.L1 + P1 * B3_PE + U.own;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      const double up = r == 0 ? ylo : a[P1][r - 1];
+      const double dn = r == B3_ROWS - 1 ? yhi : a[P1][r + 1];
+      double v = xl[r] + xr[r];
+      v = v + up;
+      v = v + dn;
+      v = v + a[P2][r];
+      v = v + a[P0][r];
+      v = U.c * v;
+      v = ((keep >> r) & 1) ? a[P1][r] : v;
+      b[P1][r] = v;
+      W[r * B3_X] = v;
+    }
+  }
+  __syncthreads();
+  if (q >= 4) {  // level 2 of plane q-2 (an output plane of this unit): level-1 slots P1, P2, P0 = planes q-1, q-2, q-3
+    const double* Lr = U.L1 + P2 * B3_PE;
+    double xl[B3_ROWS], xr[B3_ROWS];
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      xl[r] = Lr[U.xm + r * B3_X];
+      xr[r] = Lr[U.xp + r * B3_X];
+    }
+    const double ylo = Lr[U.ylo], yhi = Lr[U.yhi];
+    char* out = U.out + (int64_t)(U.ka - 4 + q) * U.d_sm3;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      const double up = r == 0 ? ylo : b[P2][r - 1];
+      const double dn = r == B3_ROWS - 1 ? yhi : b[P2][r + 1];
+      double v = xl[r] + xr[r];
+      v = v + up;
+      v = v + dn;
+      v = v + b[P0][r];
+      v = v + b[P1][r];
+      v = U.c * v;
+      if ((U.st_rows >> r) & 1) *reinterpret_cast<double*>(out + r * U.d_sm2) = v;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(B3_THREADS, 1) jacobi3d_tb2(const __grid_constant__ CUtensorMap map,
                                                               const __grid_constant__ J3TParams p) {
@@ -46,121 +170,81 @@ __global__ void __launch_bounds__(B3_THREADS, 1) jacobi3d_tb2(const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const uint32_t soff = (uint32_t)(smem - smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (B3_NS0 + B3_NS1) * B3_PLANE);
-  uint64_t* empty = full + B3_NS0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  J3Geom G;
+  G.ntile = (int32_t)(p.tiles_i * p.tiles_j);
+  G.tiles_i = (int32_t)p.tiles_i;
+  G.seg = (int32_t)p.seg;
+  G.n3 = (int32_t)p.n3;
+  const uint32_t units = (uint32_t)p.units;
+  J3Cursor cur;
+  cur.u = blockIdx.x;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < B3_NS0; ++s) {
-      dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], B3_CT / 32);
-    }
+    for (int s = 0; s < B3_NS0; ++s) dev::mbar_init(&full[s], 1);
     dev::fence_barrier_init();
+    dev::prefetch_tma(&map);
+    if (cur.u < units) cursor_unit(cur, G);
+    for (uint32_t g = 0; g < B3_NS0; ++g) cursor_issue(cur, G, units, &map, smem, full, g);
   }
   __syncthreads();
-  const int64_t G = gridDim.x;
-  const int64_t ntile = p.tiles_i * p.tiles_j;
-  const int64_t nk = p.n3 - 2;
 
-  if (warp == B3_CT / 32) {
-    if (lane == 0) {
-      dev::prefetch_tma(&map);
-      int64_t g = 0;
-      for (int64_t u = blockIdx.x; u < p.units; u += G) {
-        const int64_t t = u % ntile;
-        const int32_t ci = (int32_t)((t % p.tiles_i) * B3_OX - 2), cj = (int32_t)((t / p.tiles_i) * B3_OY - 2);
-        const int64_t ka = 1 + (u / ntile) * p.seg, kb = min(ka + p.seg, 1 + nk);
-        for (int64_t kk = ka - 2; kk < kb + 2; ++kk, ++g) {
-          const int s = (int)(g % B3_NS0);
-          if (g >= B3_NS0) dev::mbar_wait(&empty[s], (uint32_t)(((g / B3_NS0) - 1) & 1));
-          dev::mbar_arrive_expect_tx(&full[s], B3_PLANE);
-          dev::tma_load_3d(smem + s * B3_PLANE, &map, &full[s], ci, cj, (int32_t)kk);
-        }
-      }
-      for (int64_t q = g - B3_NS0 > 0 ? g - B3_NS0 : 0; q < g; ++q)  // producer tail
-        dev::mbar_wait(&empty[q % B3_NS0], (uint32_t)((q / B3_NS0) & 1));
-    }
-    return;
-  }
-
-  const int x = threadIdx.x % B3_X;            // box column
-  const int y0 = (threadIdx.x / B3_X) * B3_ROWS;  // first box row of this thread
-  const double c = p.coeff;
-  const double* L0 = reinterpret_cast<const double*>(smem_raw + soff);
-  double* L1 = reinterpret_cast<double*>(smem_raw + soff + B3_NS0 * B3_PLANE);
-  int64_t g = 0;  // global level-0 plane counter (ring slots / phases)
-  for (int64_t u = blockIdx.x; u < p.units; u += G) {
-    const int64_t t = u % ntile;
-    const int64_t gi0 = (t % p.tiles_i) * B3_OX - 2, gj0 = (t / p.tiles_i) * B3_OY - 2;  // global (i, j) of box (0, 0)
-    const int64_t ka = 1 + (u / ntile) * p.seg, kb = min(ka + p.seg, 1 + nk);
-    const int nq = (int)(kb - ka + 4);                 // level-0 planes ka-2 .. kb+1
-    const int64_t gi = gi0 + x;
+  J3Unit U;
+  U.L0 = reinterpret_cast<const double*>(smem_raw + soff);
+  U.L1 = reinterpret_cast<double*>(smem_raw + soff + B3_NS0 * B3_PLANE);
+  U.full = full;
+  U.d_sm2 = p.d_sm2;
+  U.d_sm3 = p.d_sm3;
+  U.c = p.coeff;
+  const int x = threadIdx.x % B3_X, y0 = (threadIdx.x / B3_X) * B3_ROWS;
+  U.own = y0 * B3_X + x;
+  U.xm = y0 * B3_X + (x > 0 ? x - 1 : 0);
+  U.xp = y0 * B3_X + (x < B3_X - 1 ? x + 1 : B3_X - 1);
+  U.ylo = (y0 > 0 ? y0 - 1 : 0) * B3_X + x;                            // unused when y0 == 0
+  U.yhi = (y0 + B3_ROWS < B3_Y ? y0 + B3_ROWS : B3_Y - 1) * B3_X + x;  // unused when y0 + R == 32
+  double a[3][B3_ROWS], b[3][B3_ROWS];
+  uint32_t g = 0;  // level-0 planes consumed so far (ring slot / phase)
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    int32_t i0, j0, ka, kb;
+    G.unit(u, i0, j0, ka, kb);
+    const int64_t gi = i0 + x;
+    U.ka = ka;
+    // level 1 at step q is plane ka - 3 + q: a boundary plane when <= 0 or >= n3 - 1
+    U.qlo = 3 - ka;
+    U.qhi = G.n3 + 2 - ka;
     const bool col_fixed = gi <= 0 || gi >= p.n1 - 1;
-    const int64_t g0 = g;
-    for (int q = 0; q < nq; ++q) {
-      const int64_t gq = g0 + q;
-      dev::mbar_wait(&full[gq % B3_NS0], (uint32_t)((gq / B3_NS0) & 1));
-      // ---- level 1 of plane q-1 (global k = ka - 2 + q - 1) from level-0 planes q-2, q-1, q
-      if (q >= 2) {
-        const double* P0 = L0 + ((gq - 1) % B3_NS0) * (B3_X * B3_Y);
-        const double* Pm = L0 + ((gq - 2) % B3_NS0) * (B3_X * B3_Y);
-        const double* Pp = L0 + (gq % B3_NS0) * (B3_X * B3_Y);
-        double* O = L1 + ((q - 1) & 3) * (B3_X * B3_Y);
-        const int64_t gk = ka - 2 + q - 1;
-        const bool plane_fixed = gk <= 0 || gk >= p.n3 - 1;
-        if (x >= 1 && x < B3_X - 1) {
+    const bool st_col = x >= 2 && x < B3_X - 2 && gi >= 1 && gi <= p.n1 - 2;
+    U.out = p.dst + gi * p.d_sm1 + (int64_t)(j0 + y0) * p.d_sm2;
+    U.fix_rows = 0;
+    U.st_rows = 0;
 #pragma unroll
-          for (int r = 0; r < B3_ROWS; ++r) {
-            const int y = y0 + r;
-            if (y < 1 || y >= B3_Y - 1) continue;
-            const int o = y * B3_X + x;
-            const int64_t gj = gj0 + y;
-            double v = P0[o - 1] + P0[o + 1];
-            v = v + P0[o - B3_X];
-            v = v + P0[o + B3_X];
-            v = v + Pm[o];
-            v = v + Pp[o];
-            v = c * v;
-            if (col_fixed || plane_fixed || gj <= 0 || gj >= p.n2 - 1) v = P0[o];
-            O[o] = v;
-          }
-        }
-        // level-0 plane q-2 is no longer needed by anyone after this step's level 1
-        __syncwarp();
-        if (lane == 0) dev::mbar_arrive(&empty[(gq - 2) % B3_NS0]);
+    for (int r = 0; r < B3_ROWS; ++r) {
+      const int y = y0 + r;
+      const int64_t gj = j0 + y;
+      if (col_fixed || gj <= 0 || gj >= p.n2 - 1) U.fix_rows |= 1u << r;
+      if (st_col && y >= 2 && y < B3_Y - 2 && gj >= 1 && gj <= p.n2 - 2) U.st_rows |= 1u << r;
+    }
+    const int nq = kb - ka + 4;  // level-0 planes ka-2 .. kb+1
+    for (int q = 0; q < nq; q += 3) {
+      tb3_step<0>(U, q, g + q, a, b);
+      if (threadIdx.x == 0 && g + q >= 1) {  // level-0 plane g+q-1 is free: refill its slot
+        dev::fence_proxy_async();
+        cursor_issue(cur, G, units, &map, smem, full, g + q - 1 + B3_NS0);
       }
-      bar_compute3();
-      // ---- level 2 of plane q-2 (global k = ka - 2 + q - 2) from level-1 planes q-3, q-2, q-1
-      if (q >= 4) {
-        const double* Q0 = L1 + ((q - 2) & 3) * (B3_X * B3_Y);
-        const double* Qm = L1 + ((q - 3) & 3) * (B3_X * B3_Y);
-        const double* Qp = L1 + ((q - 1) & 3) * (B3_X * B3_Y);
-        const int64_t gk = ka - 2 + q - 2;  // in [ka, kb): an interior plane
-        if (x >= 2 && x < B3_X - 2 && gi >= 1 && gi <= p.n1 - 2) {
-          char* out = p.dst + gi * p.d_sm1 + gk * p.d_sm3;
-#pragma unroll
-          for (int r = 0; r < B3_ROWS; ++r) {
-            const int y = y0 + r;
-            if (y < 2 || y >= B3_Y - 2) continue;
-            const int64_t gj = gj0 + y;
-            if (gj < 1 || gj > p.n2 - 2) continue;
-            const int o = y * B3_X + x;
-            double v = Q0[o - 1] + Q0[o + 1];
-            v = v + Q0[o - B3_X];
-            v = v + Q0[o + B3_X];
-            v = v + Qm[o];
-            v = v + Qp[o];
-            *reinterpret_cast<double*>(out + gj * p.d_sm2) = c * v;
-          }
+      if (q + 1 < nq) {
+        tb3_step<1>(U, q + 1, g + q + 1, a, b);
+        if (threadIdx.x == 0) {
+          dev::fence_proxy_async();
+          cursor_issue(cur, G, units, &map, smem, full, g + q + B3_NS0);
+        }
+      }
+      if (q + 2 < nq) {
+        tb3_step<2>(U, q + 2, g + q + 2, a, b);
+        if (threadIdx.x == 0) {
+          dev::fence_proxy_async();
+          cursor_issue(cur, G, units, &map, smem, full, g + q + 1 + B3_NS0);
         }
       }
     }
-    // the unit's last two level-0 planes (nq-2, nq-1) were never released by a level 1
-    __syncwarp();
-    if (lane == 0) {
-      dev::mbar_arrive(&empty[(g0 + nq - 2) % B3_NS0]);
-      dev::mbar_arrive(&empty[(g0 + nq - 1) % B3_NS0]);
-    }
-    g = g0 + nq;
-    bar_compute3();  // level-1 ring reuse across units
+    g += nq;
   }
 }
 

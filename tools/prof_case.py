@@ -34,8 +34,10 @@ def main(which):
         U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
-        ftn.jacobi(U, W, 2)
-        ftn.jacobi(U, W, 1)
+        ftn.jacobi(U, W, 4)      # two launches of jacobi3d_tb2 (2 sweeps each)
+        ftn.jacobi_set_fusion(1)
+        ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi3d_tma)
+        ftn.jacobi_set_fusion(4)
         del U, W
     if "muladd" in which:
         n = 1 << 27
