@@ -12,10 +12,15 @@ sys.path.insert(0, ROOT)
 from paper_2409_18824_b200 import ftn  # noqa: E402
 
 
-def main(shapes):
+def main(shapes, pad=0):
     torch.cuda.set_device(0)
     for shape in shapes:
-        U, W = ftn.FArray.empty(shape), ftn.FArray.empty(shape)
+        if pad:   # leading dimension padded by `pad` elements: sections of a larger array
+            BU, BW = ftn.FArray.empty((shape[0] + pad,) + shape[1:]), ftn.FArray.empty((shape[0] + pad,) + shape[1:])
+            sec = [(1, shape[0])] + [(1, e) for e in shape[1:]]
+            U, W = BU.section(*sec), BW.section(*sec)
+        else:
+            U, W = ftn.FArray.empty(shape), ftn.FArray.empty(shape)
         ftn.gen_fill(U, 18824, 0, ftn.GEN_U01)
         ftn.assign(W, U)
         for T in (1, 2):
@@ -35,10 +40,16 @@ def main(shapes):
             print(f"{shape} T={T}: {ms:.3f} ms/sweep  {gl:.1f} GLUPS  ({gl * 16:.0f} GB/s-equiv)")
         ftn.jacobi_set_fusion(4)
         del U, W
+        if pad:
+            del BU, BW
         torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
-    # arguments: n (an n^3 cube) or n1xn2xn3
-    main([tuple(int(v) for v in a.split("x")) if "x" in a else (int(a),) * 3 for a in sys.argv[1:]]
-         or [(n,) * 3 for n in (512, 1024, 2048)])
+    # arguments: [--pad P] n (an n^3 cube) or n1xn2xn3 ...
+    args = sys.argv[1:]
+    pad = 0
+    if args[:1] == ["--pad"]:
+        pad, args = int(args[1]), args[2:]
+    main([tuple(int(v) for v in a.split("x")) if "x" in a else (int(a),) * 3 for a in args]
+         or [(n,) * 3 for n in (512, 1024, 2048)], pad)
