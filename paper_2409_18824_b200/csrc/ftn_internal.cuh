@@ -137,6 +137,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
+// Producer-side wait: the thread is suspended in hardware until the phase completes (or
+// the time hint, in ns, expires) instead of spinning on try_wait, which would take issue
+// slots from the compute warps of its SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait_hint(bar, phase, 1000000u)) {
+  }
+}
 __device__ __forceinline__ void prefetch_tma(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

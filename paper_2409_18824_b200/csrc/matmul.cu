@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // TMA producer: lane 0 of warp 0
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
-    if (kt >= STAGES) dev::mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+    if (kt >= STAGES) dev::mbar_wait_idle(&empty[s], ((kt / STAGES) - 1) & 1);
     uint8_t* st = smem + s * STAGE_BYTES;
     dev::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
     const int k0 = kt * BK;

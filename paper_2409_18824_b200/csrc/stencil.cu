@@ -142,14 +142,14 @@ __global__ void __launch_bounds__(S2_THREADS) jacobi2d_tma(const __grid_constant
       int k = 0;
       for (; it.next(strip, j0, cnt); ++k) {
         const int s = k % S2_STAGES;
-        if (k >= S2_STAGES) dev::mbar_wait(&empty[s], ((k / S2_STAGES) - 1) & 1);
+        if (k >= S2_STAGES) dev::mbar_wait_idle(&empty[s], ((k / S2_STAGES) - 1) & 1);
         dev::mbar_arrive_expect_tx(&full[s], S2_STAGE_BYTES);
         dev::tma_load_2d(smem + s * S2_STAGE_BYTES, &src_map, &full[s], (int32_t)(strip * S2_W - S2_X0),
                          (int32_t)(j0 - 1));
       }
       // producer tail: do not retire while loads are in flight / unconsumed
       for (int kk = k - S2_STAGES > 0 ? k - S2_STAGES : 0; kk < k; ++kk)
-        dev::mbar_wait(&empty[kk % S2_STAGES], (kk / S2_STAGES) & 1);
+        dev::mbar_wait_idle(&empty[kk % S2_STAGES], (kk / S2_STAGES) & 1);
     }
     return;
   }
@@ -253,13 +253,13 @@ __global__ void __launch_bounds__(S3_THREADS) jacobi3d_tma(const __grid_constant
         const int32_t cj = (int32_t)((col / p.tiles_i) * S3_H - 1);
         for (int64_t kk = k0 - 1; kk <= k0 + n; ++kk, ++gp) {
           const int s = (int)(gp % S3_STAGES);
-          if (gp >= S3_STAGES) dev::mbar_wait(&empty[s], (uint32_t)(((gp / S3_STAGES) - 1) & 1));
+          if (gp >= S3_STAGES) dev::mbar_wait_idle(&empty[s], (uint32_t)(((gp / S3_STAGES) - 1) & 1));
           dev::mbar_arrive_expect_tx(&full[s], S3_PLANE_BYTES);
           dev::tma_load_3d(smem + s * S3_PLANE_STRIDE, &src_map, &full[s], ci, cj, (int32_t)kk);
         }
       }
       for (int64_t q = gp - S3_STAGES > 0 ? gp - S3_STAGES : 0; q < gp; ++q)   // producer tail
-        dev::mbar_wait(&empty[q % S3_STAGES], (uint32_t)((q / S3_STAGES) & 1));
+        dev::mbar_wait_idle(&empty[q % S3_STAGES], (uint32_t)((q / S3_STAGES) & 1));
     }
     return;
   }

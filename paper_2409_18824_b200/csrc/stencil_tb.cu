@@ -19,7 +19,7 @@
 //     the warp's outputs.
 //   * Global boundary points keep their value at every level (the caller presets the
 //     boundary of both arrays, R#16); values outside the array are never consumed.  Warps
-//     whose window and unit touch no global boundary take a select-free fast path.
+//     whose window and row chunk touch no global boundary take a select-free fast path.
 // Work units (strip, row segment) are taken round-robin with the strip fastest, as in
 // the single-sweep kernels.
 #include "ftn_internal.cuh"
@@ -34,9 +34,12 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 namespace {
 
 template <int T, int WF_NW = 4 /*compute warps per CTA*/, int WF_R = 8 /*rows per TMA box*/,
-          int WF_NS = 4 /*ring stages*/>
+          int WF_NS = 4 /*ring stages*/, int WF_LAG = 1 /*rows of lag per level*/,
+          int WF_MINB = 1 /*__launch_bounds__ min blocks per SM*/>
 struct WFCfg {
-  static constexpr int NW = WF_NW, R = WF_R, NS = WF_NS;
+  static constexpr int NW = WF_NW, R = WF_R, NS = WF_NS, LAG = WF_LAG, MINB = WF_MINB;
+  // level t produces row s - LAG*t at step s; extra input rows beyond the dependency cone
+  static constexpr int EXTRA = (WF_LAG - 1) * T;
   static constexpr int H = T + (T & 1);
   static constexpr int WO = 64 - 2 * T;           // output columns per warp
   static constexpr int OUT = WF_NW * WO;          // output columns per CTA strip
@@ -47,6 +50,7 @@ struct WFCfg {
   static constexpr bool ALIGNED = ((H - T) % 2) == 0;  // lane column pairs 16-byte aligned in smem
   static_assert(BW <= 256, "TMA box width");
   static_assert(WF_R % 3 == 0, "rows per box: a multiple of 3 (register ring slots are compile-time)");
+  static_assert(WF_LAG == 1 || WF_LAG == 2, "lag 1 (levels in sequence) or 2 (levels independent)");
 };
 
 struct WFParams {
@@ -64,7 +68,7 @@ struct WFParams {
 };
 
 template <int T, class C>
-__global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant__ CUtensorMap src_map,
+__global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_constant__ CUtensorMap src_map,
                                                           const __grid_constant__ WFParams p) {
   constexpr int WF_NW = C::NW, WF_R = C::R, WF_NS = C::NS;
   extern __shared__ uint8_t smem_raw[];
@@ -91,17 +95,17 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
         const int64_t c = u % p.strips;
         const int64_t ja = p.row_lo + (u / p.strips) * p.seg;
         const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
-        const int64_t nch = (jb - ja + 2 * T + WF_R - 1) / WF_R;
+        const int64_t nch = (jb - ja + 2 * T + C::EXTRA + WF_R - 1) / WF_R;
         for (int64_t q = 0; q < nch; ++q, ++k) {
           const int s = (int)(k % WF_NS);
-          if (k >= WF_NS) dev::mbar_wait(&empty[s], (uint32_t)(((k / WF_NS) - 1) & 1));
+          if (k >= WF_NS) dev::mbar_wait_idle(&empty[s], (uint32_t)(((k / WF_NS) - 1) & 1));
           dev::mbar_arrive_expect_tx(&full[s], C::BW * WF_R * 8);
           dev::tma_load_2d(smem + s * C::STAGE, &src_map, &full[s], (int32_t)(c * C::OUT - C::H),
                            (int32_t)(ja - T + q * WF_R));
         }
       }
       for (int64_t q = k - WF_NS > 0 ? k - WF_NS : 0; q < k; ++q)  // producer tail
-        dev::mbar_wait(&empty[q % WF_NS], (uint32_t)((q / WF_NS) & 1));
+        dev::mbar_wait_idle(&empty[q % WF_NS], (uint32_t)((q / WF_NS) & 1));
     }
     return;
   }
@@ -127,9 +131,10 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
       fixed[e] = g <= 0 || g >= p.n1 - 1;
       store[e] = kk >= T && kk < 64 - T && g >= 1 && g <= p.n1 - 2;
     }
-    // warp-uniform fast path: no level-1 point of this window and unit is a boundary point
+    // warp-uniform fast path, decided per chunk: no point of this window that a level
+    // computes in the chunk is a boundary point
     const int64_t wg_lo = gbase + wbase + 1, wg_hi = gbase + wbase + 62;
-    const bool fast = ja - T + 1 > p.fix_lo && jb + T - 2 < p.fix_hi && wg_lo >= 1 && wg_hi <= p.n1 - 2;
+    const bool colfast = wg_lo >= 1 && wg_hi <= p.n1 - 2;
     // relative rows r whose row ja - T + r is updated: r_lo <= r <= r_hi
     const int64_t rl = p.fix_lo + 1 - (ja - T), rh = p.fix_hi - 1 - (ja - T);
     const int r_lo = (int)max(rl, (int64_t)-1), r_hi = (int)min(rh, (int64_t)(1 << 30));
@@ -143,51 +148,65 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
     for (int t = 0; t <= T; ++t)
 #pragma unroll
       for (int q3 = 0; q3 < 3; ++q3) L[t][q3][0] = L[t][q3][1] = 0.0;
-    const int64_t nch = (nr + WF_R - 1) / WF_R;
+    const int64_t nch = (nr + C::EXTRA + WF_R - 1) / WF_R;
     const int nri = (int)nr;
+    // one level: level t row s - LAG*t from level t-1 rows (s - LAG*t) - 1, s - LAG*t, (s - LAG*t) + 1
+    auto level = [&](int t, int rr, int s, bool fastpath) {
+      const int su = ((rr - C::LAG * t - 1) % 3 + 3) % 3, sm = ((rr - C::LAG * t) % 3 + 3) % 3,
+                sd = ((rr - C::LAG * t + 1) % 3 + 3) % 3;
+      const double left0 = __shfl_up_sync(0xffffffffu, L[t - 1][sm][1], 1);
+      const double right1 = __shfl_down_sync(0xffffffffu, L[t - 1][sm][0], 1);
+      double v0 = left0 + L[t - 1][sm][1];
+      v0 = v0 + L[t - 1][su][0];
+      v0 = v0 + L[t - 1][sd][0];
+      v0 = coeff * v0;
+      double v1 = L[t - 1][sm][0] + right1;
+      v1 = v1 + L[t - 1][su][1];
+      v1 = v1 + L[t - 1][sd][1];
+      v1 = coeff * v1;
+      if (!fastpath) {
+        const int r = s - C::LAG * t;
+        const bool rowok = r >= r_lo && r <= r_hi;
+        if (!(rowok && !fixed[0])) v0 = L[t - 1][sm][0];
+        if (!(rowok && !fixed[1])) v1 = L[t - 1][sm][1];
+      }
+      L[t][sm][0] = v0;  // level t row s - LAG*t -> slot (s - LAG*t) mod 3
+      L[t][sm][1] = v1;
+    };
     auto chunk = [&](const double* st, int s0, bool fastpath) {
 #pragma unroll
       for (int rr = 0; rr < WF_R; ++rr) {
         const int s = s0 + rr;
         const double* row = st + rr * C::BW;
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int sl0 = rr % 3;
+        double in0, in1;
         if constexpr (C::ALIGNED) {
           const double2 v = *reinterpret_cast<const double2*>(row);
-          L[0][sl0][0] = v.x;
-          L[0][sl0][1] = v.y;
+          in0 = v.x;
+          in1 = v.y;
         } else {
-          L[0][sl0][0] = row[0];
-          L[0][sl0][1] = row[1];
+          in0 = row[0];
+          in1 = row[1];
         }
+        const int sl0 = rr % 3;
+        if constexpr (C::LAG == 1) {
+          // level t needs level t-1's row produced in this same step: ascending order
+          L[0][sl0][0] = in0;
+          L[0][sl0][1] = in1;
 #pragma unroll
-        for (int t = 1; t <= T; ++t) {
-          // level t row s - t from level t-1 rows s-t-1 (up), s-t (mid), s-t+1 (dn)
-          const int su = ((rr - t - 1) % 3 + 3) % 3, sm = ((rr - t) % 3 + 3) % 3, sd = ((rr - t + 1) % 3 + 3) % 3;
-          const double left0 = __shfl_up_sync(0xffffffffu, L[t - 1][sm][1], 1);
-          const double right1 = __shfl_down_sync(0xffffffffu, L[t - 1][sm][0], 1);
-          double v0 = left0 + L[t - 1][sm][1];
-          v0 = v0 + L[t - 1][su][0];
-          v0 = v0 + L[t - 1][sd][0];
-          v0 = coeff * v0;
-          double v1 = L[t - 1][sm][0] + right1;
-          v1 = v1 + L[t - 1][su][1];
-          v1 = v1 + L[t - 1][sd][1];
-          v1 = coeff * v1;
-          if (!fastpath) {
-            const int r = s - t;
-            const bool rowok = r >= r_lo && r <= r_hi;
-            if (!(rowok && !fixed[0])) v0 = L[t - 1][sm][0];
-            if (!(rowok && !fixed[1])) v1 = L[t - 1][sm][1];
-          }
-          L[t][sm][0] = v0;   // level t row s - t -> slot (s - t) mod 3
-          L[t][sm][1] = v1;
+          for (int t = 1; t <= T; ++t) level(t, rr, s, fastpath);
+        } else {
+          // level t reads level t-1 rows produced in earlier steps only, so the T levels of a
+          // step are independent; descending order lets level t read the ring slot that
+          // level t-1 overwrites later in the same step
+#pragma unroll
+          for (int t = T; t >= 1; --t) level(t, rr, s, fastpath);
+          L[0][sl0][0] = in0;
+          L[0][sl0][1] = in1;
         }
-        // level T row s - T is output row ja + (s - 2T) when 2T <= s < nr
-        const int so = ((rr - T) % 3 + 3) % 3;
-        const bool ok = s >= 2 * T && s < nri;
-        char* o = outp + (int64_t)(s - 2 * T) * p.d_sm2;
+        // level T row s - LAG*T is output row ja + (s - (LAG+1)T) when (LAG+1)T <= s < nr + (LAG-1)T
+        const int so = ((rr - C::LAG * T) % 3 + 3) % 3;
+        const bool ok = s >= (C::LAG + 1) * T && s < nri + C::EXTRA;
+        char* o = outp + (int64_t)(s - (C::LAG + 1) * T) * p.d_sm2;
         if (ok && store[0]) *reinterpret_cast<double*>(o) = L[T][so][0];
         if (ok && store[1]) *reinterpret_cast<double*>(o + p.d_sm1) = L[T][so][1];
       }
@@ -196,7 +215,10 @@ __global__ void __launch_bounds__(C::THREADS) jacobi2d_wf(const __grid_constant_
       dev::mbar_wait(&full[k % WF_NS], (uint32_t)((k / WF_NS) & 1));
       // index the __shared__ array itself so the loads are LDS (not generic LD)
       const double* st = reinterpret_cast<const double*>(smem_raw + smem_off + (k % WF_NS) * C::STAGE) + col0;
-      if (fast) chunk(st, (int)(q * WF_R), true);
+      // rows computed by levels 1..T in this chunk: s - LAG*t for s in [s0, s0+R), t in [1, T]
+      const int s0 = (int)(q * WF_R);
+      const bool fast = colfast && s0 - C::LAG * T >= r_lo && s0 + WF_R - 1 - C::LAG <= r_hi;
+      if (fast) chunk(st, s0, true);
       else chunk(st, (int)(q * WF_R), false);
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&empty[k % WF_NS]);
@@ -255,21 +277,29 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
 #define WF_ARGS src, dst, coeff, row_lo, row_hi, fix_lo, fix_hi, s
   switch (cfg < 0 ? T * 10 + 9 : T * 10 + cfg) {
     // defaults (cfg 9): measured on B200; R must be a multiple of 3
-    case 19: return launch_wf<1, WFCfg<1, 4, 12, 3>>(WF_ARGS);
-    case 29: return launch_wf<2, WFCfg<2, 4, 12, 3>>(WF_ARGS);
-    case 39: return launch_wf<3, WFCfg<3, 4, 12, 3>>(WF_ARGS);
-    case 49: return launch_wf<4, WFCfg<4, 4, 12, 3>>(WF_ARGS);
+    case 19: return launch_wf<1, WFCfg<1, 4, 12, 3, 1>>(WF_ARGS);
+    case 29: return launch_wf<2, WFCfg<2, 4, 12, 3, 1>>(WF_ARGS);
+    case 39: return launch_wf<3, WFCfg<3, 4, 12, 3, 1>>(WF_ARGS);
+    case 49: return launch_wf<4, WFCfg<4, 4, 12, 3, 1>>(WF_ARGS);
     // tuning variants (FTN_WF_CFG)
-    case 30: return launch_wf<3, WFCfg<3, 4, 24, 2>>(WF_ARGS);
-    case 40: return launch_wf<4, WFCfg<4, 4, 24, 2>>(WF_ARGS);
-    case 31: return launch_wf<3, WFCfg<3, 4, 6, 4>>(WF_ARGS);
-    case 41: return launch_wf<4, WFCfg<4, 4, 6, 4>>(WF_ARGS);
-    case 32: return launch_wf<3, WFCfg<3, 4, 12, 4>>(WF_ARGS);
-    case 42: return launch_wf<4, WFCfg<4, 4, 12, 4>>(WF_ARGS);
-    case 33: return launch_wf<3, WFCfg<3, 4, 18, 3>>(WF_ARGS);
-    case 43: return launch_wf<4, WFCfg<4, 4, 18, 3>>(WF_ARGS);
-    case 34: return launch_wf<3, WFCfg<3, 2, 12, 3>>(WF_ARGS);
-    case 44: return launch_wf<4, WFCfg<4, 2, 12, 3>>(WF_ARGS);
+    case 38: return launch_wf<3, WFCfg<3, 4, 12, 3, 2>>(WF_ARGS);   // lag 2: levels independent
+    case 48: return launch_wf<4, WFCfg<4, 4, 12, 3, 2>>(WF_ARGS);
+    case 37: return launch_wf<3, WFCfg<3, 4, 12, 4, 1>>(WF_ARGS);
+    case 47: return launch_wf<4, WFCfg<4, 4, 12, 4, 1>>(WF_ARGS);
+    case 36: return launch_wf<3, WFCfg<3, 3, 12, 3, 1>>(WF_ARGS);
+    case 46: return launch_wf<4, WFCfg<4, 3, 12, 3, 1>>(WF_ARGS);
+    case 35: return launch_wf<3, WFCfg<3, 4, 12, 2, 1, 4>>(WF_ARGS);
+    case 45: return launch_wf<4, WFCfg<4, 4, 12, 2, 1, 4>>(WF_ARGS);
+    case 30: return launch_wf<3, WFCfg<3, 4, 24, 2, 1>>(WF_ARGS);
+    case 40: return launch_wf<4, WFCfg<4, 4, 24, 2, 1>>(WF_ARGS);
+    case 31: return launch_wf<3, WFCfg<3, 4, 6, 4, 1>>(WF_ARGS);
+    case 41: return launch_wf<4, WFCfg<4, 4, 6, 4, 1>>(WF_ARGS);
+    case 32: return launch_wf<3, WFCfg<3, 4, 12, 4, 1>>(WF_ARGS);
+    case 42: return launch_wf<4, WFCfg<4, 4, 12, 4, 1>>(WF_ARGS);
+    case 33: return launch_wf<3, WFCfg<3, 4, 18, 3, 1>>(WF_ARGS);
+    case 43: return launch_wf<4, WFCfg<4, 4, 18, 3, 1>>(WF_ARGS);
+    case 34: return launch_wf<3, WFCfg<3, 2, 12, 3, 1>>(WF_ARGS);
+    case 44: return launch_wf<4, WFCfg<4, 2, 12, 3, 1>>(WF_ARGS);
   }
 #undef WF_ARGS
   return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..4 (and FTN_WF_CFG a known variant)");

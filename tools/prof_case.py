@@ -23,8 +23,8 @@ def main(which):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
-        ftn.jacobi(U, W, 4)      # one fused launch (4 sweeps, jacobi2d_wf<4>), the default
-        ftn.jacobi(U, W, 4)
+        ftn.jacobi(U, W, 8)      # two fused launches (4 sweeps each, jacobi2d_wf<4>), the default
+        ftn.jacobi(U, W, 8)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi2d_tma)
         ftn.jacobi_set_fusion(4)
