@@ -228,11 +228,23 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
 
 /* Tuning (not semantics): rank-2 sweeps are executed up to T at a time by one kernel that
  * keeps the intermediate iterates in registers (temporal blocking, SURVEY §8(f) f2,
- * DESIGN.md §4.3).  Results are bit-identical for every T; the array that does not hold
- * the result holds an earlier iterate.  T in 1..4 (1 = one sweep per launch); default 4
- * or the FTN_JACOBI_FUSE environment variable.  Process-wide. */
+ * DESIGN.md §4.3), rank-3 sweeps up to min(T, 2) at a time (§4.4).  Results are
+ * bit-identical for every T; the array that does not hold the result holds an earlier
+ * iterate.  T in 1..4 (1 = one sweep per launch); default 4 or the FTN_JACOBI_FUSE
+ * environment variable.  Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
+
+/* ftn_jacobi with the data on the host: host_u -> u (host-to-device copy), u -> unew
+ * (device copy, presets the boundary of unew), `sweeps` sweeps, then the result -> host_result
+ * (device-to-host copy), all enqueued on `stream` in that order.  host_u and host_result are
+ * packed column-major real(8) arrays of u's shape (host pointers; pinned memory makes the
+ * call asynchronous and lets calls on different streams overlap their copies and kernels);
+ * u and unew are packed device arrays (desc contiguous).  host_result may alias host_u.
+ * *result_in_unew as for ftn_jacobi.  FTN_ERR_SHAPE for non-packed device arrays. */
+ftn_status_t ftn_jacobi_host(const double* host_u, double* host_result, const ftn_desc_t* u,
+                             const ftn_desc_t* unew, int64_t sweeps, double coeff, int32_t* result_in_unew,
+                             ftn_stream_t stream);
 
 /* The launch plan ftn_jacobi / ftn_jacobi_dist use for `sweeps` sweeps with at most T per
  * launch: floor(S/T) launches of T and one of S mod T, with one launch split k -> (k-1)+1

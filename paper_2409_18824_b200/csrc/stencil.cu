@@ -579,6 +579,28 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
   return FTN_OK;
 }
 
+extern "C" ftn_status_t ftn_jacobi_host(const double* host_u, double* host_result, const ftn_desc_t* u,
+                                        const ftn_desc_t* unew, int64_t sweeps, double coeff, int32_t* result_in_unew,
+                                        ftn_stream_t stream) {
+  FTN_CHECK(jacobi_check(u, unew));
+  if (!desc_contiguous(u) || !desc_contiguous(unew))
+    return fail(FTN_ERR_SHAPE, "ftn_jacobi_host: u and unew must be packed device arrays");
+  if ((!host_u || !host_result) && desc_size(u) > 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi_host: null host buffer");
+  if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi_host: negative sweep count");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)desc_size(u) * 8;
+  int32_t in_new = 0;
+  if (bytes) {
+    FTN_CUDA(cudaMemcpyAsync(u->base_addr, host_u, bytes, cudaMemcpyHostToDevice, s));
+    FTN_CUDA(cudaMemcpyAsync(unew->base_addr, u->base_addr, bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  FTN_CHECK(ftn_jacobi(u, unew, sweeps, coeff, &in_new, stream));
+  if (bytes)
+    FTN_CUDA(cudaMemcpyAsync(host_result, (in_new ? unew : u)->base_addr, bytes, cudaMemcpyDeviceToHost, s));
+  if (result_in_unew) *result_in_unew = in_new;
+  return FTN_OK;
+}
+
 // One local step of the distributed DO nest, no communication: `sweeps`
 // (1 <= sweeps <= halo) sweeps of the owned planes [halo, n_last - halo) of a slab whose
 // halo planes are current; reads src planes [halo - sweeps, n_last - halo + sweeps).

@@ -276,24 +276,25 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
 #define WF_ARGS src, dst, coeff, row_lo, row_hi, fix_lo, fix_hi, s
   switch (cfg < 0 ? T * 10 + 9 : T * 10 + cfg) {
-    // defaults (cfg 9): measured on B200; R must be a multiple of 3
-    case 19: return launch_wf<1, WFCfg<1, 4, 12, 3, 1>>(WF_ARGS);
-    case 29: return launch_wf<2, WFCfg<2, 4, 12, 3, 1>>(WF_ARGS);
-    case 39: return launch_wf<3, WFCfg<3, 4, 12, 3, 1>>(WF_ARGS);
-    case 49: return launch_wf<4, WFCfg<4, 4, 12, 3, 1>>(WF_ARGS);
+    // defaults (cfg 9): measured on B200 (R=6 NS=4 1253 vs R=12 NS=3 1230 GLUPS at T=4),
+    // DESIGN.md §4.3; R must be a multiple of 3
+    case 19: return launch_wf<1, WFCfg<1, 4, 6, 4, 1>>(WF_ARGS);
+    case 29: return launch_wf<2, WFCfg<2, 4, 6, 4, 1>>(WF_ARGS);
+    case 39: return launch_wf<3, WFCfg<3, 4, 6, 4, 1>>(WF_ARGS);
+    case 49: return launch_wf<4, WFCfg<4, 4, 6, 4, 1>>(WF_ARGS);
     // tuning variants (FTN_WF_CFG)
     case 38: return launch_wf<3, WFCfg<3, 4, 12, 3, 2>>(WF_ARGS);   // lag 2: levels independent
     case 48: return launch_wf<4, WFCfg<4, 4, 12, 3, 2>>(WF_ARGS);
-    case 37: return launch_wf<3, WFCfg<3, 4, 12, 4, 1>>(WF_ARGS);
-    case 47: return launch_wf<4, WFCfg<4, 4, 12, 4, 1>>(WF_ARGS);
+    case 37: return launch_wf<3, WFCfg<3, 4, 6, 6, 1>>(WF_ARGS);
+    case 47: return launch_wf<4, WFCfg<4, 4, 6, 6, 1>>(WF_ARGS);
     case 36: return launch_wf<3, WFCfg<3, 3, 12, 3, 1>>(WF_ARGS);
     case 46: return launch_wf<4, WFCfg<4, 3, 12, 3, 1>>(WF_ARGS);
-    case 35: return launch_wf<3, WFCfg<3, 4, 12, 2, 1, 4>>(WF_ARGS);
-    case 45: return launch_wf<4, WFCfg<4, 4, 12, 2, 1, 4>>(WF_ARGS);
+    case 35: return launch_wf<3, WFCfg<3, 4, 3, 8, 1>>(WF_ARGS);
+    case 45: return launch_wf<4, WFCfg<4, 4, 3, 8, 1>>(WF_ARGS);
     case 30: return launch_wf<3, WFCfg<3, 4, 24, 2, 1>>(WF_ARGS);
     case 40: return launch_wf<4, WFCfg<4, 4, 24, 2, 1>>(WF_ARGS);
-    case 31: return launch_wf<3, WFCfg<3, 4, 6, 4, 1>>(WF_ARGS);
-    case 41: return launch_wf<4, WFCfg<4, 4, 6, 4, 1>>(WF_ARGS);
+    case 31: return launch_wf<3, WFCfg<3, 4, 12, 3, 1>>(WF_ARGS);
+    case 41: return launch_wf<4, WFCfg<4, 4, 12, 3, 1>>(WF_ARGS);
     case 32: return launch_wf<3, WFCfg<3, 4, 12, 4, 1>>(WF_ARGS);
     case 42: return launch_wf<4, WFCfg<4, 4, 12, 4, 1>>(WF_ARGS);
     case 33: return launch_wf<3, WFCfg<3, 4, 18, 3, 1>>(WF_ARGS);

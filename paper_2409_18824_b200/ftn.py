@@ -103,6 +103,7 @@ def _load():
         "ftn_bcast": [vp, P, ctypes.c_int32, vp],
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
         "ftn_jacobi_set_fusion": [ctypes.c_int32],
+        "ftn_jacobi_host": [vp, vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -403,6 +404,22 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float | None = None, str
         coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
     r = ctypes.c_int32()
     _call("ftn_jacobi", u.ref(), unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
+    return bool(r.value)
+
+
+def jacobi_host(host_u: torch.Tensor, host_result: torch.Tensor, u: FArray, unew: FArray, sweeps: int,
+                coeff: float | None = None, stream=None) -> bool:
+    """ftn_jacobi_host: host_u -> u, u -> unew, `sweeps` sweeps, result -> host_result, on `stream`.
+    host_u / host_result: CPU float64 tensors in Fortran (column-major) layout of u's shape."""
+    if coeff is None:
+        coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
+    for h in (host_u, host_result):
+        col_major = h.permute(*range(h.dim() - 1, -1, -1)).is_contiguous()
+        if h.device.type != "cpu" or h.dtype != torch.float64 or tuple(h.shape) != tuple(u.shape) or not col_major:
+            raise ValueError("jacobi_host: host buffers must be CPU float64 column-major tensors of u's shape")
+    r = ctypes.c_int32()
+    _call("ftn_jacobi_host", ctypes.c_void_p(host_u.data_ptr()), ctypes.c_void_p(host_result.data_ptr()), u.ref(),
+          unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
     return bool(r.value)
 
 

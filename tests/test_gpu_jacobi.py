@@ -208,3 +208,24 @@ def test_c5_full_size_sampled(ftn):
         ref = (b if new else a)[tuple(c - l for c, l in zip(p, lo))]
         got = res.section(*[(c + 1, c + 1) for c in p]).to_numpy().ravel()[0]
         assert got == ref, p
+
+
+@pytest.mark.parametrize("shape,sweeps", [((130, 77), 9), ((300, 301), 4), ((61, 29, 9), 5), ((3, 3), 1), ((40, 50), 0)])
+def test_jacobi_host_buffers(ftn, shape, sweeps):
+    """ftn_jacobi_host: host in -> device -> sweeps -> host out, same bits as the oracle; the
+    result buffer may alias the input buffer."""
+    u0 = synth.jacobi_init(shape, array_id=7)
+    coeff = C2 if len(shape) == 2 else C3
+    host_u = torch.from_numpy(u0.copy(order="F").T.copy()).permute(*range(len(shape) - 1, -1, -1))
+    host_u = host_u.pin_memory() if torch.cuda.is_available() else host_u
+    host_out = torch.empty(shape[::-1], dtype=torch.float64).pin_memory().permute(*range(len(shape) - 1, -1, -1))
+    U, W = ftn.FArray.empty(shape), ftn.FArray.empty(shape)
+    new = ftn.jacobi_host(host_u, host_out, U, W, sweeps, coeff)
+    torch.cuda.synchronize()
+    uo, wo = u0.copy(order="F"), u0.copy(order="F")
+    new_o = oracle.jacobi(OA(uo), OA(wo), sweeps, coeff)
+    assert new == new_o
+    np.testing.assert_array_equal(host_out.numpy(), wo if new_o else uo)
+    ftn.jacobi_host(host_u, host_u, U, W, sweeps, coeff)       # in place on the host
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host_u.numpy(), wo if new_o else uo)
