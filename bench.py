@@ -398,8 +398,14 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         if t:
             ns = max(2, steps // 2)
             gl = interior * sweeps * ns / t / 1e9
+            # algorithmic bytes: 16 B per interior point per launch (jacobi3d_tb2 does 2 sweeps
+            # per launch, ftn_jacobi_plan with T = min(fusion, 2); the dist path 1 per launch)
+            nl3 = len(ftn.jacobi_plan(sweeps, 1 if distmode else min(2, ftn.jacobi_fusion())))
+            gbs = 16 * interior * nl3 * ns / t / 1e9 / N
             rows["c5_jacobi3d_2048"] = {"value": gl, "unit": "GLUPS", "ms_per_sweep": t / ns / sweeps * 1e3,
-                                        "roofline": {"bound": "hbm", "frac": gl * 16 / N / hbm_peak}}
+                                        "launches_per_step": nl3,
+                                        "roofline": {"bound": "hbm", "achieved_gbs_per_gpu": gbs,
+                                                     "frac": gbs / hbm_peak}}
     return rows
 
 
