@@ -21,6 +21,9 @@
 // value at every level.
 #include "ftn_internal.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 #ifndef FTN_J3_ROWS
 #define FTN_J3_ROWS 4
 #endif
@@ -282,6 +285,16 @@ ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, doubl
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)num_sms() * occ;
   plan_units_halo(p.tiles_i * p.tiles_j, p.n3 - 2, grid, 4, &p.seg, &p.units);
+  // Cap the unit length so that a wave's units span at most ~4 GiB of k-planes (measured at
+  // 2048^3, 32 MiB planes: 128-plane units 503 GLUPS vs 432 with the cost-model choice of
+  // 1023; at 1024^3 the cap is 512 planes and changes nothing).  FTN_J3_MAXSEG overrides.
+  static const int64_t env_maxseg = getenv("FTN_J3_MAXSEG") ? atoll(getenv("FTN_J3_MAXSEG")) : -1;
+  const int64_t plane_bytes = src->dim[2].sm > 0 ? src->dim[2].sm : 1;
+  const int64_t maxseg = env_maxseg >= 0 ? env_maxseg : std::max<int64_t>(32, (int64_t(4) << 30) / plane_bytes);
+  if (maxseg > 0 && p.seg > maxseg) {
+    p.seg = maxseg;
+    p.units = p.tiles_i * p.tiles_j * ((p.n3 - 2 + p.seg - 1) / p.seg);
+  }
   if (grid > p.units) grid = p.units;
   jacobi3d_tb2<<<(unsigned)grid, B3_THREADS, B3_SMEM, s>>>(m, p);
   return after_launch("jacobi3d_tb2");
