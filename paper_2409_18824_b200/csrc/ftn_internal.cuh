@@ -181,6 +181,10 @@ __device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, dou
                : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
                : "l"(p));
 }
+// read-only (non-coherent) 256-bit load that may allocate in L1 (operands re-read by many warps)
+__device__ __forceinline__ void ldg_v4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
 __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }

@@ -23,6 +23,8 @@
 //   for every l exactly once.
 #include "ftn_internal.cuh"
 
+#include <cstdlib>
+
 #include <cstring>
 
 namespace ftn {
@@ -354,21 +356,105 @@ __global__ void __launch_bounds__(MV_ROWS) matvec_kernel(const __grid_constant__
   else p.part[ch * p.m + i] = acc;
 }
 
-__global__ void matvec_combine(const __grid_constant__ MVParams p) {
+// Packed, 32-byte aligned a with m % 4 == 0: thread owns 4 consecutive rows (one 256-bit
+// load per column, a warp covers 128 rows = 1 KB), MV_U columns in flight; every row is
+// folded over the chunk in l order exactly as in matvec_kernel (same bits).
+constexpr int MV4_THREADS = 128, MV4_ROWS = 4 * MV4_THREADS, MV_U = 8;
+
+__global__ void __launch_bounds__(MV4_THREADS) matvec_v4_kernel(const __grid_constant__ MVParams p) {
+  __shared__ double xs[MV_MAXLC];
+  const int64_t rb = blockIdx.x, ch = blockIdx.y;
+  const int64_t l0 = ch * p.lc, l1 = min(l0 + p.lc, p.k);
+  for (int64_t l = l0 + threadIdx.x; l < l1; l += blockDim.x) xs[l - l0] = *reinterpret_cast<const double*>(p.x + l * p.x_sm);
+  __syncthreads();
+  const int64_t i = rb * MV4_ROWS + 4 * threadIdx.x;
+  if (i >= p.m) return;
+  const double* ap = reinterpret_cast<const double*>(p.a) + i;
+  const int64_t ld = p.a_sm1 / 8;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t l = l0;
+  for (; l + MV_U <= l1; l += MV_U) {
+    double v[MV_U][4];
+#pragma unroll
+    for (int u = 0; u < MV_U; ++u) dev::ld_v4(ap + (l + u) * ld, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+    for (int u = 0; u < MV_U; ++u) {
+      const double xv = xs[l + u - l0];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = acc[r] + v[u][r] * xv;
+    }
+  }
+  for (; l < l1; ++l) {
+    double v0, v1, v2, v3;
+    dev::ld_v4(ap + l * ld, v0, v1, v2, v3);
+    const double xv = xs[l - l0];
+    acc[0] = acc[0] + v0 * xv;
+    acc[1] = acc[1] + v1 * xv;
+    acc[2] = acc[2] + v2 * xv;
+    acc[3] = acc[3] + v3 * xv;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (p.nch == 1) *reinterpret_cast<double*>(p.y + (i + r) * p.y_sm) = acc[r];
+    else p.part[ch * p.m + i + r] = acc[r];
+  }
+}
+
+// y(i) = ((part(0,i) + part(1,i)) + part(2,i)) + ...: chunk order; the loads of 8 chunks are
+// issued together (they are independent), the additions stay in order.
+__global__ void __launch_bounds__(64) matvec_combine(const __grid_constant__ MVParams p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.m; i += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int64_t c = 0; c < p.nch; ++c) acc = acc + p.part[c * p.m + i];
+    int64_t c = 0;
+    for (; c + 8 <= p.nch; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = p.part[(c + u) * p.m + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = acc + v[u];
+    }
+    for (; c < p.nch; ++c) acc = acc + p.part[c * p.m + i];
     *reinterpret_cast<double*>(p.y + i * p.y_sm) = acc;
   }
 }
 
-int64_t matvec_chunks(int64_t m, int64_t k) {
-  const int64_t rblocks = (m + MV_ROWS - 1) / MV_ROWS;
-  int64_t nch = (148 * 8 + rblocks - 1) / rblocks;        // >= 8 blocks per SM
-  if (nch < (k + MV_MAXLC - 1) / MV_MAXLC) nch = (k + MV_MAXLC - 1) / MV_MAXLC;
-  int64_t lc = (k + nch - 1) / nch;
-  if (lc < 64) lc = 64;
-  return (k + lc - 1) / lc;
+// Launch plan of the matrix x vector form: the 256-bit path when a is packed, 32-byte aligned
+// and m % 4 == 0; column chunks chosen so that the (row block, chunk) blocks spread evenly
+// over the SMs (the kernel time is that of the busiest SM) with >= 4 blocks per SM, at a cost
+// of 16 B per row and chunk for the partials.
+struct MVPlan {
+  bool v4;
+  int64_t nch, lc, rows_per_block;
+};
+
+MVPlan matvec_plan(const ftn_desc_t* a) {
+  MVPlan pl;
+  const int64_t m = a->dim[0].extent > 0 ? a->dim[0].extent : 1, k = a->dim[1].extent > 0 ? a->dim[1].extent : 1;
+  pl.v4 = a->dim[0].sm == 8 && (m % 4) == 0 && (a->dim[1].sm % 32) == 0 && ((uintptr_t)a->base_addr % 32) == 0;
+  pl.rows_per_block = pl.v4 ? MV4_ROWS : MV_ROWS;
+  const int64_t rblocks = (m + pl.rows_per_block - 1) / pl.rows_per_block;
+  const int64_t nsm = 148;
+  int64_t best_n = (k + MV_MAXLC - 1) / MV_MAXLC;
+  double best = 1e30;
+  for (int64_t n = (k + MV_MAXLC - 1) / MV_MAXLC; n <= k; ++n) {
+    const int64_t lc = (k + n - 1) / n;
+    const int64_t ne = (k + lc - 1) / lc;
+    if (ne != n) continue;
+    if (lc < 32 && n > 1) break;
+    const int64_t units = rblocks * n;
+    const int64_t per_sm = (units + nsm - 1) / nsm;
+    if (per_sm < 4 && lc > 64) continue;   // too few blocks to hide latency: more chunks
+    const double eff = (double)units / (double)(per_sm * nsm);
+    const double cost = (1.0 / eff) * (1.0 + (n > 1 ? 2.0 * (double)n / (double)k : 0.0));
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_n = n;
+    }
+    if (per_sm > 64) break;
+  }
+  pl.lc = (k + best_n - 1) / best_n;
+  pl.nch = (k + pl.lc - 1) / pl.lc;
+  return pl;
 }
 
 ftn_status_t run_matvec(const ftn_desc_t* y, const ftn_desc_t* a, const ftn_desc_t* x, char* ws, cudaStream_t s) {
@@ -387,15 +473,21 @@ ftn_status_t run_matvec(const ftn_desc_t* y, const ftn_desc_t* a, const ftn_desc
     const double zero = 0.0;
     return ftn_fill(y, &zero, s);
   }
-  p.nch = matvec_chunks(p.m, p.k);
-  p.lc = (p.k + p.nch - 1) / p.nch;
-  p.nch = (p.k + p.lc - 1) / p.lc;
+  const MVPlan pl = matvec_plan(a);
+  p.nch = pl.nch;
+  p.lc = pl.lc;
   p.part = reinterpret_cast<double*>(((uintptr_t)ws + 255) & ~uintptr_t(255));
-  dim3 grid((unsigned)((p.m + MV_ROWS - 1) / MV_ROWS), (unsigned)p.nch);
-  matvec_kernel<<<grid, MV_ROWS, 0, s>>>(p);
-  FTN_CHECK(after_launch("matvec_kernel"));
+  if (pl.v4) {
+    dim3 grid((unsigned)((p.m + MV4_ROWS - 1) / MV4_ROWS), (unsigned)p.nch);
+    matvec_v4_kernel<<<grid, MV4_THREADS, 0, s>>>(p);
+    FTN_CHECK(after_launch("matvec_v4_kernel"));
+  } else {
+    dim3 grid((unsigned)((p.m + MV_ROWS - 1) / MV_ROWS), (unsigned)p.nch);
+    matvec_kernel<<<grid, MV_ROWS, 0, s>>>(p);
+    FTN_CHECK(after_launch("matvec_kernel"));
+  }
   if (p.nch > 1) {
-    matvec_combine<<<(unsigned)((p.m + 255) / 256), 256, 0, s>>>(p);
+    matvec_combine<<<(unsigned)((p.m + 63) / 64), 64, 0, s>>>(p);
     FTN_CHECK(after_launch("matvec_combine"));
   }
   return FTN_OK;
@@ -445,6 +537,50 @@ __global__ void __launch_bounds__(256) vecmat_kernel(const __grid_constant__ VMP
   }
 }
 
+// Packed, 32-byte aligned operands: lane loads 4 consecutive elements with one 256-bit
+// access (a warp covers 1 KB of the column per load), 4 loads in flight per lane;
+// accumulator v of a lane takes the elements l = 128 m + 4 lane + v (m = 0, 1, ...), the tail
+// elements beyond the last full 128-element block go to accumulator 0 of lane (l / 4) mod 32 in
+// order; (a0 + a1) + (a2 + a3), then the fixed xor butterfly.
+template <int VU>
+__global__ void __launch_bounds__(256) vecmat_v4_kernel(const __grid_constant__ VMParams p) {
+  const int lane = threadIdx.x & 31;
+  const double* x = reinterpret_cast<const double*>(p.x);
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < p.n;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double* bp = reinterpret_cast<const double*>(p.b + j * p.b_sm1);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t kfull = p.k / 128 * 128;
+    int64_t l = 4 * lane;
+    for (; l + 128 * (VU - 1) < kfull; l += 128 * VU) {
+      double b[VU][4], xv[VU][4];
+#pragma unroll
+      for (int u = 0; u < VU; ++u) dev::ld_v4(bp + l + 128 * u, b[u][0], b[u][1], b[u][2], b[u][3]);
+#pragma unroll
+      for (int u = 0; u < VU; ++u) dev::ldg_v4(x + l + 128 * u, xv[u][0], xv[u][1], xv[u][2], xv[u][3]);
+#pragma unroll
+      for (int u = 0; u < VU; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[v] = acc[v] + xv[u][v] * b[u][v];
+    }
+    for (; l < kfull; l += 128) {
+      double b0, b1, b2, b3, x0, x1, x2, x3;
+      dev::ld_v4(bp + l, b0, b1, b2, b3);
+      dev::ldg_v4(x + l, x0, x1, x2, x3);
+      acc[0] = acc[0] + x0 * b0;
+      acc[1] = acc[1] + x1 * b1;
+      acc[2] = acc[2] + x2 * b2;
+      acc[3] = acc[3] + x3 * b3;
+    }
+    for (int64_t e = kfull + 4 * lane; e < p.k; e += 128)
+      for (int v = 0; v < 4 && e + v < p.k; ++v) acc[0] = acc[0] + x[e + v] * bp[e + v];
+    double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int mask = 16; mask >= 1; mask >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, mask);
+    if (lane == 0) *reinterpret_cast<double*>(p.y + j * p.y_sm) = s;
+  }
+}
+
 ftn_status_t run_vecmat(const ftn_desc_t* y, const ftn_desc_t* x, const ftn_desc_t* b, cudaStream_t s) {
   VMParams p;
   p.x = (const char*)x->base_addr;
@@ -459,6 +595,24 @@ ftn_status_t run_vecmat(const ftn_desc_t* y, const ftn_desc_t* x, const ftn_desc
   if (p.n == 0) return FTN_OK;
   int64_t blocks = (p.n * 32 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  const bool v4 = p.b_sm0 == 8 && p.x_sm == 8 && (p.b_sm1 % 32) == 0 && ((uintptr_t)p.b % 32) == 0 &&
+                  ((uintptr_t)p.x % 32) == 0;
+  static const int vu = getenv("FTN_VM_UNROLL") ? atoi(getenv("FTN_VM_UNROLL")) : 16;  // 8192^2: 16 -> 5650, 8 -> 5190, 4 -> 4510 GB/s
+  if (v4) {
+    if (vu == 8)
+      vecmat_v4_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (vu == 12)
+      vecmat_v4_kernel<12><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (vu == 16)
+      vecmat_v4_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (vu == 32)
+      vecmat_v4_kernel<32><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (vu == 2)
+      vecmat_v4_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else
+      vecmat_v4_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(p);
+    return after_launch("vecmat_v4_kernel");
+  }
   vecmat_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
   return after_launch("vecmat_kernel");
 }
@@ -474,7 +628,7 @@ size_t ws_bytes_for(const ftn_desc_t* a, const ftn_desc_t* b) {
   switch (form_of(a, b)) {
     case 1: {
       const int64_t m = a->dim[0].extent, k = a->dim[1].extent;
-      return (size_t)(matvec_chunks(m > 0 ? m : 1, k > 0 ? k : 1) * (m > 0 ? m : 1) * 8 + 512);
+      return (size_t)(matvec_plan(a).nch * (m > 0 ? m : 1) * 8 + 512);
     }
     case 2: return 0;
   }

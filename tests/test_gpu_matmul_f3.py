@@ -83,6 +83,10 @@ def test_matvec_and_vecmat(ftn, mk):
     yi = ftn.FArray.empty((m,))
     ftn.matmul(yi, ftn.FArray.from_numpy(ia), ftn.FArray.from_numpy(ix))
     np.testing.assert_array_equal(yi.to_numpy(), (ia.astype(np.int64) @ ix.astype(np.int64)).astype(np.float64))
+    ib = synth.farray((k, m), array_id=10, mode=synth.INT8)
+    zi = ftn.FArray.empty((m,))
+    ftn.matmul(zi, ftn.FArray.from_numpy(ix), ftn.FArray.from_numpy(ib))     # vector x matrix, exact
+    np.testing.assert_array_equal(zi.to_numpy(), (ix.astype(np.int64) @ ib.astype(np.int64)).astype(np.float64))
 
 
 def test_matvec_sections(ftn):

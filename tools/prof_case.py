@@ -1,6 +1,6 @@
 """Small, ncu-friendly invocations of each hot kernel (one call each after a warm-up call).
 
-    python tools/prof_case.py [jacobi2d,jacobi3d,muladd,sum,transpose,matmul|all]
+    python tools/prof_case.py [jacobi2d,jacobi3d,muladd,sum,transpose,matmul,matvec|all]
 
 Working sets are larger than L2 but small enough for ncu's replay save/restore.
 """
@@ -68,10 +68,19 @@ def main(which):
         ftn.gen_fill(B, SEED, 2, ftn.GEN_U11)
         ftn.matmul(C, A, B)
         ftn.matmul(C, A, B)
+    if "matvec" in which:
+        n = 8192
+        A = ftn.FArray.empty((n, n))
+        x, y = ftn.FArray.empty((n,)), ftn.FArray.empty((n,))
+        ftn.gen_fill(A, SEED, 1, ftn.GEN_U11)
+        ftn.gen_fill(x, SEED, 2, ftn.GEN_U11)
+        for _ in range(2):
+            ftn.matmul(y, A, x)   # matvec_v4_kernel + matvec_combine
+            ftn.matmul(y, x, A)   # vecmat_v4_kernel
     torch.cuda.synchronize()
     print("ok", ftn.launch_count())
 
 
 if __name__ == "__main__":
     arg = sys.argv[1] if len(sys.argv) > 1 else "all"
-    main(["jacobi2d", "jacobi3d", "muladd", "sum", "transpose", "matmul"] if arg == "all" else arg.split(","))
+    main(["jacobi2d", "jacobi3d", "muladd", "sum", "transpose", "matmul", "matvec"] if arg == "all" else arg.split(","))
