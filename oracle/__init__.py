@@ -98,6 +98,9 @@ def lib():
                                                     ctypes.c_double, ctypes.POINTER(ctypes.c_int64),
                                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]),
             "orc_vecmat_f64": (ctypes.c_int, [P, P, P, P]),
+            "orc_pw_advection_f64": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_void_p, ctypes.c_void_p,
+                                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                                    ctypes.c_double]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -357,3 +360,16 @@ def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol
     _check(lib().orc_jacobi_solve_f64(u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff, ctypes.byref(d),
                                       ctypes.byref(r), ctypes.byref(n)), "jacobi_solve")
     return d.value, r.value, bool(n.value)
+
+
+def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FArray, tzc1, tzc2, tzd1, tzd2,
+                 tcx: float, tcy: float) -> None:
+    """The pw-advection DO nest (R#26): fields indexed (k, j, i),
+    k contiguous; the tz* arrays are float64 vectors of length nz; boundary outputs untouched."""
+    nz = u.shape[0]
+    zs = [np.ascontiguousarray(np.asarray(z, dtype=np.float64)) for z in (tzc1, tzc2, tzd1, tzd2)]
+    for z in zs:
+        if z.shape != (nz,):
+            raise ValueError("pw_advection: coefficient arrays must have length nz")
+    _check(lib().orc_pw_advection_f64(su.ref(), sv.ref(), sw.ref(), u.ref(), v.ref(), w.ref(),
+                                      *[ctypes.c_void_p(z.ctypes.data) for z in zs], tcx, tcy), "pw_advection")

@@ -840,3 +840,75 @@ int orc_jacobi_solve_f64(const orc_array* u, const orc_array* unew, int64_t max_
   *in_unew = (int32_t)(a == unew);
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* pw-advection (R#26): the 3-field advection stencil of the  */
+/* paper's pw-advection benchmark.  Its body is NOT in the paper;    */
+/* this is the public MONC-derived kernel as reproduced in DESIGN.md R#26, written as the */
+/* Fortran DO nest with the fields indexed (k, j, i) = dims (1, 2, 3), k contiguous:      */
+/*   do i = 2, nx-1; do j = 2, ny-1; do k = 2, nz-1                                      */
+/*     su = tcx*(u(k,j,i-1)*(u(k,j,i)+u(k,j,i-1)) - u(k,j,i+1)*(u(k,j,i)+u(k,j,i+1)))    */
+/*     su = su + tcy*(u(k,j-1,i)*(v(k,j-1,i)+v(k,j-1,i+1)) - u(k,j+1,i)*(v(k,j,i)+v(k,j,i+1))) */
+/*     su = su + tzc1(k)*u(k-1,j,i)*(w(k-1,j,i)+w(k-1,j,i+1))                             */
+/*             - tzc2(k)*u(k+1,j,i)*(w(k,j,i)+w(k,j,i+1))                                 */
+/*     sv = tcy*(v(k,j-1,i)*(v(k,j,i)+v(k,j-1,i)) - v(k,j+1,i)*(v(k,j,i)+v(k,j+1,i)))    */
+/*     sv = sv + tcx*(v(k,j,i-1)*(u(k,j,i-1)+u(k,j+1,i-1)) - v(k,j,i+1)*(u(k,j,i)+u(k,j+1,i))) */
+/*     sv = sv + tzc1(k)*v(k-1,j,i)*(w(k-1,j,i)+w(k-1,j+1,i))                             */
+/*             - tzc2(k)*v(k+1,j,i)*(w(k,j,i)+w(k,j+1,i))                                 */
+/*     sw = tzd1(k)*w(k-1,j,i)*(w(k,j,i)+w(k-1,j,i)) - tzd2(k)*w(k+1,j,i)*(w(k,j,i)+w(k+1,j,i)) */
+/*     sw = sw + tcx*(w(k,j,i-1)*(u(k,j,i-1)+u(k+1,j,i-1)) - w(k,j,i+1)*(u(k,j,i)+u(k+1,j,i))) */
+/*     sw = sw + tcy*(w(k,j-1,i)*(v(k,j-1,i)+v(k+1,j-1,i)) - w(k,j+1,i)*(v(k,j,i)+v(k+1,j,i))) */
+/* Fortran evaluation: a*b*c = (a*b)*c, x + a - b = (x + a) - b; one rounding per operation. */
+/* Boundary points of su, sv, sw are not written.                                          */
+/* ------------------------------------------------------------------------ */
+int orc_pw_advection_f64(const orc_array* su, const orc_array* sv, const orc_array* sw, const orc_array* u,
+                         const orc_array* v, const orc_array* w, const double* tzc1, const double* tzc2,
+                         const double* tzd1, const double* tzd2, double tcx, double tcy) {
+  const orc_array* all[6] = {su, sv, sw, u, v, w};
+  for (int q = 0; q < 6; ++q) {
+    if (all[q]->rank != 3) return ORC_ERANK;
+    if (all[q]->type != ORC_F64) return ORC_ETYPE;
+    for (int d = 0; d < 3; ++d) if (all[q]->dim[d].ext != u->dim[d].ext) return ORC_ESHAPE;
+  }
+  const int64_t nz = u->dim[0].ext, ny = u->dim[1].ext, nx = u->dim[2].ext;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 1; i < nx - 1; ++i)
+    for (int64_t j = 1; j < ny - 1; ++j)
+      for (int64_t k = 1; k < nz - 1; ++k) {
+        double a, b, s;
+        /* su */
+        a = ld3(u, k, j, i - 1) * (ld3(u, k, j, i) + ld3(u, k, j, i - 1));
+        b = ld3(u, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k, j, i + 1));
+        s = tcx * (a - b);
+        a = ld3(u, k, j - 1, i) * (ld3(v, k, j - 1, i) + ld3(v, k, j - 1, i + 1));
+        b = ld3(u, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k, j, i + 1));
+        s = s + tcy * (a - b);
+        a = (tzc1[k] * ld3(u, k - 1, j, i)) * (ld3(w, k - 1, j, i) + ld3(w, k - 1, j, i + 1));
+        b = (tzc2[k] * ld3(u, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k, j, i + 1));
+        s = (s + a) - b;
+        st3(su, k, j, i, s);
+        /* sv */
+        a = ld3(v, k, j - 1, i) * (ld3(v, k, j, i) + ld3(v, k, j - 1, i));
+        b = ld3(v, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k, j + 1, i));
+        s = tcy * (a - b);
+        a = ld3(v, k, j, i - 1) * (ld3(u, k, j, i - 1) + ld3(u, k, j + 1, i - 1));
+        b = ld3(v, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k, j + 1, i));
+        s = s + tcx * (a - b);
+        a = (tzc1[k] * ld3(v, k - 1, j, i)) * (ld3(w, k - 1, j, i) + ld3(w, k - 1, j + 1, i));
+        b = (tzc2[k] * ld3(v, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k, j + 1, i));
+        s = (s + a) - b;
+        st3(sv, k, j, i, s);
+        /* sw */
+        a = (tzd1[k] * ld3(w, k - 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k - 1, j, i));
+        b = (tzd2[k] * ld3(w, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k + 1, j, i));
+        s = a - b;
+        a = ld3(w, k, j, i - 1) * (ld3(u, k, j, i - 1) + ld3(u, k + 1, j, i - 1));
+        b = ld3(w, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k + 1, j, i));
+        s = s + tcx * (a - b);
+        a = ld3(w, k, j - 1, i) * (ld3(v, k, j - 1, i) + ld3(v, k + 1, j - 1, i));
+        b = ld3(w, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k + 1, j, i));
+        s = s + tcy * (a - b);
+        st3(sw, k, j, i, s);
+      }
+  return ORC_OK;
+}
