@@ -269,6 +269,23 @@ ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64
 ftn_status_t ftn_maxval_absdiff(const ftn_desc_t* x, const ftn_desc_t* y, void* result_dev, void* ws,
                                 size_t ws_bytes, ftn_stream_t stream);
 
+/* ---------------------------------------------------------------- f4
+ * pw-advection (the paper's pw-advection benchmark, P:92-93, P:345-366 —
+ * its body is not in the paper; R#26 gives the DO nest this implements):
+ *   do i = 2, nx-1; do j = 2, ny-1; do k = 2, nz-1
+ *     su(k,j,i) = tcx*(u(k,j,i-1)*(u(k,j,i)+u(k,j,i-1)) - u(k,j,i+1)*(u(k,j,i)+u(k,j,i+1)))
+ *               + tcy*(...) + tzc1(k)*u(k-1,j,i)*(...) - tzc2(k)*u(k+1,j,i)*(...)   (and sv, sw)
+ * u, v, w, su, sv, sw: real(8) rank-3 conformable arrays indexed (k, j, i) (dim 1 = k);
+ * tzc1, tzc2, tzd1, tzd2: real(8) rank-1 of extent size(u, 1); tcx, tcy: scalars.  Only
+ * interior points of su, sv, sw are written (boundaries are the caller's).  Outputs must
+ * not overlap inputs or each other (FTN_ERR_SHAPE).  Bit-exact vs the oracle (one rounding
+ * per operation, Fortran evaluation order).  Any strides; the fast path needs TMA-able
+ * inputs (unit stride in dim 1, 16-byte aligned base and dim-2/3 strides). */
+ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t* sv, const ftn_desc_t* sw,
+                              const ftn_desc_t* u, const ftn_desc_t* v, const ftn_desc_t* w,
+                              const ftn_desc_t* tzc1, const ftn_desc_t* tzc2, const ftn_desc_t* tzd1,
+                              const ftn_desc_t* tzd2, double tcx, double tcy, ftn_stream_t stream);
+
 /* ---------------------------------------------------------------- a8
  * Multi-GPU (one process per GPU, NCCL over NVLink).  The id travels between
  * processes through the caller's own channel (torch.distributed store). */

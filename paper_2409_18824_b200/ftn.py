@@ -104,6 +104,7 @@ def _load():
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
         "ftn_jacobi_set_fusion": [ctypes.c_int32],
         "ftn_jacobi_host": [vp, vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
+        "ftn_pw_advection": [P, P, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_double, vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -421,6 +422,13 @@ def jacobi_host(host_u: torch.Tensor, host_result: torch.Tensor, u: FArray, unew
     _call("ftn_jacobi_host", ctypes.c_void_p(host_u.data_ptr()), ctypes.c_void_p(host_result.data_ptr()), u.ref(),
           unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
     return bool(r.value)
+
+
+def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FArray, tzc1: FArray, tzc2: FArray,
+                 tzd1: FArray, tzd2: FArray, tcx: float, tcy: float, stream=None) -> None:
+    """pw-advection (R#26): su, sv, sw at the interior points."""
+    _call("ftn_pw_advection", su.ref(), sv.ref(), sw.ref(), u.ref(), v.ref(), w.ref(), tzc1.ref(), tzc2.ref(),
+          tzd1.ref(), tzd2.ref(), tcx, tcy, _stream(stream))
 
 
 def jacobi_set_fusion(sweeps_per_launch: int):
