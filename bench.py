@@ -406,6 +406,31 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                                         "launches_per_step": nl3,
                                         "roofline": {"bound": "hbm", "achieved_gbs_per_gpu": gbs,
                                                      "frac": gbs / hbm_peak}}
+
+    # f4: pw-advection, three fields (k, j, i) = 2048 x 1024 x 1024 (R#26/R#27); at N > 1
+    # every rank owns 1024/N i-planes plus one halo plane per side (inputs do not change
+    # between calls, so there is no exchange in the timed loop: weak slabs, no collective)
+    if "f4" in args.rows:
+        nz, ny, nx = 2048, 1024, 1024
+        nxl = nx if N == 1 else nx // N + 2
+        need = 6 * nz * ny * nxl * 8
+        if torch.cuda.mem_get_info()[0] > need + (2 << 30):
+            F = [ftn.FArray.empty((nz, ny, nxl)) for _ in range(3)]
+            for q, f in enumerate(F):
+                ftn.gen_fill(f, SEED, 50 + q + 3 * rank, ftn.GEN_U11)
+            O = [ftn.FArray.empty((nz, ny, nxl)) for _ in range(3)]
+            Z = [ftn.FArray.empty((nz,)) for _ in range(4)]
+            for q, z in enumerate(Z):
+                ftn.gen_fill(z, SEED, 60 + q, ftn.GEN_U11)
+            t = timed(torch, lambda: ftn.pw_advection(*O, *F, *Z, 0.1, 0.2), steps, warm, None, dist)
+            cells = (nz - 2) * (ny - 2) * (nxl - 2) * N
+            gcs = cells * steps / t / 1e9
+            gbs = 48 * cells * steps / t / 1e9
+            rows["f4_pw_advection_2048x1024x1024"] = {
+                "value": gcs, "unit": "Gcells/s", "ms": t / steps * 1e3, "achieved_gbs": gbs,
+                "roofline": {"bound": "hbm", "bytes_per_cell": 48, "frac": gbs / N / hbm_peak}}
+            del F, O, Z
+            torch.cuda.empty_cache()
     return rows
 
 
@@ -486,7 +511,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
-    ap.add_argument("--rows", default="c4,c3,paper,c5", help="comma list of extra rows, or 'none'")
+    ap.add_argument("--rows", default="c4,c3,paper,c5,f4", help="comma list of extra rows, or 'none'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")

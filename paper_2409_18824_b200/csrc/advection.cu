@@ -7,10 +7,11 @@
 // HBM-bound: 24 B read + 24 B written per interior point (48 B/cell).
 //
 // TMA path (u, v, w TMA-able): a CTA owns a 64 (k) x 16 (j) tile of output columns and marches
-// along i.  Each i-plane of the three fields arrives as TMA boxes {66 x 18 x 1} (k-1 .. k+64,
-// j-1 .. j+16; the k start 64t is 16-byte aligned) into a 4-slot mbarrier ring; when plane
+// along i.  Each i-plane of the three fields arrives as TMA boxes {68 x 18 x 1} (k-2 .. k+65,
+// j-1 .. j+16; the k start 64t-2 is 16-byte aligned) into a 4-slot mbarrier ring; when plane
 // i+1 has landed the 512 threads compute output plane i from the slots of planes i-1, i, i+1
-// (thread = one k, two j rows), then one block barrier, after which thread 0 refills the slot
+// (thread = a pair k, k+1 of one j row: its neighbours come as 16-byte pairs, LDS.128, and its
+// results leave as 16-byte stores), then one block barrier, after which thread 0 refills the slot
 // of plane i-1 (no producer warp, no empty barriers).  Work units = (tile, i-segment), tile
 // fastest, round-robin (plan_units_halo).
 // Generic path (any strides): one thread per output point, direct loads.
@@ -30,8 +31,8 @@ bool stencil_tma_able(const ftn_desc_t* d);
 namespace {
 
 constexpr int AD_OK = 64, AD_OJ = 16;               // output tile (k, j)
-constexpr int AD_BK = AD_OK + 2, AD_BJ = AD_OJ + 2;  // box 66 x 18
-constexpr int AD_FIELD = (AD_BK * AD_BJ * 8 + 127) / 128 * 128;  // 9600 B per field box
+constexpr int AD_BK = AD_OK + 4, AD_BJ = AD_OJ + 2;  // box 68 x 18: k-2 .. k+65, j-1 .. j+16
+constexpr int AD_FIELD = (AD_BK * AD_BJ * 8 + 127) / 128 * 128;  // 9856 B per field box
 constexpr int AD_SLOT = 3 * AD_FIELD;
 constexpr int AD_NS = 4;
 constexpr int AD_THREADS = 512;
@@ -50,6 +51,7 @@ struct AdvParams {
   int32_t tiles_k, tiles_j;
   int32_t seg;          // output i-planes per unit
   uint32_t units;
+  int32_t vec_out;      // outputs: unit stride in k, 16-byte aligned base and strides
   double tcx, tcy;
 };
 
@@ -99,7 +101,7 @@ __device__ __forceinline__ double tz_at(const AdvParams& p, int q, int k) {
 __device__ __forceinline__ void adv_unit(const AdvParams& p, uint32_t u, int& k0, int& j0, int& ia, int& ib) {
   const uint32_t ntile = (uint32_t)(p.tiles_k * p.tiles_j);
   const uint32_t t = u % ntile, sgi = u / ntile;
-  k0 = 1 + (int)(t % (uint32_t)p.tiles_k) * AD_OK;
+  k0 = (int)(t % (uint32_t)p.tiles_k) * AD_OK;  // outputs k0 .. k0+63 (k = 0 is boundary)
   j0 = 1 + (int)(t / (uint32_t)p.tiles_k) * AD_OJ;
   ia = 1 + (int)sgi * p.seg;
   ib = min(ia + p.seg, p.nx - 1);
@@ -113,7 +115,7 @@ struct AdvCursor {
 __device__ __forceinline__ void adv_cursor_unit(AdvCursor& c, const AdvParams& p) {
   int k0, j0, ia, ib;
   adv_unit(p, c.u, k0, j0, ia, ib);
-  c.ck = k0 - 1;  // = 64 t: 16-byte aligned box start
+  c.ck = k0 - 2;  // = 64 t - 2: 16-byte aligned box start
   c.cj = j0 - 1;
   c.ci = ia - 1;
   c.cend = ib + 1;
@@ -134,12 +136,17 @@ __device__ __forceinline__ void adv_issue(AdvCursor& c, const AdvParams& p, cons
   }
 }
 
-// Reads field f at box offset (dk, dj) of plane slot di (-1, 0, +1) for the thread's point.
-struct SmemNbr {
-  const double* pl[3];  // plane i-1, i, i+1 (field 0 base; fields at +AD_FIELD/8 elements)
-  int o;                // element offset of the point in a field box
+// Reads field f at (k + E + dk, j + dj, i + di) for the thread's pair (k, k+1), E = 0 or 1: the
+// row segment is read as 16-byte pairs L = (k-2, k-1), C = (k, k+1), R = (k+2, k+3) (LDS.128;
+// identical loads are shared between the calls).
+template <int E>
+struct SmemPair {
+  const double* pl[3];  // plane i-1, i, i+1 (field 0 base)
+  int row0;             // element offset of the thread's row (j) and pair L in a field box
   __device__ __forceinline__ double operator()(int f, int dk, int dj, int di) const {
-    return pl[di + 1][f * (AD_FIELD / 8) + o + dj * AD_BK + dk];
+    const double2* seg = reinterpret_cast<const double2*>(pl[di + 1] + f * (AD_FIELD / 8) + row0 + dj * AD_BK);
+    const int m = E + dk;
+    return m == -1 ? seg[0].y : m == 0 ? seg[1].x : m == 1 ? seg[1].y : seg[2].x;
   }
 };
 
@@ -164,43 +171,53 @@ __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_con
   }
   __syncthreads();
   const double* base = reinterpret_cast<const double*>(smem_raw + soff);
-  const int kk = threadIdx.x % AD_OK, jr = threadIdx.x / AD_OK;  // k offset, first of two j rows
+  const int lane = threadIdx.x & 31, jr = threadIdx.x >> 5;  // pair (2 lane, 2 lane + 1), row jr
   uint32_t g = 0;  // planes consumed so far
   for (uint32_t u = blockIdx.x; u < p.units; u += gridDim.x) {
     int k0, j0, ia, ib;
     adv_unit(p, u, k0, j0, ia, ib);
-    const int k = k0 + kk;
-    const bool kin = k <= p.nz - 2;
-    const int kc = kin ? k : 1;
-    const double tzc1 = tz_at(p, 0, kc), tzc2 = tz_at(p, 1, kc), tzd1 = tz_at(p, 2, kc), tzd2 = tz_at(p, 3, kc);
-    const int ja = j0 + jr, jb = j0 + jr + AD_OJ / 2;
-    const bool st_a = kin && ja <= p.ny - 2, st_b = kin && jb <= p.ny - 2;
+    const int k = k0 + 2 * lane;
+    const bool in0 = k >= 1 && k <= p.nz - 2, in1 = k + 1 >= 1 && k + 1 <= p.nz - 2;
+    const int kc0 = in0 ? k : 1, kc1 = in1 ? k + 1 : 1;
+    const double c1a = tz_at(p, 0, kc0), c2a = tz_at(p, 1, kc0), d1a = tz_at(p, 2, kc0), d2a = tz_at(p, 3, kc0);
+    const double c1b = tz_at(p, 0, kc1), c2b = tz_at(p, 1, kc1), d1b = tz_at(p, 2, kc1), d2b = tz_at(p, 3, kc1);
+    const int j = j0 + jr;
+    const bool jin = j <= p.ny - 2;
+    const bool st0 = jin && in0, st1 = jin && in1;
     const int np = ib - ia + 2;  // planes ia-1 .. ib
     for (int q = 0; q < np; ++q) {
       const uint32_t gq = g + q;
       dev::mbar_wait(&full[gq % AD_NS], (gq / AD_NS) & 1);
-      if (q >= 2) {  // output plane i = ia - 1 + q - 1 from planes q-2, q-1, q
+      if (q >= 2) {  // output plane i from planes i-1, i, i+1 (steps q-2, q-1, q)
         const int i = ia + q - 2;
-        SmemNbr F;
-        F.pl[0] = base + ((gq - 2) % AD_NS) * (AD_SLOT / 8);
-        F.pl[1] = base + ((gq - 1) % AD_NS) * (AD_SLOT / 8);
-        F.pl[2] = base + (gq % AD_NS) * (AD_SLOT / 8);
-        double su, sv, sw;
-        F.o = (jr + 1) * AD_BK + kk + 1;
-        adv_point(F, tzc1, tzc2, tzd1, tzd2, p.tcx, p.tcy, su, sv, sw);
-        if (st_a) {
-          const int64_t oi = (int64_t)i, oj = (int64_t)ja;
-          *reinterpret_cast<double*>(p.su.base + k * p.su.sm1 + oj * p.su.sm2 + oi * p.su.sm3) = su;
-          *reinterpret_cast<double*>(p.sv.base + k * p.sv.sm1 + oj * p.sv.sm2 + oi * p.sv.sm3) = sv;
-          *reinterpret_cast<double*>(p.sw.base + k * p.sw.sm1 + oj * p.sw.sm2 + oi * p.sw.sm3) = sw;
-        }
-        F.o = (jr + 1 + AD_OJ / 2) * AD_BK + kk + 1;
-        adv_point(F, tzc1, tzc2, tzd1, tzd2, p.tcx, p.tcy, su, sv, sw);
-        if (st_b) {
-          const int64_t oi = (int64_t)i, oj = (int64_t)jb;
-          *reinterpret_cast<double*>(p.su.base + k * p.su.sm1 + oj * p.su.sm2 + oi * p.su.sm3) = su;
-          *reinterpret_cast<double*>(p.sv.base + k * p.sv.sm1 + oj * p.sv.sm2 + oi * p.sv.sm3) = sv;
-          *reinterpret_cast<double*>(p.sw.base + k * p.sw.sm1 + oj * p.sw.sm2 + oi * p.sw.sm3) = sw;
+        SmemPair<0> F0;
+        SmemPair<1> F1;
+        F0.pl[0] = F1.pl[0] = base + ((gq - 2) % AD_NS) * (AD_SLOT / 8);
+        F0.pl[1] = F1.pl[1] = base + ((gq - 1) % AD_NS) * (AD_SLOT / 8);
+        F0.pl[2] = F1.pl[2] = base + (gq % AD_NS) * (AD_SLOT / 8);
+        F0.row0 = F1.row0 = (jr + 1) * AD_BK + 2 * lane;
+        double su0, sv0, sw0, su1, sv1, sw1;
+        adv_point(F0, c1a, c2a, d1a, d2a, p.tcx, p.tcy, su0, sv0, sw0);
+        adv_point(F1, c1b, c2b, d1b, d2b, p.tcx, p.tcy, su1, sv1, sw1);
+        const int64_t ok = (int64_t)k, oj = (int64_t)j, oi = (int64_t)i;
+        char* a0 = p.su.base + ok * p.su.sm1 + oj * p.su.sm2 + oi * p.su.sm3;
+        char* a1 = p.sv.base + ok * p.sv.sm1 + oj * p.sv.sm2 + oi * p.sv.sm3;
+        char* a2 = p.sw.base + ok * p.sw.sm1 + oj * p.sw.sm2 + oi * p.sw.sm3;
+        if (p.vec_out && st0 && st1) {
+          *reinterpret_cast<double2*>(a0) = make_double2(su0, su1);
+          *reinterpret_cast<double2*>(a1) = make_double2(sv0, sv1);
+          *reinterpret_cast<double2*>(a2) = make_double2(sw0, sw1);
+        } else {
+          if (st0) {
+            *reinterpret_cast<double*>(a0) = su0;
+            *reinterpret_cast<double*>(a1) = sv0;
+            *reinterpret_cast<double*>(a2) = sw0;
+          }
+          if (st1) {
+            *reinterpret_cast<double*>(a0 + p.su.sm1) = su1;
+            *reinterpret_cast<double*>(a1 + p.sv.sm1) = sv1;
+            *reinterpret_cast<double*>(a2 + p.sw.sm1) = sw1;
+          }
         }
       }
       __syncthreads();
@@ -330,7 +347,11 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
     FTN_CHECK(make_map(&mu, u));
     FTN_CHECK(make_map(&mv, v));
     FTN_CHECK(make_map(&mw, w));
-    p.tiles_k = (int32_t)((nz - 2 + AD_OK - 1) / AD_OK);
+    p.tiles_k = (int32_t)((nz - 1 + AD_OK - 1) / AD_OK);  // outputs k in [1, nz-2] within [0, 64 tiles_k)
+    p.vec_out = 1;
+    for (const ftn_desc_t* o : {su, sv, sw})
+      if (o->dim[0].sm != 8 || ((uintptr_t)o->base_addr % 16) || (o->dim[1].sm % 16) || (o->dim[2].sm % 16))
+        p.vec_out = 0;
     p.tiles_j = (int32_t)((ny - 2 + AD_OJ - 1) / AD_OJ);
     const int64_t grid0 = num_sms();
     int64_t seg = 0, units = 0;

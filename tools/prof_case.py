@@ -1,6 +1,6 @@
 """Small, ncu-friendly invocations of each hot kernel (one call each after a warm-up call).
 
-    python tools/prof_case.py [jacobi2d,jacobi3d,muladd,sum,transpose,matmul,matvec|all]
+    python tools/prof_case.py [jacobi2d,jacobi3d,muladd,sum,transpose,matmul,matvec,advection|all]
 
 Working sets are larger than L2 but small enough for ncu's replay save/restore.
 """
@@ -77,10 +77,19 @@ def main(which):
         for _ in range(2):
             ftn.matmul(y, A, x)   # matvec_v4_kernel + matvec_combine
             ftn.matmul(y, x, A)   # vecmat_v4_kernel
+    if "advection" in which:
+        nz, ny, nx = 1024, 512, 256
+        F = [ftn.FArray.empty((nz, ny, nx)) for _ in range(6)]
+        Z = [ftn.FArray.empty((nz,)) for _ in range(4)]
+        for q, f in enumerate(F[:3] + Z):
+            ftn.gen_fill(f, SEED, q, ftn.GEN_U11)
+        ftn.pw_advection(*F[3:], *F[:3], *Z, 0.1, 0.2)
+        ftn.pw_advection(*F[3:], *F[:3], *Z, 0.1, 0.2)
+        del F, Z
     torch.cuda.synchronize()
     print("ok", ftn.launch_count())
 
 
 if __name__ == "__main__":
     arg = sys.argv[1] if len(sys.argv) > 1 else "all"
-    main(["jacobi2d", "jacobi3d", "muladd", "sum", "transpose", "matmul", "matvec"] if arg == "all" else arg.split(","))
+    main(["jacobi2d", "jacobi3d", "muladd", "sum", "transpose", "matmul", "matvec", "advection"] if arg == "all" else arg.split(","))
