@@ -8,7 +8,7 @@
 //
 // TMA path (u, v, w TMA-able): a CTA owns a 64 (k) x 16 (j) tile of output columns and marches
 // along i.  Each i-plane of the three fields arrives as TMA boxes {68 x 18 x 1} (k-2 .. k+65,
-// j-1 .. j+16; the k start 64t-2 is 16-byte aligned) into a 4-slot mbarrier ring; when plane
+// j-1 .. j+16; the k start 64t-2 is 16-byte aligned) into a 5-slot mbarrier ring; when plane
 // i+1 has landed the 512 threads compute output plane i from the slots of planes i-1, i, i+1
 // (thread = a pair k, k+1 of one j row: its neighbours come as 16-byte pairs, LDS.128, and its
 // results leave as 16-byte stores), then one block barrier, after which thread 0 refills the slot
@@ -34,9 +34,9 @@ constexpr int AD_OK = 64, AD_OJ = 16;               // output tile (k, j)
 constexpr int AD_BK = AD_OK + 4, AD_BJ = AD_OJ + 2;  // box 68 x 18: k-2 .. k+65, j-1 .. j+16
 constexpr int AD_FIELD = (AD_BK * AD_BJ * 8 + 127) / 128 * 128;  // 9856 B per field box
 constexpr int AD_SLOT = 3 * AD_FIELD;
-constexpr int AD_NS = 4;
 constexpr int AD_THREADS = 512;
-constexpr int AD_SMEM = AD_NS * AD_SLOT + 128 + 8 * AD_NS;
+template <int NS>
+constexpr int ad_smem() { return NS * AD_SLOT + 128 + 8 * NS; }
 
 struct AdvOut {
   char* base;
@@ -121,6 +121,7 @@ __device__ __forceinline__ void adv_cursor_unit(AdvCursor& c, const AdvParams& p
   c.cend = ib + 1;
 }
 
+template <int AD_NS>
 __device__ __forceinline__ void adv_issue(AdvCursor& c, const AdvParams& p, const CUtensorMap* mu, const CUtensorMap* mv,
                                           const CUtensorMap* mw, uint8_t* smem, uint64_t* full, uint32_t g) {
   if (c.u >= p.units) return;
@@ -150,6 +151,8 @@ struct SmemPair {
   }
 };
 
+// AD_NS ring slots: NS-2 planes in flight ahead of the step
+template <int AD_NS>
 __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_constant__ CUtensorMap mu,
                                                                 const __grid_constant__ CUtensorMap mv,
                                                                 const __grid_constant__ CUtensorMap mw,
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_con
     dev::prefetch_tma(&mv);
     dev::prefetch_tma(&mw);
     if (cur.u < p.units) adv_cursor_unit(cur, p);
-    for (uint32_t g = 0; g < AD_NS; ++g) adv_issue(cur, p, &mu, &mv, &mw, smem, full, g);
+    for (uint32_t g = 0; g < AD_NS; ++g) adv_issue<AD_NS>(cur, p, &mu, &mv, &mw, smem, full, g);
   }
   __syncthreads();
   const double* base = reinterpret_cast<const double*>(smem_raw + soff);
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_con
       // unit, nothing before its third plane): refill its slot with plane gq-2+NS
       if (threadIdx.x == 0 && gq >= 2) {
         dev::fence_proxy_async();
-        adv_issue(cur, p, &mu, &mv, &mw, smem, full, gq - 2 + AD_NS);
+        adv_issue<AD_NS>(cur, p, &mu, &mv, &mw, smem, full, gq - 2 + AD_NS);
       }
     }
     g += np;
@@ -267,6 +270,20 @@ __global__ void __launch_bounds__(256) adv_generic_kernel(const __grid_constant_
     *reinterpret_cast<double*>(p.sv.base + F.k * p.sv.sm1 + F.j * p.sv.sm2 + F.i * p.sv.sm3) = sv;
     *reinterpret_cast<double*>(p.sw.base + F.k * p.sw.sm1 + F.j * p.sw.sm2 + F.i * p.sw.sm3) = sw;
   }
+}
+
+template <int NS>
+ftn_status_t launch_adv(unsigned grid, const CUtensorMap& mu, const CUtensorMap& mv, const CUtensorMap& mw,
+                        const AdvParams& p, cudaStream_t s) {
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    FTN_CUDA(cudaFuncSetAttribute(adv_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, ad_smem<NS>()));
+    attr[dev & 63] = true;
+  }
+  adv_tma_kernel<NS><<<grid, AD_THREADS, ad_smem<NS>(), s>>>(mu, mv, mw, p);
+  return FTN_OK;
 }
 
 AdvOut out_of(const ftn_desc_t* d) {
@@ -336,13 +353,6 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
   p.tcy = tcy;
   const bool tma = stencil_tma_able(u) && stencil_tma_able(v) && stencil_tma_able(w);
   if (tma) {
-    static bool attr[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr[dev & 63]) {
-      FTN_CUDA(cudaFuncSetAttribute(adv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AD_SMEM));
-      attr[dev & 63] = true;
-    }
     CUtensorMap mu, mv, mw;
     FTN_CHECK(make_map(&mu, u));
     FTN_CHECK(make_map(&mv, v));
@@ -358,7 +368,8 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
     plan_units_halo((int64_t)p.tiles_k * p.tiles_j, nx - 2, grid0, 2, &seg, &units);
     // units spanning at most ~4 GiB of i-planes (three fields), as for jacobi3d_tb2
     const int64_t plane_bytes = 3 * std::max<int64_t>(u->dim[2].sm, 1);
-    const int64_t maxseg = std::max<int64_t>(16, (int64_t(4) << 30) / plane_bytes);
+    static const int64_t env_maxseg = getenv("FTN_AD_MAXSEG") ? atoll(getenv("FTN_AD_MAXSEG")) : -1;
+    const int64_t maxseg = env_maxseg > 0 ? env_maxseg : std::max<int64_t>(16, (int64_t(4) << 30) / plane_bytes);
     if (seg > maxseg) {
       seg = maxseg;
       units = (int64_t)p.tiles_k * p.tiles_j * ((nx - 2 + seg - 1) / seg);
@@ -367,7 +378,14 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
     p.seg = (int32_t)seg;
     p.units = (uint32_t)units;
     const int64_t grid = std::min<int64_t>(grid0, units);
-    adv_tma_kernel<<<(unsigned)grid, AD_THREADS, AD_SMEM, s>>>(mu, mv, mw, p);
+    // 5 slots measured best at 2048x1024x1024 (3: 56, 4: 94, 5: 94-97, 6: 86 Gcells/s)
+    static const int ns = getenv("FTN_AD_NS") ? atoi(getenv("FTN_AD_NS")) : 5;
+    switch (ns) {
+      case 3: FTN_CHECK(launch_adv<3>((unsigned)grid, mu, mv, mw, p, s)); break;
+      case 5: FTN_CHECK(launch_adv<5>((unsigned)grid, mu, mv, mw, p, s)); break;
+      case 6: FTN_CHECK(launch_adv<6>((unsigned)grid, mu, mv, mw, p, s)); break;
+      default: FTN_CHECK(launch_adv<4>((unsigned)grid, mu, mv, mw, p, s)); break;
+    }
     return after_launch("adv_tma_kernel");
   }
   AdvGenParams G;
