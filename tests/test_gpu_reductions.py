@@ -171,3 +171,29 @@ def test_c4_full_size(ftn):
     sub = s.section((1, 1024), (1, 1024), (1, 1))
     host = sub.to_numpy()
     assert ftn.sum(sub).item() == oracle.reduce_orderR(OA(host), oracle.SUM)
+
+
+@pytest.mark.slow
+def test_c4_full_size_order_r_bit_exact(ftn):
+    """The bench's C4 SUM / MAXVAL / MINVAL on x(-511:512, 0:1023, 1:1024) = 2^30 elements of
+    U[0,1) (same generator and launch configuration as bench.py): bit-exact vs the oracle's
+    order-R emulation over the whole array; and DOT_PRODUCT at the paper's 2^27 size, bit-exact
+    vs order R and within the R#8 bound of the exact dot."""
+    x = ftn.FArray.empty((1024, 1024, 1024), lbounds=[-511, 0, 1])
+    ftn.gen_fill(x, synth.SEED, 10, ftn.GEN_U01)
+    host = x.to_numpy()
+    O = OA(host, [-511, 0, 1])
+    assert ftn.sum(x).item() == oracle.reduce_orderR(O, oracle.SUM)
+    assert ftn.maxval(x).item() == oracle.maxval(O)
+    assert ftn.minval(x).item() == oracle.minval(O)
+    del x, host, O
+    torch.cuda.empty_cache()
+    n = 1 << 27
+    X, Y = ftn.FArray.empty((n,)), ftn.FArray.empty((n,))
+    ftn.gen_fill(X, synth.SEED, 20, ftn.GEN_U11)
+    ftn.gen_fill(Y, synth.SEED, 21, ftn.GEN_U11)
+    got = ftn.dot_product(X, Y).item()
+    xo, yo = OA(X.to_numpy()), OA(Y.to_numpy())
+    assert got == oracle.dot_orderR(xo, yo)
+    e, a = oracle.dot_exact(xo, yo)
+    assert abs(got - e) <= 4 * n * U * a

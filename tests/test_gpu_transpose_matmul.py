@@ -188,3 +188,23 @@ def test_matmul_c3_full_size_sampled(ftn):
     ai, bi = A.tensor.cpu().numpy().astype(np.int64), B.tensor.cpu().numpy().astype(np.int64)
     rows = rng.integers(0, n, size=8)
     np.testing.assert_array_equal(C.tensor.cpu().numpy()[rows], (ai[rows] @ bi).astype(np.float64))
+
+
+@pytest.mark.slow
+def test_transpose_paper_size(ftn):
+    """Table III shape: int32 32768^2 (the bench row's launch configuration), offset-encoded
+    input (element t = i + 32768 j wraps modulo 2^32 exactly as the generator does); sampled
+    rows and columns of the result against the closed form."""
+    n = 32768
+    a = ftn.FArray.empty((n, n), dtype=torch.int32)
+    ftn.gen_fill(a, 0, 0, ftn.GEN_LINEAR)
+    r = ftn.FArray.empty((n, n), dtype=torch.int32)
+    ftn.transpose(r, a)
+    rng = np.random.default_rng(2)
+    for c in [0, 1, n - 1] + [int(v) for v in rng.integers(0, n, 6)]:
+        col = r.section((1, n), (c + 1, c + 1)).to_numpy().ravel()      # r(:, c) = a(c, :)
+        j = np.arange(n, dtype=np.int64)
+        np.testing.assert_array_equal(col, ((c + n * j) % (1 << 32)).astype(np.uint32).view(np.int32))
+        row = r.section((c + 1, c + 1), (1, n)).to_numpy().ravel()      # r(c, :) = a(:, c)
+        i = np.arange(n, dtype=np.int64)
+        np.testing.assert_array_equal(row, ((i + n * c) % (1 << 32)).astype(np.uint32).view(np.int32))
