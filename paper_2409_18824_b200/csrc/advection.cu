@@ -6,12 +6,13 @@
 //
 // HBM-bound: 24 B read + 24 B written per interior point (48 B/cell).
 //
-// TMA path (u, v, w TMA-able): a CTA owns a 64 (k) x 16 (j) tile of output columns and marches
-// along i.  Each i-plane of the three fields arrives as TMA boxes {68 x 18 x 1} (k-2 .. k+65,
-// j-1 .. j+16; the k start 64t-2 is 16-byte aligned) into a 5-slot mbarrier ring; when plane
-// i+1 has landed the 512 threads compute output plane i from the slots of planes i-1, i, i+1
-// (thread = a pair k, k+1 of one j row: its neighbours come as 16-byte pairs, LDS.128, and its
-// results leave as 16-byte stores), then one block barrier, after which thread 0 refills the slot
+// TMA path (u, v, w TMA-able): a CTA owns a 128 (k) x 8 (j) tile of output columns and marches
+// along i.  Each i-plane of the three fields arrives as TMA boxes {132 x 10 x 1} (k-2 .. k+129,
+// j-1 .. j+8; the k start 128t-2 is 16-byte aligned; 1 KB box rows keep DRAM efficient) into a
+// 5-slot mbarrier ring; when plane i+1 has landed the 512 threads compute output plane i from
+// the slots of planes i-1, i, i+1 (thread = a pair k, k+1 of one j row: its neighbours come as
+// 16-byte pairs, LDS.128, and its results leave as 16-byte stores), then one block barrier,
+// after which thread 0 refills the slot
 // of plane i-1 (no producer warp, no empty barriers).  Work units = (tile, i-segment), tile
 // fastest, round-robin (plan_units_halo).
 // Generic path (any strides): one thread per output point, direct loads.
@@ -30,11 +31,18 @@ bool stencil_tma_able(const ftn_desc_t* d);
 
 namespace {
 
-constexpr int AD_OK = 64, AD_OJ = 16;               // output tile (k, j)
-constexpr int AD_BK = AD_OK + 4, AD_BJ = AD_OJ + 2;  // box 68 x 18: k-2 .. k+65, j-1 .. j+16
+#ifndef FTN_AD_OK
+#define FTN_AD_OK 128
+#endif
+#ifndef FTN_AD_OJ
+#define FTN_AD_OJ 8
+#endif
+constexpr int AD_OK = FTN_AD_OK, AD_OJ = FTN_AD_OJ;  // output tile (k, j)
+constexpr int AD_PAIRS = AD_OK / 2;                 // threads per j row
+constexpr int AD_BK = AD_OK + 4, AD_BJ = AD_OJ + 2;  // box 132 x 10: k-2 .. k+129, j-1 .. j+8
 constexpr int AD_FIELD = (AD_BK * AD_BJ * 8 + 127) / 128 * 128;  // 9856 B per field box
 constexpr int AD_SLOT = 3 * AD_FIELD;
-constexpr int AD_THREADS = 512;
+constexpr int AD_THREADS = AD_PAIRS * AD_OJ;
 template <int NS>
 constexpr int ad_smem() { return NS * AD_SLOT + 128 + 8 * NS; }
 
@@ -101,7 +109,7 @@ __device__ __forceinline__ double tz_at(const AdvParams& p, int q, int k) {
 __device__ __forceinline__ void adv_unit(const AdvParams& p, uint32_t u, int& k0, int& j0, int& ia, int& ib) {
   const uint32_t ntile = (uint32_t)(p.tiles_k * p.tiles_j);
   const uint32_t t = u % ntile, sgi = u / ntile;
-  k0 = (int)(t % (uint32_t)p.tiles_k) * AD_OK;  // outputs k0 .. k0+63 (k = 0 is boundary)
+  k0 = (int)(t % (uint32_t)p.tiles_k) * AD_OK;  // outputs k0 .. k0+AD_OK-1 (k = 0 is boundary)
   j0 = 1 + (int)(t / (uint32_t)p.tiles_k) * AD_OJ;
   ia = 1 + (int)sgi * p.seg;
   ib = min(ia + p.seg, p.nx - 1);
@@ -174,7 +182,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_con
   }
   __syncthreads();
   const double* base = reinterpret_cast<const double*>(smem_raw + soff);
-  const int lane = threadIdx.x & 31, jr = threadIdx.x >> 5;  // pair (2 lane, 2 lane + 1), row jr
+  const int lane = threadIdx.x % AD_PAIRS, jr = threadIdx.x / AD_PAIRS;  // pair (2 lane, 2 lane + 1), row jr
   uint32_t g = 0;  // planes consumed so far
   for (uint32_t u = blockIdx.x; u < p.units; u += gridDim.x) {
     int k0, j0, ia, ib;
@@ -357,7 +365,7 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
     FTN_CHECK(make_map(&mu, u));
     FTN_CHECK(make_map(&mv, v));
     FTN_CHECK(make_map(&mw, w));
-    p.tiles_k = (int32_t)((nz - 1 + AD_OK - 1) / AD_OK);  // outputs k in [1, nz-2] within [0, 64 tiles_k)
+    p.tiles_k = (int32_t)((nz - 1 + AD_OK - 1) / AD_OK);  // outputs k in [1, nz-2] within [0, AD_OK tiles_k)
     p.vec_out = 1;
     for (const ftn_desc_t* o : {su, sv, sw})
       if (o->dim[0].sm != 8 || ((uintptr_t)o->base_addr % 16) || (o->dim[1].sm % 16) || (o->dim[2].sm % 16))
@@ -378,12 +386,14 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
     p.seg = (int32_t)seg;
     p.units = (uint32_t)units;
     const int64_t grid = std::min<int64_t>(grid0, units);
-    // 5 slots measured best at 2048x1024x1024 (3: 56, 4: 94, 5: 94-97, 6: 86 Gcells/s)
+    // measured at 2048x1024x1024 (Gcells/s): tile 64x16: NS 3: 56, 4: 94, 5: 94-97, 6: 86;
+    // tile 128x8: NS 4: 100, 5: 110, 6: 96, 7: 95; tile 192x5: NS 5: 107, 6: 109
     static const int ns = getenv("FTN_AD_NS") ? atoi(getenv("FTN_AD_NS")) : 5;
     switch (ns) {
       case 3: FTN_CHECK(launch_adv<3>((unsigned)grid, mu, mv, mw, p, s)); break;
       case 5: FTN_CHECK(launch_adv<5>((unsigned)grid, mu, mv, mw, p, s)); break;
       case 6: FTN_CHECK(launch_adv<6>((unsigned)grid, mu, mv, mw, p, s)); break;
+      case 7: FTN_CHECK(launch_adv<7>((unsigned)grid, mu, mv, mw, p, s)); break;
       default: FTN_CHECK(launch_adv<4>((unsigned)grid, mu, mv, mw, p, s)); break;
     }
     return after_launch("adv_tma_kernel");
