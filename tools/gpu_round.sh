@@ -10,5 +10,5 @@ python bench.py --steps 2 --warmup 1 --rows none --no-cpu > gpurun_out/bench_sma
   python bench.py --steps 2 --warmup 1 --rows none --no-cpu > gpurun_out/ncu_launch_$tag.log 2>&1; echo "ncu launches rc=$?"
 python tools/prof_case.py all > gpurun_out/prof_plain_$tag.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"jacobi2d_wf|jacobi2d_tma|jacobi3d_tma|jacobi3d_tb2|reduce_chunks|transpose_kernel|dmma_gemm|ew_kernel<double, 5" -c 16 \
+  -k regex:"jacobi2d_wf|jacobi2d_tma|jacobi3d_tma|jacobi3d_tb2|reduce_chunks|transpose_kernel|dmma_gemm|ew_kernel<double, 5|vec|adv_tma" -c 24 \
   -o gpurun_out/prof_$tag python tools/prof_case.py all > gpurun_out/ncu_full_$tag.log 2>&1; echo "ncu full rc=$?"
