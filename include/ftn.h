@@ -230,7 +230,7 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
  * keeps the intermediate iterates in registers (temporal blocking, SURVEY §8(f) f2,
  * DESIGN.md §4.3), rank-3 sweeps up to min(T, 2) at a time (§4.4).  Results are
  * bit-identical for every T; the array that does not hold the result holds an earlier
- * iterate.  T in 1..4 (1 = one sweep per launch); default 4 or the FTN_JACOBI_FUSE
+ * iterate.  T in 1..6 (1 = one sweep per launch); default 5 or the FTN_JACOBI_FUSE
  * environment variable.  Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);

@@ -464,16 +464,17 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
 
 static bool g_attr_done[64];
 
-// Sweeps fused per launch for 2-D arrays (1 = off, 2..4): ftn_jacobi_set_fusion, else the
-// FTN_JACOBI_FUSE environment variable, else 4 (measured on B200 at 8192^2 x 100 with the
-// register-ring kernel: T=2 ~640, T=3 955-975, T=4 1036-1039 GLUPS).
+// Sweeps fused per launch for 2-D arrays (1 = off, 2..6): ftn_jacobi_set_fusion, else the
+// FTN_JACOBI_FUSE environment variable, else 5 (measured on B200 at 8192^2 x 100 with the
+// register-ring kernel: T=2 ~640, T=3 955-975, T=4 1230-1254, T=5 1484-1501, T=6 1190-1330
+// GLUPS).
 static std::atomic<int> g_fuse{0};
 int jacobi_fuse_T() {
   int t = g_fuse.load();
   if (t == 0) {
     const char* e = getenv("FTN_JACOBI_FUSE");
-    t = e ? atoi(e) : 4;
-    t = t < 1 ? 1 : (t > 4 ? 4 : t);
+    t = e ? atoi(e) : 5;
+    t = t < 1 ? 1 : (t > 6 ? 6 : t);
     g_fuse.store(t);
   }
   return t;
@@ -510,8 +511,8 @@ ftn_status_t jacobi_prepare() {
 using namespace ftn;
 
 extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
-  if (sweeps_per_launch < 1 || sweeps_per_launch > 4)
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..4 sweeps per launch");
+  if (sweeps_per_launch < 1 || sweeps_per_launch > 6)
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..6 sweeps per launch");
   g_fuse.store(sweeps_per_launch);
   return FTN_OK;
 }

@@ -282,6 +282,15 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 29: return launch_wf<2, WFCfg<2, 4, 6, 4, 1>>(WF_ARGS);
     case 39: return launch_wf<3, WFCfg<3, 4, 6, 4, 1>>(WF_ARGS);
     case 49: return launch_wf<4, WFCfg<4, 4, 6, 4, 1>>(WF_ARGS);
+    case 59: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3>>(WF_ARGS);   // 128 regs: 3 CTAs/SM
+    case 69: return launch_wf<6, WFCfg<6, 4, 6, 4, 1>>(WF_ARGS);
+    case 58: return launch_wf<5, WFCfg<5, 4, 6, 4, 1>>(WF_ARGS);
+    case 68: return launch_wf<6, WFCfg<6, 4, 6, 4, 1, 3>>(WF_ARGS);
+    case 57: return launch_wf<5, WFCfg<5, 4, 12, 3, 1, 3>>(WF_ARGS);
+    case 56: return launch_wf<5, WFCfg<5, 4, 6, 6, 1, 3>>(WF_ARGS);
+    case 55: return launch_wf<5, WFCfg<5, 4, 3, 8, 1, 3>>(WF_ARGS);
+    case 67: return launch_wf<6, WFCfg<6, 4, 3, 8, 1, 3>>(WF_ARGS);
+    case 66: return launch_wf<6, WFCfg<6, 3, 6, 4, 1, 4>>(WF_ARGS);
     // tuning variants (FTN_WF_CFG)
     case 38: return launch_wf<3, WFCfg<3, 4, 12, 3, 2>>(WF_ARGS);   // lag 2: levels independent
     case 48: return launch_wf<4, WFCfg<4, 4, 12, 3, 2>>(WF_ARGS);
@@ -303,7 +312,7 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 44: return launch_wf<4, WFCfg<4, 2, 12, 3, 1>>(WF_ARGS);
   }
 #undef WF_ARGS
-  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..4 (and FTN_WF_CFG a known variant)");
+  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..6 (and FTN_WF_CFG a known variant)");
 }
 
 // The whole interior of a single array: rows 1 .. n2-2, boundary rows 0 and n2-1.

@@ -75,6 +75,7 @@ def _slabs(u0, p, halo, rng_fill=True):
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("shape,halo", [((300, 203), 1), ((300, 203), 3), ((140, 33, 45), 1), ((130, 301), 4),
+                                        ((260, 407), 5), ((200, 500), 6),
                                         ((129, 201), 2)])
 def test_jacobi_decomposition_independence(ftn, p, shape, halo):
     """p slabs with `halo` halo planes; k owned planes exchanged per step (device copies standing

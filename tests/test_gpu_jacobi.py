@@ -7,6 +7,7 @@ import torch
 import oracle
 import synth
 from oracle import FArray as OA
+DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
 
 pytestmark = pytest.mark.gpu
 C2, C3 = 0.25, 1.0 / 6.0
@@ -129,7 +130,7 @@ def test_c2_full_size_sampled(ftn):
         assert got == ref, (i, j)
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("shape", [(3, 3), (5, 40), (40, 5), (129, 31), (200, 301), (257, 77), (1000, 130)])
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 7, 8, 9])
 def test_2d_temporal_blocking(ftn, T, shape, sweeps):
@@ -141,17 +142,17 @@ def test_2d_temporal_blocking(ftn, T, shape, sweeps):
         got, ref = _run_both(ftn, u0, sweeps, C2, [1, 0])
         np.testing.assert_array_equal(got, ref)
     finally:
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
 
 
 def test_2d_temporal_blocking_long_strip(ftn):
     """Many units per CTA, uneven segments, 60 sweeps."""
-    for T in (2, 3, 4):
+    for T in (2, 3, 4, 5, 6):
         ftn.jacobi_set_fusion(T)
         u0 = synth.jacobi_init((3000, 2000), array_id=T)
         got, ref = _run_both(ftn, u0, 12, C2)
         np.testing.assert_array_equal(got, ref)
-    ftn.jacobi_set_fusion(4)
+    ftn.jacobi_set_fusion(DEFAULT_FUSION)
 
 
 @pytest.mark.parametrize("T", [1, 2])
@@ -168,7 +169,7 @@ def test_3d_temporal_blocking(ftn, T, shape, sweeps):
         got, ref = _run_both(ftn, u0, sweeps, C3, [0, 2, -1])
         np.testing.assert_array_equal(got, ref)
     finally:
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
 
 
 def test_3d_temporal_blocking_many_units(ftn):

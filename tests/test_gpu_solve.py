@@ -6,6 +6,7 @@ import pytest
 import oracle
 import synth
 from oracle import FArray as OA
+DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
 
 pytestmark = pytest.mark.gpu
 
@@ -29,7 +30,7 @@ def test_maxval_absdiff(ftn):
     assert got == np.max(np.abs(a[88::-2, ::3] - b[0:89:2, ::-3]))
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("shape,check,tol", [((130, 97), 5, 1e-3), ((130, 97), 7, -1.0), ((300, 200), 10, 1e-4),
                                              ((60, 50, 40), 4, 1e-3)])
 def test_jacobi_solve(ftn, T, shape, check, tol):
@@ -44,4 +45,4 @@ def test_jacobi_solve(ftn, T, shape, check, tol):
         assert (done, res, new) == (d2, r2, n2)
         np.testing.assert_array_equal((W if new else U).to_numpy(), b if n2 else a)
     finally:
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)

@@ -12,6 +12,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2409_18824_b200 import ftn  # noqa: E402
+DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
 
 SEED = 18824
 
@@ -23,11 +24,11 @@ def main(which):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
-        ftn.jacobi(U, W, 8)      # two fused launches (4 sweeps each, jacobi2d_wf<4>), the default
-        ftn.jacobi(U, W, 8)
+        ftn.jacobi(U, W, 10)     # two fused launches (5 sweeps each, jacobi2d_wf<5>), the default
+        ftn.jacobi(U, W, 10)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi2d_tma)
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
         del U, W
     if "jacobi3d" in which:
         n = 512
@@ -37,7 +38,7 @@ def main(which):
         ftn.jacobi(U, W, 4)      # two launches of jacobi3d_tb2 (2 sweeps each)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi3d_tma)
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
         del U, W
     if "muladd" in which:
         n = 1 << 27

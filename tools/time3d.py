@@ -10,6 +10,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2409_18824_b200 import ftn  # noqa: E402
+DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
 
 
 def main(shapes, pad=0):
@@ -38,7 +39,7 @@ def main(shapes, pad=0):
             ms = e0.elapsed_time(e1) / reps / sweeps
             gl = (shape[0] - 2) * (shape[1] - 2) * (shape[2] - 2) / ms / 1e6
             print(f"{shape} T={T}: {ms:.3f} ms/sweep  {gl:.1f} GLUPS  ({gl * 16:.0f} GB/s-equiv)")
-        ftn.jacobi_set_fusion(4)
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
         del U, W
         if pad:
             del BU, BW
