@@ -194,7 +194,7 @@ def bench_jacobi2d(torch, ftn, args, ctx):
         # rotate over NSTR streams and buffer sets, so one step's device-to-host copy overlaps
         # the next steps' host-to-device copies (PCIe is full duplex) and kernels; every step
         # still moves its full input and result
-        NSTR = 3
+        NSTR = int(os.environ.get("FTN_E2E_STREAMS", "3"))
         sets = [(ftn.FArray.empty(shape), ftn.FArray.empty(shape),
                  torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True).t()) for _ in range(NSTR)]
         streams = [torch.cuda.Stream() for _ in range(NSTR)]
