@@ -34,7 +34,10 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 
 namespace {
 
-constexpr int B3_X = 64, B3_Y = 32;                  // box (level 0) extent in i, j
+#ifndef FTN_J3_BOX_X
+#define FTN_J3_BOX_X 64
+#endif
+constexpr int B3_X = FTN_J3_BOX_X, B3_Y = 2048 / FTN_J3_BOX_X;  // box (level 0) extent in i, j
 constexpr int B3_OX = B3_X - 4, B3_OY = B3_Y - 4;    // output tile 60 x 28
 constexpr int B3_PE = B3_X * B3_Y;                   // elements per plane
 constexpr int B3_PLANE = B3_PE * 8;                  // 16 KB
