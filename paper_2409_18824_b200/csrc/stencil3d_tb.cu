@@ -37,7 +37,13 @@ namespace {
 #ifndef FTN_J3_BOX_X
 #define FTN_J3_BOX_X 64
 #endif
-constexpr int B3_X = FTN_J3_BOX_X, B3_Y = 2048 / FTN_J3_BOX_X;  // box (level 0) extent in i, j
+#ifndef FTN_J3_BOX_Y
+#define FTN_J3_BOX_Y 32
+#endif
+#ifndef FTN_J3_CTAS
+#define FTN_J3_CTAS 1
+#endif
+constexpr int B3_X = FTN_J3_BOX_X, B3_Y = FTN_J3_BOX_Y;  // box (level 0) extent in i, j
 constexpr int B3_OX = B3_X - 4, B3_OY = B3_Y - 4;    // output tile 60 x 28
 constexpr int B3_PE = B3_X * B3_Y;                   // elements per plane
 constexpr int B3_PLANE = B3_PE * 8;                  // 16 KB
@@ -170,7 +176,7 @@ __device__ __forceinline__ void tb3_step(const J3Unit& U, int q, uint32_t gq, do
   }
 }
 
-__global__ void __launch_bounds__(B3_THREADS, 1) jacobi3d_tb2(const __grid_constant__ CUtensorMap map,
+__global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __grid_constant__ CUtensorMap map,
                                                               const __grid_constant__ J3TParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
