@@ -230,3 +230,29 @@ def test_jacobi_host_buffers(ftn, shape, sweeps):
     ftn.jacobi_host(host_u, host_u, U, W, sweeps, coeff)       # in place on the host
     torch.cuda.synchronize()
     np.testing.assert_array_equal(host_u.numpy(), wo if new_o else uo)
+
+
+@pytest.mark.slow
+def test_c5_bench_configuration_100_sweeps(ftn):
+    """C5 exactly as bench.py runs it (2048^3, 100 sweeps = 50 launches of jacobi3d_tb2):
+    sampled points recomputed by the oracle on their dependence cone (203^3 windows)."""
+    n, sweeps = 2048, 100
+    U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
+    ftn.gen_fill(U, synth.SEED, 7, ftn.GEN_U01)
+    ftn.assign(W, U)
+    assert ftn.jacobi_plan(sweeps, 2) == [2] * 50
+    pts = [(1, 1, 1), (n - 2, 1000, 5), (700, 1300, 1900), (150, n - 2, 60)]
+    R = sweeps + 1
+    wins = []
+    for p in pts:
+        lo = [max(0, c - R) for c in p]
+        hi = [min(n, c + R + 1) for c in p]
+        wins.append((p, lo, np.asfortranarray(U.section(*[(a + 1, b) for a, b in zip(lo, hi)]).to_numpy())))
+    in_new = ftn.jacobi(U, W, sweeps)
+    assert not in_new
+    for p, lo, win in wins:
+        a, b = win.copy(order="F"), win.copy(order="F")
+        new = oracle.jacobi(OA(a), OA(b), sweeps, C3)
+        ref = (b if new else a)[tuple(c - l for c, l in zip(p, lo))]
+        got = U.section(*[(c + 1, c + 1) for c in p]).to_numpy().ravel()[0]
+        assert got == ref, p
