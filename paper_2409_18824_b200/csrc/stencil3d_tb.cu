@@ -47,7 +47,11 @@ constexpr int B3_X = FTN_J3_BOX_X, B3_Y = FTN_J3_BOX_Y;  // box (level 0) extent
 constexpr int B3_OX = B3_X - 4, B3_OY = B3_Y - 4;    // output tile 60 x 28
 constexpr int B3_PE = B3_X * B3_Y;                   // elements per plane
 constexpr int B3_PLANE = B3_PE * 8;                  // 16 KB
-constexpr int B3_NS0 = 8, B3_NS1 = 3;                // level-0 TMA ring, level-1 ring
+#ifndef FTN_J3_LAG2
+#define FTN_J3_LAG2 0  // measured: lag 2 512 vs lag 1 566 GLUPS at 2048^3 x 100
+#endif
+// level 2 lags level 1 by two planes (LAG2: the two levels of a step are independent) or one
+constexpr int B3_NS0 = 8, B3_NS1 = FTN_J3_LAG2 ? 4 : 3;  // level-0 TMA ring, level-1 ring
 constexpr int B3_ROWS = FTN_J3_ROWS;                 // j rows per thread
 constexpr int B3_THREADS = B3_X * (B3_Y / B3_ROWS);  // 512 at 4 rows
 constexpr int B3_SMEM = (B3_NS0 + B3_NS1) * B3_PLANE + 128 + 8 * B3_NS0;
@@ -176,6 +180,76 @@ __device__ __forceinline__ void tb3_step(const J3Unit& U, int q, uint32_t gq, do
   }
 }
 
+// Lag-2 step (PH = q mod 4): level 1 of plane q-1 and level 2 of plane q-3 are independent
+// (level 2 reads level-1 planes q-4 .. q-2, finished in earlier steps), so their instruction
+// streams interleave; 4-slot register rings (a: level 0, b: level 1) and a 4-slot shared
+// level-1 ring (the slot written at step q, plane q-1, was last read at step q-2).  Step nq
+// (no new plane) only drains level 2.
+template <int PH>
+__device__ __forceinline__ void tb3_step_l2(const J3Unit& U, int q, int nq, uint32_t gq, double (&a)[4][B3_ROWS],
+                                            double (&b)[4][B3_ROWS]) {
+  constexpr int A0 = PH, A1 = (PH + 3) % 4, A2 = (PH + 2) % 4;  // a slots of planes q, q-1, q-2
+  constexpr int B1 = (PH + 3) % 4;                              // b slot of level-1 plane q-1
+  constexpr int C2 = (PH + 2) % 4, C3 = (PH + 1) % 4, C4 = PH;  // b slots of planes q-2, q-3, q-4
+  const bool load = q < nq;
+  if (load) {
+    dev::mbar_wait(&U.full[gq % B3_NS0], (uint32_t)((gq / B3_NS0) & 1));
+    const double* Lq = U.L0 + (gq % B3_NS0) * B3_PE + U.own;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) a[A0][r] = Lq[r * B3_X];
+  }
+  if (load && q >= 2) {  // level 1 of plane q-1 -> b[B1] and shared slot B1
+    const double* Lp = U.L0 + ((gq - 1) % B3_NS0) * B3_PE;
+    double xl[B3_ROWS], xr[B3_ROWS];
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      xl[r] = Lp[U.xm + r * B3_X];
+      xr[r] = Lp[U.xp + r * B3_X];
+    }
+    const double ylo = Lp[U.ylo], yhi = Lp[U.yhi];
+    const uint32_t keep = (q <= U.qlo || q >= U.qhi) ? 0xffffffffu : U.fix_rows;
+    double* W = U.L1 + B1 * B3_PE + U.own;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      const double up = r == 0 ? ylo : a[A1][r - 1];
+      const double dn = r == B3_ROWS - 1 ? yhi : a[A1][r + 1];
+      double v = xl[r] + xr[r];
+      v = v + up;
+      v = v + dn;
+      v = v + a[A2][r];
+      v = v + a[A0][r];
+      v = U.c * v;
+      v = ((keep >> r) & 1) ? a[A1][r] : v;
+      b[B1][r] = v;
+      W[r * B3_X] = v;
+    }
+  }
+  if (q >= 5) {  // level 2 of plane q-3 (an output plane) from level-1 planes q-4, q-3, q-2
+    const double* Lr = U.L1 + C3 * B3_PE;
+    double xl[B3_ROWS], xr[B3_ROWS];
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      xl[r] = Lr[U.xm + r * B3_X];
+      xr[r] = Lr[U.xp + r * B3_X];
+    }
+    const double ylo = Lr[U.ylo], yhi = Lr[U.yhi];
+    char* out = U.out + (int64_t)(U.ka - 5 + q) * U.d_sm3;
+#pragma unroll
+    for (int r = 0; r < B3_ROWS; ++r) {
+      const double up = r == 0 ? ylo : b[C3][r - 1];
+      const double dn = r == B3_ROWS - 1 ? yhi : b[C3][r + 1];
+      double v = xl[r] + xr[r];
+      v = v + up;
+      v = v + dn;
+      v = v + b[C4][r];
+      v = v + b[C2][r];
+      v = U.c * v;
+      if ((U.st_rows >> r) & 1) *reinterpret_cast<double*>(out + r * U.d_sm2) = v;
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __grid_constant__ CUtensorMap map,
                                                               const __grid_constant__ J3TParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -212,7 +286,9 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
   U.xp = y0 * B3_X + (x < B3_X - 1 ? x + 1 : B3_X - 1);
   U.ylo = (y0 > 0 ? y0 - 1 : 0) * B3_X + x;                            // unused when y0 == 0
   U.yhi = (y0 + B3_ROWS < B3_Y ? y0 + B3_ROWS : B3_Y - 1) * B3_X + x;  // unused when y0 + R == 32
+#if !FTN_J3_LAG2
   double a[3][B3_ROWS], b[3][B3_ROWS];
+#endif
   uint32_t g = 0;  // level-0 planes consumed so far (ring slot / phase)
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
     int32_t i0, j0, ka, kb;
@@ -235,6 +311,29 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
       if (st_col && y >= 2 && y < B3_Y - 2 && gj >= 1 && gj <= p.n2 - 2) U.st_rows |= 1u << r;
     }
     const int nq = kb - ka + 4;  // level-0 planes ka-2 .. kb+1
+#if FTN_J3_LAG2
+    double a4[4][B3_ROWS], b4[4][B3_ROWS];
+    // steps 0 .. nq-1 consume a plane; step nq drains level 2; thread 0 refills the slot of
+    // level-0 plane gq-1 after the barrier of step gq (consuming steps only)
+    for (int q = 0; q <= nq; q += 4) {
+      tb3_step_l2<0>(U, q, nq, g + q, a4, b4);
+      if (threadIdx.x == 0 && q < nq && g + q >= 1) {
+        dev::fence_proxy_async();
+        cursor_issue(cur, G, units, &map, smem, full, g + q - 1 + B3_NS0);
+      }
+#pragma unroll
+      for (int d = 1; d < 4; ++d) {
+        if (q + d > nq) break;
+        if (d == 1) tb3_step_l2<1>(U, q + 1, nq, g + q + 1, a4, b4);
+        if (d == 2) tb3_step_l2<2>(U, q + 2, nq, g + q + 2, a4, b4);
+        if (d == 3) tb3_step_l2<3>(U, q + 3, nq, g + q + 3, a4, b4);
+        if (threadIdx.x == 0 && q + d < nq) {
+          dev::fence_proxy_async();
+          cursor_issue(cur, G, units, &map, smem, full, g + q + d - 1 + B3_NS0);
+        }
+      }
+    }
+#else
     for (int q = 0; q < nq; q += 3) {
       tb3_step<0>(U, q, g + q, a, b);
       if (threadIdx.x == 0 && g + q >= 1) {  // level-0 plane g+q-1 is free: refill its slot
@@ -256,6 +355,7 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
         }
       }
     }
+#endif
     g += nq;
   }
 }
