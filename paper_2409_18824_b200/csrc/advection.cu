@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) adv_generic_kernel(const __grid_constant_
 template <int NS>
 ftn_status_t launch_adv(unsigned grid, const CUtensorMap& mu, const CUtensorMap& mv, const CUtensorMap& mw,
                         const AdvParams& p, cudaStream_t s) {
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64] = {};  // per device: dynamic smem attribute set (idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {

@@ -253,7 +253,7 @@ ftn_status_t make_map(CUtensorMap* map, const ftn_desc_t* d, uint32_t box0, uint
 
 template <bool TA, bool TB>
 ftn_status_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const MParams& p, cudaStream_t s) {
-  static bool attr_set[64] = {false};
+  static std::atomic<bool> attr_set[64] = {};  // per device (idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {

@@ -462,7 +462,7 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
   return FTN_OK;
 }
 
-static bool g_attr_done[64];
+static std::atomic<bool> g_attr_done[64] = {};  // per device (idempotent)
 
 // Sweeps fused per launch for 2-D arrays (1 = off, 2..6): ftn_jacobi_set_fusion, else the
 // FTN_JACOBI_FUSE environment variable, else 5 (measured on B200 at 8192^2 x 100 with the

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
 
 // Two fused 3-D sweeps src -> dst over the whole interior (TMA-able rank-3 src).
 ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s) {
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64] = {};  // per device: dynamic smem attribute set (idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {

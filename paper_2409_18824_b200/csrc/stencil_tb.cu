@@ -230,7 +230,7 @@ template <int T, class C>
 ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t row_lo, int64_t row_hi,
                        int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
   constexpr int WF_R = C::R;
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64] = {};  // per device: dynamic smem attribute set (idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
