@@ -359,7 +359,10 @@ __global__ void __launch_bounds__(MV_ROWS) matvec_kernel(const __grid_constant__
 // Packed, 32-byte aligned a with m % 4 == 0: thread owns 4 consecutive rows (one 256-bit
 // load per column, a warp covers 128 rows = 1 KB), MV_U columns in flight; every row is
 // folded over the chunk in l order exactly as in matvec_kernel (same bits).
-constexpr int MV4_THREADS = 128, MV4_ROWS = 4 * MV4_THREADS, MV_U = 8;
+#ifndef FTN_MV_U
+#define FTN_MV_U 8
+#endif
+constexpr int MV4_THREADS = 128, MV4_ROWS = 4 * MV4_THREADS, MV_U = FTN_MV_U;
 
 __global__ void __launch_bounds__(MV4_THREADS) matvec_v4_kernel(const __grid_constant__ MVParams p) {
   __shared__ double xs[MV_MAXLC];
