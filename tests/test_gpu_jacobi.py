@@ -256,3 +256,33 @@ def test_c5_bench_configuration_100_sweeps(ftn):
         ref = (b if new else a)[tuple(c - l for c, l in zip(p, lo))]
         got = U.section(*[(c + 1, c + 1) for c in p]).to_numpy().ravel()[0]
         assert got == ref, p
+
+
+def test_error_paths_launch_nothing(ftn):
+    """Every rejected call returns its status before any launch and leaves the arrays as they
+    were (host validation first, never partial output)."""
+    u0 = synth.jacobi_init((20, 16))
+    U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+    n0 = ftn.launch_count()
+    cases = [
+        lambda: ftn.jacobi(U, W, -1),                                          # negative sweeps
+        lambda: ftn.jacobi(U, U.section((1, 20), (1, 16)), 1),                 # overlapping
+        lambda: ftn.jacobi(ftn.FArray.empty((20, 16), dtype=torch.float32),
+                           ftn.FArray.empty((20, 16), dtype=torch.float32), 1),  # real(4)
+        lambda: ftn.jacobi_slab(U, W, 2, 1, True, True),                       # sweeps > halo
+        lambda: ftn.jacobi_slab(U, W, 1, 8, True, True),                       # no owned plane
+        lambda: ftn.jacobi_set_fusion(7),
+        lambda: ftn.jacobi_set_fusion(0),
+    ]
+    for f in cases:
+        with pytest.raises(ftn.FtnError):
+            f()
+    host = torch.zeros((16, 20), dtype=torch.float64).t()
+    h10 = torch.zeros((16, 10), dtype=torch.float64).t()
+    with pytest.raises(ftn.FtnError):            # device arrays must be packed
+        ftn.jacobi_host(h10, h10, U.section((1, 20, 2), (1, 16)), W.section((1, 20, 2), (1, 16)), 1)
+    with pytest.raises(ValueError):              # host buffers must have u's shape
+        ftn.jacobi_host(torch.zeros((5, 5), dtype=torch.float64), host, U, W, 1)
+    assert ftn.launch_count() == n0
+    np.testing.assert_array_equal(U.to_numpy(), u0)
+    np.testing.assert_array_equal(W.to_numpy(), u0)
