@@ -35,9 +35,10 @@ namespace {
 
 template <int T, int WF_NW = 4 /*compute warps per CTA*/, int WF_R = 8 /*rows per TMA box*/,
           int WF_NS = 4 /*ring stages*/, int WF_LAG = 1 /*rows of lag per level*/,
-          int WF_MINB = 1 /*__launch_bounds__ min blocks per SM*/>
+          int WF_MINB = 1 /*__launch_bounds__ min blocks per SM*/,
+          int WF_NOPROD = 0 /*1: no producer warp; the last warp to release a slot refills it*/>
 struct WFCfg {
-  static constexpr int NW = WF_NW, R = WF_R, NS = WF_NS, LAG = WF_LAG, MINB = WF_MINB;
+  static constexpr int NW = WF_NW, R = WF_R, NS = WF_NS, LAG = WF_LAG, MINB = WF_MINB, NOPROD = WF_NOPROD;
   // level t produces row s - LAG*t at step s; extra input rows beyond the dependency cone
   static constexpr int EXTRA = (WF_LAG - 1) * T;
   static constexpr int H = T + (T & 1);
@@ -45,8 +46,8 @@ struct WFCfg {
   static constexpr int OUT = WF_NW * WO;          // output columns per CTA strip
   static constexpr int BW = OUT + 2 * H;          // box width (<= 256, even)
   static constexpr int STAGE = (BW * WF_R * 8 + 127) / 128 * 128;
-  static constexpr int SMEM = WF_NS * STAGE + 128 + 64;
-  static constexpr int THREADS = (WF_NW + 1) * 32;
+  static constexpr int SMEM = WF_NS * STAGE + 128 + 128;
+  static constexpr int THREADS = (WF_NW + (WF_NOPROD ? 0 : 1)) * 32;
   static constexpr bool ALIGNED = ((H - T) % 2) == 0;  // lane column pairs 16-byte aligned in smem
   static_assert(BW <= 256, "TMA box width");
   static_assert(WF_R % 3 == 0, "rows per box: a multiple of 3 (register ring slots are compile-time)");
@@ -67,6 +68,36 @@ struct WFParams {
   double coeff;
 };
 
+// Box cursor for the producer-less variant: the position of a box in this CTA's sequence
+// (unit, chunk); every compute warp keeps one NS boxes ahead of the box it consumes, so the
+// warp that releases a slot last can refill it at once (no producer warp, no polling).
+template <int T, class C>
+struct WFCursor {
+  int64_t u, q, nch, c, ja;
+  __device__ __forceinline__ void unit(const WFParams& p) {
+    c = u % p.strips;
+    ja = p.row_lo + (u / p.strips) * p.seg;
+    const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
+    nch = (jb - ja + 2 * T + C::EXTRA + C::R - 1) / C::R;
+    q = 0;
+  }
+  __device__ __forceinline__ void start(const WFParams& p) {
+    u = blockIdx.x;
+    if (u < p.units) unit(p);
+  }
+  __device__ __forceinline__ void advance(const WFParams& p) {
+    if (u < p.units && ++q == nch) {
+      u += gridDim.x;
+      if (u < p.units) unit(p);
+    }
+  }
+  __device__ __forceinline__ void issue(const WFParams& p, const CUtensorMap* map, uint8_t* smem, uint64_t* full,
+                                        int s) const {
+    dev::mbar_arrive_expect_tx(&full[s], C::BW * C::R * 8);
+    dev::tma_load_2d(smem + s * C::STAGE, map, &full[s], (int32_t)(c * C::OUT - C::H), (int32_t)(ja - T + q * C::R));
+  }
+};
+
 template <int T, class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_constant__ CUtensorMap src_map,
                                                           const __grid_constant__ WFParams p) {
@@ -83,10 +114,23 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_
     }
     dev::fence_barrier_init();
   }
+  uint32_t* relcnt = reinterpret_cast<uint32_t*>(empty + WF_NS);  // NOPROD: warps done with a slot
+  if (C::NOPROD && threadIdx.x == 0) {
+    for (int s = 0; s < WF_NS; ++s) relcnt[s] = 0;
+  }
   __syncthreads();
   const int64_t G = gridDim.x;
+  WFCursor<T, C> icur;  // NOPROD: NS boxes ahead of the consumed one
+  if (C::NOPROD) {
+    icur.start(p);
+    if (threadIdx.x == 0) dev::prefetch_tma(&src_map);
+    for (int s = 0; s < WF_NS; ++s) {
+      if (threadIdx.x == 0 && icur.u < p.units) icur.issue(p, &src_map, smem, full, s);
+      icur.advance(p);
+    }
+  }
 
-  if (warp == WF_NW) {
+  if (!C::NOPROD && warp == WF_NW) {
     // ---------------- producer lane: every box of every unit of this CTA, in order
     if (lane == 0) {
       dev::prefetch_tma(&src_map);
@@ -221,7 +265,23 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_
       if (fast) chunk(st, s0, true);
       else chunk(st, (int)(q * WF_R), false);
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[k % WF_NS]);
+      if constexpr (C::NOPROD) {
+        if (lane == 0) {
+          const int sl = (int)(k % WF_NS);
+          __threadfence_block();  // this warp's reads of the slot happen before its release
+          if (atomicAdd(&relcnt[sl], 1u) == WF_NW - 1) {  // last warp out: refill with box k + NS
+            relcnt[sl] = 0;
+            __threadfence_block();
+            if (icur.u < p.units) {
+              dev::fence_proxy_async();
+              icur.issue(p, &src_map, smem, full, sl);
+            }
+          }
+        }
+        icur.advance(p);
+      } else {
+        if (lane == 0) dev::mbar_arrive(&empty[k % WF_NS]);
+      }
     }
   }
 }
@@ -273,18 +333,30 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
 // Input rows [row_lo - T, row_hi + T] are read.
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                                  int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
+  // FTN_WF_CFG selects a tuning variant for every T that has one; other T use the default
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
+  int key = cfg < 0 ? T * 10 + 9 : T * 10 + cfg;
+  for (int attempt = 0; attempt < 2; ++attempt, key = T * 10 + 9) {
 #define WF_ARGS src, dst, coeff, row_lo, row_hi, fix_lo, fix_hi, s
-  switch (cfg < 0 ? T * 10 + 9 : T * 10 + cfg) {
+  switch (key) {
     // defaults (cfg 9): measured on B200 (R=6 NS=4 1253 vs R=12 NS=3 1230 GLUPS at T=4),
     // DESIGN.md §4.3; R must be a multiple of 3
     case 19: return launch_wf<1, WFCfg<1, 4, 6, 4, 1>>(WF_ARGS);
     case 29: return launch_wf<2, WFCfg<2, 4, 6, 4, 1>>(WF_ARGS);
     case 39: return launch_wf<3, WFCfg<3, 4, 6, 4, 1>>(WF_ARGS);
     case 49: return launch_wf<4, WFCfg<4, 4, 6, 4, 1>>(WF_ARGS);
-    case 59: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3>>(WF_ARGS);   // 128 regs: 3 CTAs/SM
+    // T = 5: no producer warp (the last warp to release a slot refills it), 128 registers,
+    // 4 CTAs x 4 warps per SM: 1570 GLUPS vs 1500 with a producer warp (3 CTAs x 5 warps)
+    case 59: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
     case 69: return launch_wf<6, WFCfg<6, 4, 6, 4, 1>>(WF_ARGS);
-    case 58: return launch_wf<5, WFCfg<5, 4, 6, 4, 1>>(WF_ARGS);
+    case 58: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3>>(WF_ARGS);   // producer warp, 3 CTAs/SM
+    case 51: return launch_wf<5, WFCfg<5, 4, 6, 4, 1>>(WF_ARGS);
+    case 50: return launch_wf<5, WFCfg<5, 4, 6, 5, 1, 4, 1>>(WF_ARGS);
+    case 40: return launch_wf<4, WFCfg<4, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
+    case 30: return launch_wf<3, WFCfg<3, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
+    case 20: return launch_wf<2, WFCfg<2, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
+    case 60: return launch_wf<6, WFCfg<6, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
+    case 61: return launch_wf<6, WFCfg<6, 4, 3, 8, 1, 4, 1>>(WF_ARGS);
     case 68: return launch_wf<6, WFCfg<6, 4, 6, 4, 1, 3>>(WF_ARGS);
     case 57: return launch_wf<5, WFCfg<5, 4, 12, 3, 1, 3>>(WF_ARGS);
     case 56: return launch_wf<5, WFCfg<5, 4, 6, 6, 1, 3>>(WF_ARGS);
@@ -300,8 +372,6 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 46: return launch_wf<4, WFCfg<4, 3, 12, 3, 1>>(WF_ARGS);
     case 35: return launch_wf<3, WFCfg<3, 4, 3, 8, 1>>(WF_ARGS);
     case 45: return launch_wf<4, WFCfg<4, 4, 3, 8, 1>>(WF_ARGS);
-    case 30: return launch_wf<3, WFCfg<3, 4, 24, 2, 1>>(WF_ARGS);
-    case 40: return launch_wf<4, WFCfg<4, 4, 24, 2, 1>>(WF_ARGS);
     case 31: return launch_wf<3, WFCfg<3, 4, 12, 3, 1>>(WF_ARGS);
     case 41: return launch_wf<4, WFCfg<4, 4, 12, 3, 1>>(WF_ARGS);
     case 32: return launch_wf<3, WFCfg<3, 4, 12, 4, 1>>(WF_ARGS);
@@ -312,6 +382,7 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 44: return launch_wf<4, WFCfg<4, 2, 12, 3, 1>>(WF_ARGS);
   }
 #undef WF_ARGS
+  }
   return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_fused: T must be 1..6 (and FTN_WF_CFG a known variant)");
 }
 
