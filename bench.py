@@ -388,11 +388,11 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                 t, interior = None, 0
         else:
             from paper_2409_18824_b200 import dist as D
-            g0, nl = D.jacobi_slab(n, N, rank)
+            g0, nl = D.jacobi_slab(n, N, rank, halo=2)   # 2 halo planes: 2 fused sweeps per exchange
             U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
             ftn.gen_fill(U, SEED, 7 + rank, ftn.GEN_U01)
             ftn.assign(W, U)
-            t = timed(torch, lambda: comm.jacobi(U, W, sweeps, halo=1), max(2, steps // 2), 1, ctx["clocks"], dist)
+            t = timed(torch, lambda: comm.jacobi(U, W, sweeps, halo=2), max(2, steps // 2), 1, ctx["clocks"], dist)
             interior = (n - 2) ** 3
             del U, W
         torch.cuda.empty_cache()
@@ -400,8 +400,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             ns = max(2, steps // 2)
             gl = interior * sweeps * ns / t / 1e9
             # algorithmic bytes: 16 B per interior point per launch (jacobi3d_tb2 does 2 sweeps
-            # per launch, ftn_jacobi_plan with T = min(fusion, 2); the dist path 1 per launch)
-            nl3 = len(ftn.jacobi_plan(sweeps, 1 if distmode else min(2, ftn.jacobi_fusion())))
+            # per launch, ftn_jacobi_plan with T = min(fusion, 2), also on the 2-halo slabs)
+            nl3 = len(ftn.jacobi_plan(sweeps, min(2, ftn.jacobi_fusion())))
             gbs = 16 * interior * nl3 * ns / t / 1e9 / N
             rows["c5_jacobi3d_2048"] = {"value": gl, "unit": "GLUPS", "ms_per_sweep": t / ns / sweeps * 1e3,
                                         "launches_per_step": nl3,

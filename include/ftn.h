@@ -320,9 +320,9 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local,
  * [halo, n_last - halo) are owned, rank r's first owned plane follows rank r-1's last,
  * and on the first (last) rank local plane halo-1 (n_last-halo) is the global boundary
  * plane.  Per step the k owned planes next to each neighbour are exchanged with
- * ncclSend/ncclRecv (k = 1, or k = T sweeps fused per step for TMA-able rank-2 slabs,
- * T = min(halo, ftn_jacobi_get_fusion())) and ftn_jacobi_slab advances the owned planes
- * by k sweeps.  Results are bit-identical to ftn_jacobi on the undivided array;
+ * ncclSend/ncclRecv (k = 1, or k = T sweeps fused per step for TMA-able slabs,
+ * T = min(halo, ftn_jacobi_get_fusion()) for rank 2 and min(halo, 2, fusion) for rank 3)
+ * and ftn_jacobi_slab advances the owned planes by k sweeps.  Results are bit-identical to ftn_jacobi on the undivided array;
  * *result_in_unew as for ftn_jacobi. */
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const ftn_desc_t* unew_local,
                              int64_t sweeps, double coeff, int32_t halo, int32_t* result_in_unew,
@@ -333,7 +333,7 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const f
  * slab laid out as for ftn_jacobi_dist whose halo planes are current, src -> dst.  Reads src
  * planes [halo - sweeps, n_last - halo + sweeps); writes only the owned interior of dst.
  * first / last: this slab holds the global lower / upper boundary plane.  sweeps > 1 needs
- * a TMA-able rank-2 slab (FTN_ERR_UNSUPPORTED otherwise). */
+ * a TMA-able slab: rank 2 up to 6 sweeps, rank 3 exactly 2 (FTN_ERR_UNSUPPORTED otherwise). */
 ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
                              int32_t halo, int32_t first, int32_t last, ftn_stream_t stream);
 

@@ -10,6 +10,8 @@
 //   * MATMUL: column blocks of b and c, a replicated (ftn_bcast once).
 #include "ftn_internal.cuh"
 
+#include <algorithm>
+
 #include <nccl.h>
 #include <cstring>
 #include <vector>
@@ -162,10 +164,11 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
-  // temporal blocking: T sweeps per exchange when the slab is rank 2 and TMA-able
+  // temporal blocking: up to T sweeps per exchange (rank 2: the fusion setting, rank 3: 2),
+  // at most the halo depth
   int T = 1;
-  if (r == 2 && stencil_tma_able(u) && stencil_tma_able(unew)) {
-    T = jacobi_fuse_T();
+  if (stencil_tma_able(u) && stencil_tma_able(unew)) {
+    T = r == 2 ? jacobi_fuse_T() : std::min(2, jacobi_fuse_T());
     if (T > halo) T = halo;
   }
   const int64_t nplan = ftn_jacobi_plan(sweeps, T, nullptr, 0);

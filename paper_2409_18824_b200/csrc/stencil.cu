@@ -50,6 +50,8 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
 ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s);
+ftn_status_t jacobi3d_fused2_planes(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t plane_lo,
+                                    int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                                  int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 
@@ -614,8 +616,9 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
     return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need halo >= 1 and at least one owned plane");
   if (sweeps < 1 || sweeps > halo) return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need 1 <= sweeps <= halo");
   const bool tma = stencil_tma_able(src) && stencil_tma_able(dst);
-  if (sweeps > 1 && !(r == 2 && tma))
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_slab: several sweeps per step need a TMA-able rank-2 slab");
+  if (sweeps > 1 && !(tma && (r == 2 || sweeps == 2)))
+    return fail(FTN_ERR_UNSUPPORTED,
+                "ftn_jacobi_slab: several sweeps per step need a TMA-able slab (rank 2: up to 6, rank 3: 2)");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
@@ -631,6 +634,11 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
   }
   const int64_t fix_lo = first ? lo - 1 : INT64_MIN / 4;
   const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
+  if (r == 3) {
+    // 32-bit plane arithmetic in the kernel: clamp the "no boundary" sentinels to the slab
+    const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
+    return jacobi3d_fused2_planes(src, dst, coeff, lo, hi, flo, fhi, s);
+  }
   return jacobi2d_fused_rows(src, dst, sweeps, coeff, lo, hi, fix_lo, fix_hi, s);
 }
 

@@ -62,18 +62,20 @@ struct J3TParams {
   int64_t n1, n2, n3;
   int64_t tiles_i, tiles_j;
   int64_t seg, units;   // output planes per unit, units = tiles * segments
+  int64_t plane_lo, plane_hi;  // output planes [plane_lo, plane_hi] (0-based positions in dim 3)
+  int64_t fix_lo, fix_hi;      // planes <= fix_lo and >= fix_hi keep their value at every level
   double coeff;
 };
 
 // Unit u -> (tile origin, output planes [ka, kb)); 32-bit (units, tiles < 2^31).
 struct J3Geom {
-  int32_t ntile, tiles_i, seg, n3;
+  int32_t ntile, tiles_i, seg, plane_lo, plane_end;  // output planes [plane_lo, plane_end)
   __device__ __forceinline__ void unit(uint32_t u, int32_t& i0, int32_t& j0, int32_t& ka, int32_t& kb) const {
     const uint32_t t = u % (uint32_t)ntile, sgi = u / (uint32_t)ntile;
     i0 = (int32_t)(t % (uint32_t)tiles_i) * B3_OX - 2;
     j0 = (int32_t)(t / (uint32_t)tiles_i) * B3_OY - 2;
-    ka = 1 + (int32_t)sgi * seg;
-    kb = min(ka + seg, n3 - 1);
+    ka = plane_lo + (int32_t)sgi * seg;
+    kb = min(ka + seg, plane_end);
   }
 };
 
@@ -260,7 +262,8 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
   G.ntile = (int32_t)(p.tiles_i * p.tiles_j);
   G.tiles_i = (int32_t)p.tiles_i;
   G.seg = (int32_t)p.seg;
-  G.n3 = (int32_t)p.n3;
+  G.plane_lo = (int32_t)p.plane_lo;
+  G.plane_end = (int32_t)(p.plane_hi + 1);
   const uint32_t units = (uint32_t)p.units;
   J3Cursor cur;
   cur.u = blockIdx.x;
@@ -296,8 +299,9 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
     const int64_t gi = i0 + x;
     U.ka = ka;
     // level 1 at step q is plane ka - 3 + q: a boundary plane when <= 0 or >= n3 - 1
-    U.qlo = 3 - ka;
-    U.qhi = G.n3 + 2 - ka;
+    // level 1 at step q is plane ka - 3 + q: held fixed when <= fix_lo or >= fix_hi
+    U.qlo = (int)(p.fix_lo + 3 - ka);
+    U.qhi = (int)(p.fix_hi + 3 - ka);
     const bool col_fixed = gi <= 0 || gi >= p.n1 - 1;
     const bool st_col = x >= 2 && x < B3_X - 2 && gi >= 1 && gi <= p.n1 - 2;
     U.out = p.dst + gi * p.d_sm1 + (int64_t)(j0 + y0) * p.d_sm2;
@@ -362,8 +366,12 @@ __global__ void __launch_bounds__(B3_THREADS, FTN_J3_CTAS) jacobi3d_tb2(const __
 
 }  // namespace
 
-// Two fused 3-D sweeps src -> dst over the whole interior (TMA-able rank-3 src).
-ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s) {
+// Two fused 3-D sweeps src -> dst on output planes [plane_lo, plane_hi] (0-based positions in
+// dim 3) of a TMA-able rank-3 src; planes <= fix_lo and >= fix_hi are held fixed (the global
+// boundary; for a slab of the distributed path the planes outside the global array are never
+// consumed).  Reads src planes [plane_lo - 2, plane_hi + 2].
+ftn_status_t jacobi3d_fused2_planes(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t plane_lo,
+                                    int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
   static std::atomic<bool> attr[64] = {};  // per device: dynamic smem attribute set (idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
@@ -379,7 +387,12 @@ ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, doubl
   p.n1 = src->dim[0].extent;
   p.n2 = src->dim[1].extent;
   p.n3 = src->dim[2].extent;
-  if (p.n1 < 3 || p.n2 < 3 || p.n3 < 3) return FTN_OK;
+  p.plane_lo = plane_lo;
+  p.plane_hi = plane_hi;
+  p.fix_lo = fix_lo;
+  p.fix_hi = fix_hi;
+  const int64_t nk = plane_hi - plane_lo + 1;
+  if (p.n1 < 3 || p.n2 < 3 || nk <= 0) return FTN_OK;
   p.tiles_i = (p.n1 - 1 + B3_OX - 1) / B3_OX;
   p.tiles_j = (p.n2 - 1 + B3_OY - 1) / B3_OY;
   p.coeff = coeff;
@@ -393,7 +406,7 @@ ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, doubl
   FTN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi3d_tb2, B3_THREADS, B3_SMEM));
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)num_sms() * occ;
-  plan_units_halo(p.tiles_i * p.tiles_j, p.n3 - 2, grid, 4, &p.seg, &p.units);
+  plan_units_halo(p.tiles_i * p.tiles_j, nk, grid, 4, &p.seg, &p.units);
   // Cap the unit length so that a wave's units span at most ~4 GiB of k-planes (measured at
   // 2048^3, 32 MiB planes: 128-plane units 503 GLUPS vs 432 with the cost-model choice of
   // 1023; at 1024^3 the cap is 512 planes and changes nothing).  FTN_J3_MAXSEG overrides.
@@ -402,11 +415,17 @@ ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, doubl
   const int64_t maxseg = env_maxseg >= 0 ? env_maxseg : std::max<int64_t>(32, (int64_t(4) << 30) / plane_bytes);
   if (maxseg > 0 && p.seg > maxseg) {
     p.seg = maxseg;
-    p.units = p.tiles_i * p.tiles_j * ((p.n3 - 2 + p.seg - 1) / p.seg);
+    p.units = p.tiles_i * p.tiles_j * ((nk + p.seg - 1) / p.seg);
   }
   if (grid > p.units) grid = p.units;
   jacobi3d_tb2<<<(unsigned)grid, B3_THREADS, B3_SMEM, s>>>(m, p);
   return after_launch("jacobi3d_tb2");
+}
+
+// Two fused 3-D sweeps src -> dst over the whole interior.
+ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s) {
+  const int64_t n3 = src->dim[2].extent;
+  return jacobi3d_fused2_planes(src, dst, coeff, 1, n3 - 2, 0, n3 - 1, s);
 }
 
 }  // namespace ftn

@@ -36,12 +36,13 @@ def slab(n_last: int, nranks: int, rank: int) -> Slab:
     return Slab(rank, nranks, lo, hi, rank > 0, rank < nranks - 1)
 
 
-def jacobi_slab(n_last: int, nranks: int, rank: int) -> tuple[int, int]:
+def jacobi_slab(n_last: int, nranks: int, rank: int, halo: int = 1) -> tuple[int, int]:
     """Interior planes 1..n_last-2 are split over the ranks; the local array of a rank spans
-    global planes [lo-1, hi+1) (one halo / boundary plane on each side).  Returns (first
-    global plane of the local array, local extent)."""
+    its owned planes plus `halo` halo planes on each side (the first / last rank's outermost
+    planes beyond the global boundary plane are never consumed).  Returns (first global plane
+    of the local array, local extent)."""
     s = slab(n_last - 2, nranks, rank)
-    return s.lo, s.owned + 2
+    return s.lo + 1 - halo, s.owned + 2 * halo
 
 
 def reduction_slab_aligned(n_elems: int, plane_elems: int, nranks: int) -> bool:

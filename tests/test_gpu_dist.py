@@ -76,7 +76,7 @@ def _slabs(u0, p, halo, rng_fill=True):
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("shape,halo", [((300, 203), 1), ((300, 203), 3), ((140, 33, 45), 1), ((130, 301), 4),
                                         ((260, 407), 5), ((200, 500), 6),
-                                        ((129, 201), 2)])
+                                        ((129, 201), 2), ((70, 40, 61), 2), ((64, 33, 50), 3), ((65, 33, 50), 2)])
 def test_jacobi_decomposition_independence(ftn, p, shape, halo):
     """p slabs with `halo` halo planes; k owned planes exchanged per step (device copies standing
     in for ncclSend/Recv), ftn_jacobi_slab advancing k sweeps; == the undivided ftn_jacobi."""
@@ -93,8 +93,10 @@ def test_jacobi_decomposition_independence(ftn, p, shape, halo):
             if 0 <= g0 + k < shape[-1]:
                 part[..., k] = u0[..., g0 + k]
         arrs.append([ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)])
-    tma_able = len(shape) == 2 and (shape[0] * 8) % 16 == 0       # dim-2 stride a multiple of 16 B
-    T = min(ftn.jacobi_fusion(), halo) if tma_able else 1
+    # TMA-able slabs: every stride beyond dim 1 a multiple of 16 B (the local slabs share them)
+    tma_able = all((int(np.prod(shape[:d])) * 8) % 16 == 0 for d in range(1, len(shape)))
+    fuse = ftn.jacobi_fusion() if len(shape) == 2 else min(2, ftn.jacobi_fusion())
+    T = min(fuse, halo) if tma_able else 1
     steps = ftn.jacobi_plan(sweeps, T)                 # ftn_jacobi_dist's launch plan
     cur = 0
     for k in steps:
@@ -128,6 +130,23 @@ def test_jacobi_dist_single_rank_deep_halo(ftn, comm):
     n2 = ftn.jacobi(R, S, 11)
     assert n1 == n2
     got = (W if n1 else U).to_numpy()[:, halo - 1:halo - 1 + 120]
+    np.testing.assert_array_equal(got, (S if n2 else R).to_numpy())
+
+
+@pytest.mark.parametrize("halo,sweeps", [(2, 10), (2, 7), (3, 9)])
+def test_jacobi_dist_single_rank_3d_two_sweeps(ftn, comm, halo, sweeps):
+    """ftn_jacobi_dist at nranks = 1 on a 3-D slab with 2-3 halo planes: two fused sweeps per
+    exchange (jacobi3d_tb2 on a plane range with the global boundary planes held fixed); the
+    planes outside the global array are garbage that must never be consumed."""
+    u0 = synth.jacobi_init((70, 45, 40))
+    part = np.full((70, 45, 40 + 2 * (halo - 1)), 7.0e300, order="F")
+    part[:, :, halo - 1:halo - 1 + 40] = u0
+    U, W = ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)
+    n1 = comm.jacobi(U, W, sweeps, halo=halo)
+    R, S = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+    n2 = ftn.jacobi(R, S, sweeps)
+    assert n1 == n2
+    got = (W if n1 else U).to_numpy()[:, :, halo - 1:halo - 1 + 40]
     np.testing.assert_array_equal(got, (S if n2 else R).to_numpy())
 
 
