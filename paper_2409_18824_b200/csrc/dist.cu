@@ -5,8 +5,9 @@
 //     all-gathered and combined by the same balanced tree on every rank
 //     (deterministic; equal to the 1-GPU result when slabs are equal power-of-two
 //     multiples of the R chunk);
-//   * Jacobi: last-dimension slabs with one halo plane per side, halos exchanged
-//     with ncclSend/ncclRecv every sweep;
+//   * Jacobi: last-dimension slabs with `halo` planes per side; per launch of the plan the
+//     k owned planes next to each neighbour go out with grouped ncclSend/ncclRecv and the
+//     slab advances k fused sweeps (k <= halo: deep halos, one exchange per k sweeps);
 //   * MATMUL: column blocks of b and c, a replicated (ftn_bcast once).
 #include "ftn_internal.cuh"
 
