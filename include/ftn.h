@@ -295,6 +295,12 @@ ftn_status_t ftn_comm_unique_id(uint8_t id[FTN_COMM_ID_BYTES]);
 ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank,
                            const uint8_t id[FTN_COMM_ID_BYTES], int32_t device);
 ftn_status_t ftn_comm_destroy(ftn_comm_t comm);
+/* Overlap of the Jacobi halo exchange with the interior sweeps in ftn_jacobi_dist: the owned
+ * planes whose dependence cone stays inside the owned planes are advanced on a side stream
+ * of the communicator while ncclSend/ncclRecv run on the caller's stream; the planes next to
+ * the halos follow the exchange.  mode 0 = off, 1 = when nranks > 1 (default), 2 = always
+ * (also at nranks = 1, for testing).  Results are identical in every mode. */
+ftn_status_t ftn_comm_set_overlap(ftn_comm_t comm, int32_t mode);
 
 /* Global reductions of an array slab-distributed over the ranks along its
  * last dimension (x_local is this rank's slab).  The result, identical on

@@ -20,6 +20,9 @@
 struct ftn_comm_s {
   ncclComm_t nccl;
   int nranks, rank, device;
+  int overlap = 1;                 // 0 off, 1 when nranks > 1, 2 always (ftn_comm_set_overlap)
+  cudaStream_t side = nullptr;     // interior sweeps while the halo exchange runs
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
 };
 
 namespace ftn {
@@ -30,6 +33,9 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew);
 ftn_status_t jacobi_prepare();
 int jacobi_fuse_T();
 bool stencil_tma_able(const ftn_desc_t* d);
+ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
+                              int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
+                              cudaStream_t s);
 
 namespace {
 
@@ -111,12 +117,29 @@ ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank, const
     delete c;
     return nccl_fail(r, "ncclCommInitRank");
   }
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return fail(FTN_ERR_CUDA, "ftn_comm_init: stream / event creation failed");
+  }
   *comm = c;
+  return FTN_OK;
+}
+
+ftn_status_t ftn_comm_set_overlap(ftn_comm_t comm, int32_t mode) {
+  if (!comm) return fail(FTN_ERR_NULL, "ftn_comm_set_overlap: comm NULL");
+  if (mode < 0 || mode > 2) return fail(FTN_ERR_SHAPE, "ftn_comm_set_overlap: mode must be 0, 1 or 2");
+  comm->overlap = mode;
   return FTN_OK;
 }
 
 ftn_status_t ftn_comm_destroy(ftn_comm_t comm) {
   if (!comm) return FTN_OK;
+  if (comm->ev_in) cudaEventDestroy(comm->ev_in);
+  if (comm->ev_out) cudaEventDestroy(comm->ev_out);
+  if (comm->side) cudaStreamDestroy(comm->side);
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   delete comm;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
@@ -178,6 +201,8 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
   const size_t plane = (size_t)(desc_size(u) / nl);
   const int lower = comm->rank - 1, upper = comm->rank + 1;
   const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
+  const bool overlap = comm->overlap == 2 || (comm->overlap == 1 && comm->nranks > 1);
+  const int64_t lo = halo, hi = nl - halo - 1;
   int64_t launches = 0;
   for (; launches < nplan; ++launches) {
     const int k = plan[(size_t)launches];
@@ -185,6 +210,16 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
     const ftn_desc_t* dst = (launches % 2 == 0) ? unew : u;
     char* b = (char*)src->base_addr;
     const int64_t sm = src->dim[r - 1].sm;
+    // Overlap: the owned planes whose k-sweep dependence cone stays inside the owned planes,
+    // [lo + k, hi - k], are advanced on the side stream while the halos travel; the k planes
+    // next to each halo follow on the caller's stream after the exchange.
+    const bool split = overlap && hi - lo + 1 >= 4 * (int64_t)k;
+    if (split) {
+      FTN_CUDA(cudaEventRecord(comm->ev_in, s));
+      FTN_CUDA(cudaStreamWaitEvent(comm->side, comm->ev_in, 0));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side));
+      FTN_CUDA(cudaEventRecord(comm->ev_out, comm->side));
+    }
     if (comm->nranks > 1) {
       // the k owned planes next to each neighbour -> its k halo planes next to its owned planes
       FTN_NCCL(ncclGroupStart());
@@ -199,7 +234,13 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
       FTN_NCCL(ncclGroupEnd());
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    FTN_CHECK(ftn_jacobi_slab(src, dst, k, coeff, halo, first, last, stream));
+    if (split) {
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s));
+      FTN_CUDA(cudaStreamWaitEvent(s, comm->ev_out, 0));
+    } else {
+      FTN_CHECK(ftn_jacobi_slab(src, dst, k, coeff, halo, first, last, stream));
+    }
   }
   if (result_in_unew) *result_in_unew = (int32_t)(launches % 2);
   return FTN_OK;

@@ -604,6 +604,38 @@ extern "C" ftn_status_t ftn_jacobi_host(const double* host_u, double* host_resul
   return FTN_OK;
 }
 
+// Output planes [out_lo, out_hi] (within the owned planes [halo, n_last - halo)) of one
+// local step of the distributed DO nest: `sweeps` fused sweeps with the global boundary
+// planes of a first / last slab held fixed.  No validation (callers validate).
+namespace ftn {
+ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
+                              int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
+                              cudaStream_t s) {
+  const int r = src->rank;
+  const int64_t nl = src->dim[r - 1].extent;
+  const bool tma = stencil_tma_able(src) && stencil_tma_able(dst);
+  const int64_t lo = halo, hi = nl - halo - 1;
+  if (out_lo > out_hi) return FTN_OK;
+  if (sweeps == 1) {
+    CUtensorMap m;
+    const CUtensorMap* mp = nullptr;
+    if (tma) {
+      FTN_CHECK(make_stencil_map(&m, src));
+      mp = &m;
+    }
+    return sweep(src, dst, mp, coeff, out_lo, out_hi, s);
+  }
+  const int64_t fix_lo = first ? lo - 1 : INT64_MIN / 4;
+  const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
+  if (r == 3) {
+    // 32-bit plane arithmetic in the kernel: clamp the "no boundary" sentinels to the slab
+    const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
+    return jacobi3d_fused2_planes(src, dst, coeff, out_lo, out_hi, flo, fhi, s);
+  }
+  return jacobi2d_fused_rows(src, dst, sweeps, coeff, out_lo, out_hi, fix_lo, fix_hi, s);
+}
+}  // namespace ftn
+
 // One local step of the distributed DO nest, no communication: `sweeps`
 // (1 <= sweeps <= halo) sweeps of the owned planes [halo, n_last - halo) of a slab whose
 // halo planes are current; reads src planes [halo - sweeps, n_last - halo + sweeps).
@@ -621,25 +653,7 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
                 "ftn_jacobi_slab: several sweeps per step need a TMA-able slab (rank 2: up to 6, rank 3: 2)");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t lo = halo, hi = nl - halo - 1;
-  if (sweeps == 1) {
-    CUtensorMap m;
-    const CUtensorMap* mp = nullptr;
-    if (tma) {
-      FTN_CHECK(make_stencil_map(&m, src));
-      mp = &m;
-    }
-    return sweep(src, dst, mp, coeff, lo, hi, s);
-  }
-  const int64_t fix_lo = first ? lo - 1 : INT64_MIN / 4;
-  const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
-  if (r == 3) {
-    // 32-bit plane arithmetic in the kernel: clamp the "no boundary" sentinels to the slab
-    const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
-    return jacobi3d_fused2_planes(src, dst, coeff, lo, hi, flo, fhi, s);
-  }
-  return jacobi2d_fused_rows(src, dst, sweeps, coeff, lo, hi, fix_lo, fix_hi, s);
+  return jacobi_slab_part(src, dst, sweeps, coeff, halo, first, last, halo, nl - halo - 1, (cudaStream_t)stream);
 }
 
 // Jacobi iteration to convergence (R#25): blocks of check_every

@@ -92,6 +92,7 @@ def _load():
         "ftn_comm_init": [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8),
                           ctypes.c_int32],
         "ftn_comm_destroy": [vp],
+        "ftn_comm_set_overlap": [vp, ctypes.c_int32],
         "ftn_sum_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_maxval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_minval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
@@ -515,6 +516,10 @@ class Comm:
         if self.handle:
             _call("ftn_comm_destroy", self.handle)
             self.handle = ctypes.c_void_p()
+
+    def set_overlap(self, mode: int):
+        """Halo exchange / interior sweep overlap in jacobi(): 0 off, 1 when nranks > 1, 2 always."""
+        _call("ftn_comm_set_overlap", self.handle, mode)
 
     def _ws(self, x: FArray) -> torch.Tensor:
         return workspace(reduce_workspace_size(x) + 8 * (self.nranks + 1) + 64, x.tensor.device, "global")

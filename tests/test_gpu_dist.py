@@ -150,6 +150,31 @@ def test_jacobi_dist_single_rank_3d_two_sweeps(ftn, comm, halo, sweeps):
     np.testing.assert_array_equal(got, (S if n2 else R).to_numpy())
 
 
+@pytest.mark.parametrize("shape,halo,sweeps", [((300, 200), 5, 23), ((300, 200), 3, 10), ((257, 40), 5, 12),
+                                              ((70, 45, 60), 2, 9), ((70, 45, 60), 1, 5), ((100, 30, 12), 2, 6)])
+def test_jacobi_dist_overlap_split(ftn, comm, shape, halo, sweeps):
+    """ftn_comm_set_overlap(2) at nranks = 1: every launch is split into the interior part on
+    the communicator's side stream and the two halo-adjacent parts on the caller's stream
+    (the N > 1 overlap schedule); bit-identical to the unsplit run and to ftn_jacobi."""
+    u0 = synth.jacobi_init(shape, array_id=sum(shape))
+    ext = shape[:-1] + (shape[-1] + 2 * (halo - 1),)
+    part = np.full(ext, 7.0e300, order="F")
+    part[..., halo - 1:halo - 1 + shape[-1]] = u0
+    R, S = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+    n2 = ftn.jacobi(R, S, sweeps)
+    ref = (S if n2 else R).to_numpy()
+    try:
+        for mode in (2, 0):
+            comm.set_overlap(mode)
+            U, W = ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)
+            n1 = comm.jacobi(U, W, sweeps, halo=halo)
+            torch.cuda.synchronize()
+            assert n1 == n2
+            np.testing.assert_array_equal((W if n1 else U).to_numpy()[..., halo - 1:halo - 1 + shape[-1]], ref)
+    finally:
+        comm.set_overlap(1)
+
+
 @pytest.mark.parametrize("p", [2, 4, 8])
 def test_sum_decomposition_independence(ftn, p):
     n = 8 * 65536 * 4
