@@ -286,3 +286,26 @@ def test_error_paths_launch_nothing(ftn):
     assert ftn.launch_count() == n0
     np.testing.assert_array_equal(U.to_numpy(), u0)
     np.testing.assert_array_equal(W.to_numpy(), u0)
+
+
+def test_random_shapes_fusions_and_sweeps(ftn):
+    """Fuzz: random 2-D / 3-D shapes, lower bounds, sweep counts and fusion settings, all
+    bit-identical to the oracle (covers unit / segment / strip remainders the fixed cases miss)."""
+    rng = np.random.default_rng(2409)
+    try:
+        for it in range(40):
+            T = int(rng.integers(1, 7))
+            ftn.jacobi_set_fusion(T)
+            if it % 4 == 3:
+                shape = tuple(int(v) for v in rng.integers(3, 90, 3))
+                coeff = C3
+            else:
+                shape = (int(rng.integers(3, 700)), int(rng.integers(3, 300)))
+                coeff = C2
+            sweeps = int(rng.integers(0, 14))
+            lbs = [int(v) for v in rng.integers(-5, 6, len(shape))]
+            u0 = synth.jacobi_init(shape, array_id=it)
+            got, ref = _run_both(ftn, u0, sweeps, coeff, lbs)
+            np.testing.assert_array_equal(got, ref, err_msg=f"shape {shape} sweeps {sweeps} T {T}")
+    finally:
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
