@@ -104,3 +104,11 @@ def test_f4_full_size_sampled(ftn):
         for o, r in zip(O, ref):
             got = o.section((k + 1, k + 1), (j + 1, j + 1), (i + 1, i + 1)).to_numpy().ravel()[0]
             assert got == r[1, 1, 1], (k, j, i)
+
+
+def test_random_shapes(ftn):
+    """Fuzz: random shapes (tile remainders in k and j, short i), lower bounds, bit-exact."""
+    rng = np.random.default_rng(18824)
+    for it in range(12):
+        shape = (int(rng.integers(3, 300)), int(rng.integers(3, 40)), int(rng.integers(3, 20)))
+        _check(ftn, shape, lbs=[int(v) for v in rng.integers(-3, 4, 3)])
