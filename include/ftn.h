@@ -222,7 +222,13 @@ ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_d
  * u, unew: real(8), rank 2 (5-point) or rank 3 (7-point), conformable, not
  * overlapping.  Only interior points are written: the caller presets the
  * boundary of both arrays.  *result_in_unew (host) receives 1 when the final
- * values are in unew (odd sweeps), else 0.  Bit-exact vs the oracle. */
+ * values are in unew (odd sweeps), else 0.  Bit-exact vs the oracle.
+ * Arrays the TMA kernels cannot address (odd leading dimension, strided or reversed
+ * sections) are, for sweeps >= 8, copied to padded packed temporaries, advanced there by the
+ * temporally blocked kernels and copied back (both arrays; stream-ordered temporaries from
+ * the device's default memory pool, whose release threshold the library raises so that
+ * freed temporaries are reused); if the temporaries cannot be allocated the generic kernel
+ * runs instead.  Results are identical either way. */
 ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                         int32_t* result_in_unew, ftn_stream_t stream);
 

@@ -208,6 +208,19 @@ StreamTemp::~StreamTemp() {
 
 ftn_status_t StreamTemp::alloc(size_t bytes, cudaStream_t s) {
   stream = s;
+  // Keep freed temporaries in the device's default stream-ordered pool instead of returning
+  // them to the driver at every synchronisation (the default release threshold is 0, which
+  // makes a large temporary cost a fresh mapping on every call).
+  static std::atomic<bool> pool_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!pool_set[dev & 63].exchange(true)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   FTN_CUDA(cudaMallocAsync(&ptr, bytes > 0 ? bytes : 16, s));
   return FTN_OK;
 }

@@ -558,6 +558,48 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     FTN_CHECK(make_stencil_map(&mw, unew));
   }
   const int64_t nlast = u->dim[u->rank - 1].extent;
+  // Arrays the TMA kernels cannot address (odd leading dimension, sections with a non-unit
+  // first stride or unaligned strides): for enough sweeps, run the temporally blocked kernels
+  // on padded packed copies (copy both arrays in, the sweeps, copy both back: 4 extra passes
+  // instead of `sweeps` passes of the generic one-point-per-thread kernel).  Same results,
+  // same result array; falls back to the generic kernel if the temporaries do not fit.
+  static const int64_t pad_min = getenv("FTN_JACOBI_PAD_MIN") ? atoll(getenv("FTN_JACOBI_PAD_MIN")) : 8;
+  if (!tma && pad_min > 0 && sweeps >= pad_min) {
+    bool ok = true;
+    for (int d = 0; d < u->rank; ++d) ok = ok && u->dim[d].extent >= 3 && u->dim[d].extent < (1ll << 31);
+    if (ok) {
+      ftn_desc_t du, dw;
+      const int64_t n1 = u->dim[0].extent, ld = n1 + (n1 & 1);  // even leading dimension: 16-byte rows
+      size_t elems = (size_t)ld;
+      for (int d = 1; d < u->rank; ++d) elems *= (size_t)u->dim[d].extent;
+      StreamTemp tu, tw;
+      if (tu.alloc(elems * 8, s) == FTN_OK && tw.alloc(elems * 8, s) == FTN_OK) {
+        for (ftn_desc_t* d : {&du, &dw}) {
+          memset(d, 0, sizeof(*d));
+          d->base_addr = d == &du ? tu.ptr : tw.ptr;
+          d->elem_len = 8;
+          d->rank = u->rank;
+          d->type = FTN_F64;
+          int64_t sm = 8;
+          for (int k = 0; k < u->rank; ++k) {
+            d->dim[k].lower_bound = 1;
+            d->dim[k].extent = u->dim[k].extent;
+            d->dim[k].sm = sm;
+            sm *= k == 0 ? ld : u->dim[k].extent;
+          }
+        }
+        int32_t in_new = 0;
+        FTN_CHECK(launch_copy(&du, u, s));
+        FTN_CHECK(launch_copy(&dw, unew, s));
+        FTN_CHECK(ftn_jacobi(&du, &dw, sweeps, coeff, &in_new, stream));
+        FTN_CHECK(launch_copy(u, &du, s));
+        FTN_CHECK(launch_copy(unew, &dw, s));
+        if (result_in_unew) *result_in_unew = in_new;
+        return FTN_OK;
+      }
+      cudaGetLastError();  // allocation failed: clear it and take the generic path
+    }
+  }
   // Temporal blocking: launches of up to T fused sweeps (ftn_jacobi_plan).
   // Every launch swaps u/unew; the plan's launch count has the parity of `sweeps`, so the
   // result lands in unew iff sweeps is odd.
