@@ -512,6 +512,42 @@ ftn_status_t jacobi_prepare() {
 
 using namespace ftn;
 
+// Padded packed copies of u / unew (even leading dimension: TMA-able) for arrays the TMA
+// kernels cannot address; copies both in.  false (nothing enqueued) when an extent is
+// unsuitable or the temporaries cannot be allocated.
+static int64_t jacobi_pad_min() {
+  static const int64_t v = getenv("FTN_JACOBI_PAD_MIN") ? atoll(getenv("FTN_JACOBI_PAD_MIN")) : 8;
+  return v > 0 ? v : INT64_MAX;
+}
+
+static bool padded_pair(const ftn_desc_t* u, const ftn_desc_t* unew, cudaStream_t s, StreamTemp& tu, StreamTemp& tw,
+                        ftn_desc_t* du, ftn_desc_t* dw) {
+  for (int d = 0; d < u->rank; ++d)
+    if (u->dim[d].extent < 3 || u->dim[d].extent >= (1ll << 31)) return false;
+  const int64_t n1 = u->dim[0].extent, ld = n1 + (n1 & 1);  // even leading dimension: 16-byte rows
+  size_t elems = (size_t)ld;
+  for (int d = 1; d < u->rank; ++d) elems *= (size_t)u->dim[d].extent;
+  if (tu.alloc(elems * 8, s) != FTN_OK || tw.alloc(elems * 8, s) != FTN_OK) {
+    cudaGetLastError();  // allocation failed: the caller takes the generic path
+    return false;
+  }
+  for (ftn_desc_t* d : {du, dw}) {
+    memset(d, 0, sizeof(*d));
+    d->base_addr = d == du ? tu.ptr : tw.ptr;
+    d->elem_len = 8;
+    d->rank = u->rank;
+    d->type = FTN_F64;
+    int64_t sm = 8;
+    for (int k = 0; k < u->rank; ++k) {
+      d->dim[k].lower_bound = 1;
+      d->dim[k].extent = u->dim[k].extent;
+      d->dim[k].sm = sm;
+      sm *= k == 0 ? ld : u->dim[k].extent;
+    }
+  }
+  return launch_copy(du, u, s) == FTN_OK && launch_copy(dw, unew, s) == FTN_OK;
+}
+
 extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
   if (sweeps_per_launch < 1 || sweeps_per_launch > 6)
     return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..6 sweeps per launch");
@@ -563,41 +599,16 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
   // on padded packed copies (copy both arrays in, the sweeps, copy both back: 4 extra passes
   // instead of `sweeps` passes of the generic one-point-per-thread kernel).  Same results,
   // same result array; falls back to the generic kernel if the temporaries do not fit.
-  static const int64_t pad_min = getenv("FTN_JACOBI_PAD_MIN") ? atoll(getenv("FTN_JACOBI_PAD_MIN")) : 8;
-  if (!tma && pad_min > 0 && sweeps >= pad_min) {
-    bool ok = true;
-    for (int d = 0; d < u->rank; ++d) ok = ok && u->dim[d].extent >= 3 && u->dim[d].extent < (1ll << 31);
-    if (ok) {
-      ftn_desc_t du, dw;
-      const int64_t n1 = u->dim[0].extent, ld = n1 + (n1 & 1);  // even leading dimension: 16-byte rows
-      size_t elems = (size_t)ld;
-      for (int d = 1; d < u->rank; ++d) elems *= (size_t)u->dim[d].extent;
-      StreamTemp tu, tw;
-      if (tu.alloc(elems * 8, s) == FTN_OK && tw.alloc(elems * 8, s) == FTN_OK) {
-        for (ftn_desc_t* d : {&du, &dw}) {
-          memset(d, 0, sizeof(*d));
-          d->base_addr = d == &du ? tu.ptr : tw.ptr;
-          d->elem_len = 8;
-          d->rank = u->rank;
-          d->type = FTN_F64;
-          int64_t sm = 8;
-          for (int k = 0; k < u->rank; ++k) {
-            d->dim[k].lower_bound = 1;
-            d->dim[k].extent = u->dim[k].extent;
-            d->dim[k].sm = sm;
-            sm *= k == 0 ? ld : u->dim[k].extent;
-          }
-        }
-        int32_t in_new = 0;
-        FTN_CHECK(launch_copy(&du, u, s));
-        FTN_CHECK(launch_copy(&dw, unew, s));
-        FTN_CHECK(ftn_jacobi(&du, &dw, sweeps, coeff, &in_new, stream));
-        FTN_CHECK(launch_copy(u, &du, s));
-        FTN_CHECK(launch_copy(unew, &dw, s));
-        if (result_in_unew) *result_in_unew = in_new;
-        return FTN_OK;
-      }
-      cudaGetLastError();  // allocation failed: clear it and take the generic path
+  if (!tma && sweeps >= jacobi_pad_min()) {
+    StreamTemp tu, tw;
+    ftn_desc_t du, dw;
+    if (padded_pair(u, unew, s, tu, tw, &du, &dw)) {
+      int32_t in_new = 0;
+      FTN_CHECK(ftn_jacobi(&du, &dw, sweeps, coeff, &in_new, stream));
+      FTN_CHECK(launch_copy(u, &du, s));
+      FTN_CHECK(launch_copy(unew, &dw, s));
+      if (result_in_unew) *result_in_unew = in_new;
+      return FTN_OK;
     }
   }
   // Temporal blocking: launches of up to T fused sweeps (ftn_jacobi_plan).
@@ -717,6 +728,17 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
   const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
+  if (!tma && max_sweeps >= jacobi_pad_min() && check_every >= 3) {  // as in ftn_jacobi
+    StreamTemp tu, tw;
+    ftn_desc_t du, dw;
+    if (padded_pair(u, unew, s, tu, tw, &du, &dw)) {
+      FTN_CHECK(ftn_jacobi_solve(&du, &dw, max_sweeps, check_every, tol, coeff, ws, ws_bytes, sweeps_done, residual,
+                                 result_in_unew, stream));
+      FTN_CHECK(launch_copy(u, &du, s));
+      FTN_CHECK(launch_copy(unew, &dw, s));
+      return FTN_OK;
+    }
+  }
   const int T = jacobi_fuse_for(u, unew);
   double* res_dev = reinterpret_cast<double*>(ws);
   char* rw = reinterpret_cast<char*>(ws) + 16;
