@@ -31,15 +31,20 @@ _NP2TYPE = {np.dtype(np.int32): I32, np.dtype(np.int64): I64,
             np.dtype(np.float32): F32, np.dtype(np.float64): F64}
 
 
-def build(openmp: bool = True) -> str:
-    """Compile liboracle.so with gcc (-O2 -ffp-contract=off; no -ffast-math)."""
+def build(openmp: bool = True, sanitize: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2 -ffp-contract=off; no -ffast-math).  sanitize=True
+    builds liboracle_san.so instead: AddressSanitizer + UndefinedBehaviorSanitizer, errors fatal,
+    no OpenMP (tests/test_oracle_sanitized.py loads it through FTN_ORACLE_LIB)."""
+    out = _LIB if not sanitize else os.path.join(_HERE, "liboracle_san.so")
     cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=gnu11",
-           "-Wall", _SRC, "-o", _LIB + ".tmp", "-lm"]
-    if openmp:
+           "-Wall", _SRC, "-o", out + ".tmp", "-lm"]
+    if sanitize:
+        cmd[1:1] = ["-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined", "-fno-sanitize-recover=all"]
+    elif openmp:
         cmd.insert(1, "-fopenmp")
     subprocess.run(cmd, check=True)
-    os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 class _Dim(ctypes.Structure):
@@ -57,9 +62,12 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if (not os.path.exists(_LIB)) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-            build()
-        L = ctypes.CDLL(_LIB)
+        path = os.environ.get("FTN_ORACLE_LIB")   # e.g. the sanitizer build
+        if path is None:
+            if (not os.path.exists(_LIB)) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+                build()
+            path = _LIB
+        L = ctypes.CDLL(path)
         P = ctypes.POINTER(_Array)
         i64p = ctypes.POINTER(ctypes.c_int64)
         dp = ctypes.POINTER(ctypes.c_double)
