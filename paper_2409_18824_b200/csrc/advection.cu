@@ -319,6 +319,7 @@ extern "C" ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t*
                                          const ftn_desc_t* u, const ftn_desc_t* v, const ftn_desc_t* w,
                                          const ftn_desc_t* tzc1, const ftn_desc_t* tzc2, const ftn_desc_t* tzd1,
                                          const ftn_desc_t* tzd2, double tcx, double tcy, ftn_stream_t stream) {
+  NvtxRange nvtx_("ftn_pw_advection");
   const ftn_desc_t* f6[6] = {su, sv, sw, u, v, w};
   const char* names[6] = {"ftn_pw_advection(su)", "ftn_pw_advection(sv)", "ftn_pw_advection(sw)",
                           "ftn_pw_advection(u)", "ftn_pw_advection(v)", "ftn_pw_advection(w)"};

@@ -176,6 +176,7 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local, 
 
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
                              double coeff, int32_t halo, int32_t* result_in_unew, ftn_stream_t stream) {
+  NvtxRange nvtx_("ftn_jacobi_dist");
   if (!comm) return fail(FTN_ERR_NULL, "ftn_jacobi_dist: comm NULL");
   FTN_CHECK(jacobi_check(u, unew));
   if (!plane_contiguous(u) || !plane_contiguous(unew))
@@ -215,12 +216,14 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
     // next to each halo follow on the caller's stream after the exchange.
     const bool split = overlap && hi - lo + 1 >= 4 * (int64_t)k;
     if (split) {
+      NvtxRange r_("jacobi_dist interior (side stream)");
       FTN_CUDA(cudaEventRecord(comm->ev_in, s));
       FTN_CUDA(cudaStreamWaitEvent(comm->side, comm->ev_in, 0));
       FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side));
       FTN_CUDA(cudaEventRecord(comm->ev_out, comm->side));
     }
     if (comm->nranks > 1) {
+      NvtxRange r_("jacobi_dist halo exchange");
       // the k owned planes next to each neighbour -> its k halo planes next to its owned planes
       FTN_NCCL(ncclGroupStart());
       if (lower >= 0) {
@@ -235,6 +238,7 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
     if (split) {
+      NvtxRange r_("jacobi_dist halo-adjacent planes");
       FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s));
       FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s));
       FTN_CUDA(cudaStreamWaitEvent(s, comm->ev_out, 0));

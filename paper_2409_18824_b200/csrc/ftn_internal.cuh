@@ -11,7 +11,17 @@
 
 #include "ftn.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace ftn {
+
+// NVTX range for profilers (nsys / ncu --nvtx); header-only NVTX3, free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);

@@ -653,6 +653,7 @@ size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b) { return ws_bytes_for
 
 ftn_status_t matmul_local_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags, void* ws,
                              size_t ws_bytes, cudaStream_t s) {
+  NvtxRange nvtx_("ftn_matmul");
   const bool ta = flags & FTN_MATMUL_TRANSPOSE_A, tb = flags & FTN_MATMUL_TRANSPOSE_B;
   const size_t need = ws_bytes_for(a, b);
   if (need > 512 && (!ws || ws_bytes < need))

@@ -582,6 +582,7 @@ extern "C" int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, in
 
 extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                                    int32_t* result_in_unew, ftn_stream_t stream) {
+  NvtxRange nvtx_("ftn_jacobi");
   FTN_CHECK(jacobi_check(u, unew));
   if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi: negative sweep count");
   FTN_CHECK(require_sm100());
@@ -718,6 +719,7 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
                                          int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
                                          int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
                                          ftn_stream_t stream) {
+  NvtxRange nvtx_("ftn_jacobi_solve");
   FTN_CHECK(jacobi_check(u, unew));
   if (max_sweeps < 0 || check_every < 1) return fail(FTN_ERR_SHAPE, "ftn_jacobi_solve: need max_sweeps >= 0, check_every >= 1");
   size_t rws = 0;
