@@ -197,3 +197,24 @@ def test_c4_full_size_order_r_bit_exact(ftn):
     assert got == oracle.dot_orderR(xo, yo)
     e, a = oracle.dot_exact(xo, yo)
     assert abs(got - e) <= 4 * n * U * a
+
+
+@pytest.mark.slow
+def test_more_than_2_32_elements(ftn):
+    """64-bit indexing end to end (SURVEY §7 hard part 6): a (2^16 + 3) x 2^16 array (2^32 +
+    196608 elements, 32 GB) with the t mod 1024 pattern: SUM / MAXVAL closed forms, and an
+    element-wise b*c+d into a second array checked at sampled positions past 2^32."""
+    n1, n2 = 65536 + 3, 65536
+    x = ftn.FArray.empty((n1, n2))
+    ftn.gen_fill(x, synth.SEED, 0, ftn.GEN_MOD1024)
+    n = n1 * n2
+    full, rem = divmod(n, 1024)
+    assert ftn.sum(x).item() == float(full * 523776 + rem * (rem - 1) // 2)
+    assert ftn.maxval(x).item() == 1023.0
+    r = ftn.FArray.empty((n1, n2))
+    ftn.muladd(r, x, x, x)                                  # t' (t' + 1), t' = t mod 1024
+    for t in [0, 1023, (1 << 32) - 1, 1 << 32, (1 << 32) + 1025, n - 1]:
+        i, j = t % n1, t // n1
+        v = r.section((i + 1, i + 1), (j + 1, j + 1)).to_numpy().ravel()[0]
+        m = t % 1024
+        assert v == float(m * m + m), t
