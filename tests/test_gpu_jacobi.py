@@ -349,3 +349,14 @@ def test_non_tma_arrays_take_padded_fused_path(ftn, case, sweeps):
     res = (sw if new else su).to_numpy()
     ref = (OA(ow) if onew else OA(ou)).section(*osec).to_numpy()
     np.testing.assert_array_equal(res, ref)
+
+
+def test_subnormal_values_are_not_flushed(ftn):
+    """Neither side flushes subnormals (SURVEY §7 hard part 3): a field scaled into the
+    subnormal range gives the same bits on the fused GPU kernels and in the oracle."""
+    for shape, coeff, sweeps in (((130, 70), C2, 7), ((40, 30, 20), C3, 4)):
+        u0 = np.asfortranarray(synth.jacobi_init(shape, array_id=3) * 2.0 ** -1060)
+        assert np.count_nonzero((np.abs(u0) < 2.0 ** -1022) & (u0 != 0)) > 0
+        got, ref = _run_both(ftn, u0, sweeps, coeff)
+        np.testing.assert_array_equal(got, ref)
+        assert np.count_nonzero((np.abs(got) < 2.0 ** -1022) & (got != 0)) > 0
