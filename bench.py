@@ -550,7 +550,8 @@ def main():
 
     if rank == 0:
         cpu = None if args.no_cpu or world > 1 else cpu_oracle_jacobi()
-        frac = head["achieved_gbs"] / world / hbm_peak
+        # achieved_gbs is per GPU already (one rank's slab bytes per launch / max-over-ranks time)
+        frac = head["achieved_gbs"] / hbm_peak
         line = {
             "metric": METRIC, "value": head["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
@@ -562,7 +563,7 @@ def main():
             "roofline": {"bound": "hbm",
                          "kernel": (f"jacobi2d_wf<{head['plan']['max_sweeps_per_launch']}>"
                                     if head["plan"]["max_sweeps_per_launch"] > 1 else "jacobi2d_tma"),
-                         "achieved": head["achieved_gbs"] / world,
+                         "achieved": head["achieved_gbs"],
                          "peak": hbm_peak, "unit": "GB/s", "frac": frac, "peak_source": peak_src,
                          "traffic": traffic_from_profiles(),
                          "algorithmic_bytes_per_launch": head["per_launch_bytes"],
