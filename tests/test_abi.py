@@ -103,8 +103,12 @@ def test_compute_calls_validate_before_device(ftn):
 def test_jacobi_launch_plan(ftn):
     """ftn_jacobi_plan (host logic): sweep counts sum to S, each in 1..T, and the launch count
     has the parity of S (the result lands in unew iff S is odd)."""
-    for S in range(0, 60):
-        for T in (1, 2, 3, 4):
+    for S in range(0, 120):
+        for T in (1, 2, 3, 4, 5, 6):
             p = ftn.jacobi_plan(S, T)
             assert sum(p) == S and len(p) % 2 == S % 2 and all(1 <= k <= T for k in p), (S, T, p)
+            # at most two launches shorter than T (the remainder and the parity split)
+            assert sum(1 for k in p if k < T) <= 2, (S, T, p)
     assert ftn.jacobi_plan(100, 4).count(4) == 24 and len(ftn.jacobi_plan(100, 4)) == 26
+    assert ftn.jacobi_plan(100, 5) == [5] * 20          # the bench's plan: no short launch
+    assert ftn.jacobi_plan(100, 2) == [2] * 50          # C5's plan
