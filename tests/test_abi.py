@@ -107,8 +107,9 @@ def test_jacobi_launch_plan(ftn):
         for T in (1, 2, 3, 4, 5, 6):
             p = ftn.jacobi_plan(S, T)
             assert sum(p) == S and len(p) % 2 == S % 2 and all(1 <= k <= T for k in p), (S, T, p)
-            # at most two launches shorter than T (the remainder and the parity split)
-            assert sum(1 for k in p if k < T) <= 2, (S, T, p)
+            # at most three launches shorter than T (the remainder and the parity split k ->
+            # (k-1) + 1; e.g. S = 3, T = 2 needs [1, 1, 1])
+            assert sum(1 for k in p if k < T) <= 3, (S, T, p)
     assert ftn.jacobi_plan(100, 4).count(4) == 24 and len(ftn.jacobi_plan(100, 4)) == 26
     assert ftn.jacobi_plan(100, 5) == [5] * 20          # the bench's plan: no short launch
     assert ftn.jacobi_plan(100, 2) == [2] * 50          # C5's plan
