@@ -269,12 +269,17 @@ class FArray:
 _ws: dict = {}
 
 
-def workspace(nbytes: int, device=None, slot: str = "main") -> torch.Tensor:
+def workspace(nbytes: int, device=None, slot: str = "main", stream=None) -> torch.Tensor:
+    """Cached device workspace, one per (device, slot, stream): calls on different streams never
+    share one, and a buffer is allocated with its stream current so that the caching allocator
+    reuses it only in that stream's order after it is replaced."""
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    key = (dev, slot)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev, slot, st.cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(st):
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
         _ws[key] = buf
     return buf
 
@@ -318,7 +323,7 @@ def reduce_workspace_size(x: FArray) -> int:
 
 def _reduce(name, x: FArray, out=None, stream=None):
     res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
-    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce")
+    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce", stream)
     _call(name, x.ref(), ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
           _stream(stream))
     return res
@@ -368,7 +373,7 @@ def minval_dim(x: FArray, dim: int, out=None, stream=None) -> FArray:
 
 def dot_product(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:
     res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
-    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce")
+    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce", stream)
     _call("ftn_dot_product", x.ref(), y.ref(), ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
           ws.numel(), _stream(stream))
     return res
@@ -392,11 +397,11 @@ def matmul(c: FArray, a: FArray, b: FArray, transpose_a: bool = False, transpose
     if flags:
         n = ctypes.c_size_t()
         _call("ftn_matmul_ex_workspace_size", c.ref(), a.ref(), b.ref(), flags, ctypes.byref(n))
-        ws = workspace(n.value, c.tensor.device, "matmul")
+        ws = workspace(n.value, c.tensor.device, "matmul", stream)
         _call("ftn_matmul_ex", c.ref(), a.ref(), b.ref(), flags, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
               _stream(stream))
         return
-    ws = workspace(matmul_workspace_size(c, a, b), c.tensor.device, "matmul")
+    ws = workspace(matmul_workspace_size(c, a, b), c.tensor.device, "matmul", stream)
     _call("ftn_matmul", c.ref(), a.ref(), b.ref(), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
 
 
@@ -440,7 +445,7 @@ def jacobi_set_fusion(sweeps_per_launch: int):
 def maxval_absdiff(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:
     """MAXVAL(ABS(x - y)) without forming x - y."""
     res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
-    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce")
+    ws = workspace(reduce_workspace_size(x), x.tensor.device, "reduce", stream)
     _call("ftn_maxval_absdiff", x.ref(), y.ref(), ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
           ws.numel(), _stream(stream))
     return res
@@ -451,7 +456,7 @@ def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol
     """Jacobi to convergence (R#25): (sweeps done, last residual, result in unew)."""
     if coeff is None:
         coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
-    ws = workspace(reduce_workspace_size(u) + 64, u.tensor.device, "solve")
+    ws = workspace(reduce_workspace_size(u) + 64, u.tensor.device, "solve", stream)
     done, res, new = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
     _call("ftn_jacobi_solve", u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff,
           ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(done), ctypes.byref(res), ctypes.byref(new),
@@ -521,12 +526,12 @@ class Comm:
         """Halo exchange / interior sweep overlap in jacobi(): 0 off, 1 when nranks > 1, 2 always."""
         _call("ftn_comm_set_overlap", self.handle, mode)
 
-    def _ws(self, x: FArray) -> torch.Tensor:
-        return workspace(reduce_workspace_size(x) + 8 * (self.nranks + 1) + 64, x.tensor.device, "global")
+    def _ws(self, x: FArray, stream=None) -> torch.Tensor:
+        return workspace(reduce_workspace_size(x) + 8 * (self.nranks + 1) + 64, x.tensor.device, "global", stream)
 
     def _global(self, name, x: FArray, out=None, stream=None):
         res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
-        ws = self._ws(x)
+        ws = self._ws(x, stream)
         _call(name, self.handle, x.ref(), ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
               ws.numel(), _stream(stream))
         return res
@@ -542,7 +547,7 @@ class Comm:
 
     def dot_product(self, x, y, out=None, stream=None):
         res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
-        ws = self._ws(x)
+        ws = self._ws(x, stream)
         _call("ftn_dot_product_global", self.handle, x.ref(), y.ref(), ctypes.c_void_p(res.data_ptr()),
               ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
         return res
@@ -557,7 +562,7 @@ class Comm:
         return bool(r.value)
 
     def matmul(self, c_local: FArray, a_full: FArray, b_local: FArray, stream=None):
-        ws = workspace(matmul_workspace_size(c_local, a_full, b_local), c_local.tensor.device, "matmul")
+        ws = workspace(matmul_workspace_size(c_local, a_full, b_local), c_local.tensor.device, "matmul", stream)
         _call("ftn_matmul_colsharded", self.handle, c_local.ref(), a_full.ref(), b_local.ref(),
               ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
 

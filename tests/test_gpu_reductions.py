@@ -218,3 +218,17 @@ def test_more_than_2_32_elements(ftn):
         v = r.section((i + 1, i + 1), (j + 1, j + 1)).to_numpy().ravel()[0]
         m = t % 1024
         assert v == float(m * m + m), t
+
+
+def test_concurrent_streams_do_not_share_workspaces(ftn):
+    """Reductions issued on several streams at once get separate workspaces (the binding keys
+    them by stream): every result equals the serial one."""
+    xs = [ftn.FArray.empty((3 * 65536 + 77,)) for _ in range(4)]
+    for q, x in enumerate(xs):
+        ftn.gen_fill(x, synth.SEED, 30 + q, ftn.GEN_U11)
+    serial = [ftn.sum(x).item() for x in xs]
+    streams = [torch.cuda.Stream() for _ in xs]
+    for _ in range(3):
+        outs = [ftn.sum(x, stream=s) for x, s in zip(xs, streams)]
+        torch.cuda.synchronize()
+        assert [o.item() for o in outs] == serial
