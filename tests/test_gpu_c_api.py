@@ -1,0 +1,39 @@
+"""The C ABI from plain C (examples/c_api_demo.c, no Python in the loop): compiled with gcc
+against include/ftn.h and libftn.so, run, and its output compared with the oracle."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import FArray as OA
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_c_program_matches_oracle(tmp_path):
+    exe = tmp_path / "c_api_demo"
+    lib = os.path.join(ROOT, "paper_2409_18824_b200")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run(["gcc", "-O2", os.path.join(ROOT, "examples", "c_api_demo.c"), "-I", os.path.join(ROOT, "include"),
+                    "-I", os.path.join(cuda, "include"), "-L", lib, "-lftn", "-L", os.path.join(cuda, "lib64"),
+                    "-lcudart", f"-Wl,-rpath,{lib}", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", str(exe)],
+                   check=True)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    raw = out.read_bytes()
+    total = np.frombuffer(raw[:8], dtype=np.float64)[0]
+    in_unew = bool(np.frombuffer(raw[8:12], dtype=np.int32)[0])
+    n1, n2 = 300, 200
+    got = np.frombuffer(raw[12:], dtype=np.float64).reshape((n1, n2), order="F")
+    u0 = synth.jacobi_init((n1, n2))           # the same recipe as the C program
+    uo, wo = u0.copy(order="F"), u0.copy(order="F")
+    new = oracle.jacobi(OA(uo, [0, -5]), OA(wo, [0, -5]), 10, 0.25)
+    ref = wo if new else uo
+    assert in_unew == new
+    np.testing.assert_array_equal(got, ref)
+    assert total == oracle.reduce_orderR(OA(ref, [0, -5]).section((0, n1 - 1, 2), (-5, n2 - 6, 1)), oracle.SUM)
