@@ -362,7 +362,10 @@ __global__ void __launch_bounds__(MV_ROWS) matvec_kernel(const __grid_constant__
 #ifndef FTN_MV_U
 #define FTN_MV_U 8
 #endif
-constexpr int MV4_THREADS = 128, MV4_ROWS = 4 * MV4_THREADS, MV_U = FTN_MV_U;
+#ifndef FTN_MV4_THREADS
+#define FTN_MV4_THREADS 256  // 8192^2: 256 -> 5590, 128 -> 5000-5270, 512 -> 5130 GB/s
+#endif
+constexpr int MV4_THREADS = FTN_MV4_THREADS, MV4_ROWS = 4 * MV4_THREADS, MV_U = FTN_MV_U;
 
 __global__ void __launch_bounds__(MV4_THREADS) matvec_v4_kernel(const __grid_constant__ MVParams p) {
   __shared__ double xs[MV_MAXLC];
