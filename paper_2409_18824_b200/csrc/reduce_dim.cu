@@ -109,15 +109,25 @@ __global__ void __launch_bounds__(RB_WARPS * 32) reduce_dim_leading(const __grid
     rowbase[warp][lane] = p.x + mk0 * p.ks[0] + mk1 * p.ks[1];
     __syncwarp();
     T acc = init_val<T, KIND>();
-    for (int64_t j0 = 0; j0 < p.n; j0 += 32) {
-      const int64_t j = j0 + lane;
-      const bool jok = j < p.n;
-      T v[32];
+    // software pipeline: the 32 row loads of tile j0 + 32 are in flight while tile j0 is
+    // transposed through shared memory and folded (the fold order is unchanged)
+    T v[32];
+    {
+      const bool jok = lane < p.n;
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr)  // 32 independent coalesced row loads in flight
-        v[rr] = (rr < rows && jok) ? *reinterpret_cast<const T*>(rowbase[warp][rr] + j * p.step) : T(0);
+      for (int rr = 0; rr < 32; ++rr)
+        v[rr] = (rr < rows && jok) ? *reinterpret_cast<const T*>(rowbase[warp][rr] + (int64_t)lane * p.step) : T(0);
+    }
+    for (int64_t j0 = 0; j0 < p.n; j0 += 32) {
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) tile[warp][rr][lane] = v[rr];
+      {
+        const int64_t jn = j0 + 32 + lane;
+        const bool jok = jn < p.n;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)  // 32 independent coalesced row loads in flight
+          v[rr] = (rr < rows && jok) ? *reinterpret_cast<const T*>(rowbase[warp][rr] + jn * p.step) : T(0);
+      }
       __syncwarp();
       const int cnt = (int)min((int64_t)32, p.n - j0);
       if (cnt == 32) {
