@@ -118,9 +118,10 @@ __device__ __forceinline__ const char* addr(const KDesc& k, int64_t i0, int64_t 
   return k.base + i0 * k.sm[0] + i1 * k.sm[1] + i2 * k.sm[2];
 }
 
-// Steps 1-5 of order R for chunk blockIdx.x.  FLAT: the array is one contiguous
-// run (rank-1 after collapsing) with 32-byte aligned base.  VEC: groups never
-// straddle a row and rows are aligned, so each group is one vector load.
+// Steps 1-5 of order R for chunk blockIdx.x.  FLAT: every chunk is one contiguous, 32-byte
+// aligned run -- the array is one contiguous run after collapsing, or its (collapsed) rows are
+// unit-stride, a whole number of chunks long and aligned, as for a section of whole planes.
+// VEC: groups never straddle a row and rows are aligned, so each group is one vector load.
 template <typename T, int KIND, bool FLAT, bool VEC>
 __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant__ RParams p, void* out) {
   typedef typename Acc<T>::type A;
@@ -135,8 +136,13 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
 
   const int64_t g0 = start + R_GROUP * tau;
   if constexpr (FLAT) {
-    const T* xp = reinterpret_cast<const T*>(p.x.base);
-    const T* yp = reinterpret_cast<const T*>(p.y.base);
+    // chunk base pointers: element g of the chunk is xp[g - start]
+    const int64_t r0 = start % p.x.ext[0], rr = start / p.x.ext[0];
+    const int64_t r1 = rr % p.x.ext[1], r2 = rr / p.x.ext[1];
+    const T* xp = reinterpret_cast<const T*>(addr(p.x, r0, r1, r2));
+    const T* yp = KIND == RK_DOT || KIND == RK_MAXABSDIFF ? reinterpret_cast<const T*>(addr(p.y, r0, r1, r2))
+                                                          : nullptr;
+    const int64_t l0 = g0 - start;  // this thread's first group, relative to the chunk
     if (end - start == R_CHUNK) {
       constexpr int U = 8;
 #pragma unroll 1
@@ -144,9 +150,9 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
         T xv[U][R_GROUP], yv[U][R_GROUP];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          ld_group<T>(reinterpret_cast<const char*>(xp + g0 + 1024 * (m0 + u)), xv[u]);
+          ld_group<T>(reinterpret_cast<const char*>(xp + l0 + 1024 * (m0 + u)), xv[u]);
           if constexpr (KIND == RK_DOT || KIND == RK_MAXABSDIFF)
-            ld_group<T>(reinterpret_cast<const char*>(yp + g0 + 1024 * (m0 + u)), yv[u]);
+            ld_group<T>(reinterpret_cast<const char*>(yp + l0 + 1024 * (m0 + u)), yv[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -166,9 +172,10 @@ __global__ void __launch_bounds__(R_THREADS) reduce_chunks(const __grid_constant
         for (int v = 0; v < R_GROUP; ++v)
           if (g + v < end) {
             A e;
-            if constexpr (KIND == RK_DOT) e = __dmul_rn(xp[g + v], yp[g + v]);
-            else if constexpr (KIND == RK_MAXABSDIFF) e = fabs(__dsub_rn(xp[g + v], yp[g + v]));
-            else e = (A)xp[g + v];
+            const int64_t l = g + v - start;
+            if constexpr (KIND == RK_DOT) e = __dmul_rn(xp[l], yp[l]);
+            else if constexpr (KIND == RK_MAXABSDIFF) e = fabs(__dsub_rn(xp[l], yp[l]));
+            else e = (A)xp[l];
             acc[v] = combine<T, KIND>(acc[v], e);
           }
       }
@@ -325,8 +332,11 @@ ftn_status_t reduce_local(int kind, const ftn_desc_t* x, const ftn_desc_t* y, vo
     const int r2 = collapse(arr2, 2, kd);
     p.x = kd[0];
     p.y = kd[1];
-    const bool flat = r2 == 1 && p.x.sm[0] == el && p.y.sm[0] == el && ((uintptr_t)p.x.base % 32) == 0 &&
-                      ((uintptr_t)p.y.base % 32) == 0;
+    auto chunks_flat = [&](const KDesc& k) {
+      return k.sm[0] == el && ((uintptr_t)k.base % 32) == 0 &&
+             (r2 == 1 || ((k.ext[0] % R_CHUNK) == 0 && (k.sm[1] % 32) == 0 && (k.sm[2] % 32) == 0));
+    };
+    const bool flat = chunks_flat(p.x) && chunks_flat(p.y);
     const unsigned blocks = (unsigned)(p.nc > 0 ? p.nc : 1);
     void* out = p.nc > 1 ? ws : result;
     if (kind == RK_DOT) {
@@ -349,7 +359,9 @@ ftn_status_t reduce_local(int kind, const ftn_desc_t* x, const ftn_desc_t* y, vo
   const int r = collapse(arr, 1, &k);
   p.x = k;
   const int64_t va = R_GROUP * el;
-  const bool flat = r == 1 && k.sm[0] == el && ((uintptr_t)k.base % va) == 0;
+  // every chunk one aligned contiguous run (see reduce_chunks)
+  const bool flat = k.sm[0] == el && ((uintptr_t)k.base % 32) == 0 &&
+                    (r == 1 || ((k.ext[0] % R_CHUNK) == 0 && (k.sm[1] % 32) == 0 && (k.sm[2] % 32) == 0));
   const bool vec = k.sm[0] == el && (k.ext[0] % R_GROUP) == 0 && ((uintptr_t)k.base % va) == 0 &&
                    (k.sm[1] % va) == 0 && (k.sm[2] % va) == 0;
   switch (x->type) {
