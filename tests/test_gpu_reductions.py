@@ -232,3 +232,27 @@ def test_concurrent_streams_do_not_share_workspaces(ftn):
         outs = [ftn.sum(x, stream=s) for x, s in zip(xs, streams)]
         torch.cuda.synchronize()
         assert [o.item() for o in outs] == serial
+
+
+@pytest.mark.parametrize("kind", ["sum", "maxval", "absdiff"])
+def test_chunk_contiguous_sections(ftn, kind):
+    """Sections whose collapsed rows are whole multiples of the 65536-element chunk (every
+    other plane of a stack) take the 256-bit chunk path, one- and two-operand: bit-exact vs
+    order R on the oracle / exact max |x - y|."""
+    shape = (256, 512, 6)                                 # plane = 131072 elements = 2 chunks
+    a = synth.farray(shape, array_id=11, mode=synth.U11)
+    b = synth.farray(shape, array_id=12, mode=synth.U11)
+    A, B = ftn.FArray.from_numpy(a), ftn.FArray.from_numpy(b)
+    sec = ((1, 256), (1, 512), (1, 6, 2))
+    G = A.section(*sec)
+    O = OA(a).section((1, 256, 1), (1, 512, 1), (1, 6, 2))
+    if kind == "sum":
+        assert ftn.sum(G).item() == oracle.reduce_orderR(O, oracle.SUM)
+        packed = ftn.FArray.empty(G.shape)
+        ftn.assign(packed, G)
+        assert ftn.sum(G).item() == ftn.sum(packed).item()
+    elif kind == "maxval":
+        assert ftn.maxval(G).item() == oracle.maxval(O)
+    else:
+        got = ftn.maxval_absdiff(G, B.section(*sec)).item()
+        assert got == np.max(np.abs(a[:, :, ::2] - b[:, :, ::2]))
