@@ -208,3 +208,29 @@ def test_transpose_paper_size(ftn):
         row = r.section((c + 1, c + 1), (1, n)).to_numpy().ravel()      # r(c, :) = a(:, c)
         i = np.arange(n, dtype=np.int64)
         np.testing.assert_array_equal(row, ((i + n * c) % (1 << 32)).astype(np.uint32).view(np.int32))
+
+
+def test_matmul_ieee_specials(ftn):
+    """NaN and Inf propagate as IEEE arithmetic requires whatever the summation order: every
+    result element is classified (NaN / +Inf / -Inf / finite) exactly as by the oracle, and the
+    finite ones stay within the R#8 bound."""
+    m, k, n = 70, 90, 50
+    a = synth.farray((m, k), array_id=21, mode=synth.U11)
+    b = synth.farray((k, n), array_id=22, mode=synth.U11)
+    a[3, 5] = np.nan
+    a[10, 7] = np.inf
+    a[11, 7] = -np.inf
+    b[7, 4] = 0.0                       # Inf * 0 = NaN in column 4 of rows 10, 11
+    b[20, 9] = np.inf
+    a[40, 20] = -1.0                     # row 40, column 9: -Inf
+    A, B = ftn.FArray.from_numpy(a), ftn.FArray.from_numpy(b)
+    C = ftn.FArray.empty((m, n))
+    ftn.matmul(C, A, B)
+    got = C.to_numpy()
+    co, t = np.zeros((m, n), order="F"), np.zeros((m, n), order="F")
+    oracle.matmul(OA(co), OA(a), OA(b), OA(t))
+    for cls in (np.isnan, np.isposinf, np.isneginf):
+        np.testing.assert_array_equal(cls(got), cls(co))
+    fin = np.isfinite(co)
+    assert np.all(np.abs(got[fin] - co[fin]) <= 4 * k * U * t[fin])
+    assert np.isnan(got[3, 0]) and np.isnan(got[10, 4]) and np.isneginf(got[40, 9])
