@@ -22,6 +22,7 @@
 #include "ftn_internal.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace ftn {
@@ -38,7 +39,11 @@ namespace {
 #define FTN_AD_OJ 8
 #endif
 constexpr int AD_OK = FTN_AD_OK, AD_OJ = FTN_AD_OJ;  // output tile (k, j)
-constexpr int AD_PAIRS = AD_OK / 2;                 // threads per j row
+#ifndef FTN_AD_PP
+#define FTN_AD_PP 2
+#endif
+constexpr int AD_PP = FTN_AD_PP;                    // consecutive k points per thread (2 or 4)
+constexpr int AD_PAIRS = AD_OK / AD_PP;             // threads per j row
 constexpr int AD_BK = AD_OK + 4, AD_BJ = AD_OJ + 2;  // box 132 x 10: k-2 .. k+129, j-1 .. j+8
 constexpr int AD_FIELD = (AD_BK * AD_BJ * 8 + 127) / 128 * 128;  // 9856 B per field box
 constexpr int AD_SLOT = 3 * AD_FIELD;
@@ -154,8 +159,8 @@ struct SmemPair {
   int row0;             // element offset of the thread's row (j) and pair L in a field box
   __device__ __forceinline__ double operator()(int f, int dk, int dj, int di) const {
     const double2* seg = reinterpret_cast<const double2*>(pl[di + 1] + f * (AD_FIELD / 8) + row0 + dj * AD_BK);
-    const int m = E + dk;
-    return m == -1 ? seg[0].y : m == 0 ? seg[1].x : m == 1 ? seg[1].y : seg[2].x;
+    const int m = E + dk + 2;  // element index from the L pair; pair m / 2, component m % 2
+    return (m & 1) ? seg[m >> 1].y : seg[m >> 1].x;
   }
 };
 
@@ -187,48 +192,66 @@ __global__ void __launch_bounds__(AD_THREADS, 1) adv_tma_kernel(const __grid_con
   for (uint32_t u = blockIdx.x; u < p.units; u += gridDim.x) {
     int k0, j0, ia, ib;
     adv_unit(p, u, k0, j0, ia, ib);
-    const int k = k0 + 2 * lane;
-    const bool in0 = k >= 1 && k <= p.nz - 2, in1 = k + 1 >= 1 && k + 1 <= p.nz - 2;
-    const int kc0 = in0 ? k : 1, kc1 = in1 ? k + 1 : 1;
-    const double c1a = tz_at(p, 0, kc0), c2a = tz_at(p, 1, kc0), d1a = tz_at(p, 2, kc0), d2a = tz_at(p, 3, kc0);
-    const double c1b = tz_at(p, 0, kc1), c2b = tz_at(p, 1, kc1), d1b = tz_at(p, 2, kc1), d2b = tz_at(p, 3, kc1);
+    const int k = k0 + AD_PP * lane;
     const int j = j0 + jr;
     const bool jin = j <= p.ny - 2;
-    const bool st0 = jin && in0, st1 = jin && in1;
+    double cz[AD_PP][4];
+    bool st[AD_PP];
+    bool all_st = jin;
+#pragma unroll
+    for (int e = 0; e < AD_PP; ++e) {
+      const bool in = k + e >= 1 && k + e <= p.nz - 2;
+      const int kc = in ? k + e : 1;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) cz[e][q4] = tz_at(p, q4, kc);
+      st[e] = jin && in;
+      all_st = all_st && in;
+    }
     const int np = ib - ia + 2;  // planes ia-1 .. ib
     for (int q = 0; q < np; ++q) {
       const uint32_t gq = g + q;
       dev::mbar_wait(&full[gq % AD_NS], (gq / AD_NS) & 1);
       if (q >= 2) {  // output plane i from planes i-1, i, i+1 (steps q-2, q-1, q)
         const int i = ia + q - 2;
-        SmemPair<0> F0;
-        SmemPair<1> F1;
-        F0.pl[0] = F1.pl[0] = base + ((gq - 2) % AD_NS) * (AD_SLOT / 8);
-        F0.pl[1] = F1.pl[1] = base + ((gq - 1) % AD_NS) * (AD_SLOT / 8);
-        F0.pl[2] = F1.pl[2] = base + (gq % AD_NS) * (AD_SLOT / 8);
-        F0.row0 = F1.row0 = (jr + 1) * AD_BK + 2 * lane;
-        double su0, sv0, sw0, su1, sv1, sw1;
-        adv_point(F0, c1a, c2a, d1a, d2a, p.tcx, p.tcy, su0, sv0, sw0);
-        adv_point(F1, c1b, c2b, d1b, d2b, p.tcx, p.tcy, su1, sv1, sw1);
+        const double* pl0 = base + ((gq - 2) % AD_NS) * (AD_SLOT / 8);
+        const double* pl1 = base + ((gq - 1) % AD_NS) * (AD_SLOT / 8);
+        const double* pl2 = base + (gq % AD_NS) * (AD_SLOT / 8);
+        const int row0 = (jr + 1) * AD_BK + AD_PP * lane;
+        double su[AD_PP], sv[AD_PP], sw[AD_PP];
+        auto point = [&](auto E_) {
+          constexpr int E = decltype(E_)::value;
+          SmemPair<E> F;
+          F.pl[0] = pl0;
+          F.pl[1] = pl1;
+          F.pl[2] = pl2;
+          F.row0 = row0;
+          adv_point(F, cz[E][0], cz[E][1], cz[E][2], cz[E][3], p.tcx, p.tcy, su[E], sv[E], sw[E]);
+        };
+        point(std::integral_constant<int, 0>{});
+        point(std::integral_constant<int, 1>{});
+        if constexpr (AD_PP == 4) {
+          point(std::integral_constant<int, 2>{});
+          point(std::integral_constant<int, 3>{});
+        }
         const int64_t ok = (int64_t)k, oj = (int64_t)j, oi = (int64_t)i;
         char* a0 = p.su.base + ok * p.su.sm1 + oj * p.su.sm2 + oi * p.su.sm3;
         char* a1 = p.sv.base + ok * p.sv.sm1 + oj * p.sv.sm2 + oi * p.sv.sm3;
         char* a2 = p.sw.base + ok * p.sw.sm1 + oj * p.sw.sm2 + oi * p.sw.sm3;
-        if (p.vec_out && st0 && st1) {
-          *reinterpret_cast<double2*>(a0) = make_double2(su0, su1);
-          *reinterpret_cast<double2*>(a1) = make_double2(sv0, sv1);
-          *reinterpret_cast<double2*>(a2) = make_double2(sw0, sw1);
+        if (p.vec_out && all_st) {
+#pragma unroll
+          for (int e = 0; e < AD_PP; e += 2) {
+            *reinterpret_cast<double2*>(a0 + e * 8) = make_double2(su[e], su[e + 1]);
+            *reinterpret_cast<double2*>(a1 + e * 8) = make_double2(sv[e], sv[e + 1]);
+            *reinterpret_cast<double2*>(a2 + e * 8) = make_double2(sw[e], sw[e + 1]);
+          }
         } else {
-          if (st0) {
-            *reinterpret_cast<double*>(a0) = su0;
-            *reinterpret_cast<double*>(a1) = sv0;
-            *reinterpret_cast<double*>(a2) = sw0;
-          }
-          if (st1) {
-            *reinterpret_cast<double*>(a0 + p.su.sm1) = su1;
-            *reinterpret_cast<double*>(a1 + p.sv.sm1) = sv1;
-            *reinterpret_cast<double*>(a2 + p.sw.sm1) = sw1;
-          }
+#pragma unroll
+          for (int e = 0; e < AD_PP; ++e)
+            if (st[e]) {
+              *reinterpret_cast<double*>(a0 + e * p.su.sm1) = su[e];
+              *reinterpret_cast<double*>(a1 + e * p.sv.sm1) = sv[e];
+              *reinterpret_cast<double*>(a2 + e * p.sw.sm1) = sw[e];
+            }
         }
       }
       __syncthreads();
