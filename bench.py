@@ -259,6 +259,59 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         rows[name] = {"value": gbs, "unit": "GB/s", "ms": t / steps * 1e3,
                       "roofline": {"bound": "hbm", "frac": gbs / N / hbm_peak}}
 
+    # C1: real(8) a(0:63,1:48) = its 0-based offset, s = a(::2,:); latency of each call (median of
+    # 1000, CUDA events around the call: host launch overhead included) and the closed forms of
+    # SURVEY §8(c.4) checked on the results (not a roofline case: 24 KiB)
+    if "c1" in args.rows and N == 1:
+        a = ftn.FArray.empty((64, 48), lbounds=[0, 1])
+        ftn.gen_fill(a, SEED, 0, ftn.GEN_LINEAR)          # a(i,j) = i + 64(j-1)
+        s = a.section((0, 63, 2), (1, 48))
+        c = a.section((1, 63, 2), (1, 48))
+        e = ftn.FArray.empty((32, 48), lbounds=[-5, 10])
+        ftn.gen_fill(e, SEED, 1, ftn.GEN_U01)
+        r = ftn.FArray.empty((32, 48))
+        st = ftn.FArray.empty((48, 32))
+        m48 = ftn.FArray.empty((48, 48))
+        b48 = [ftn.FArray.empty((48, 48)) for _ in range(2)]
+        for q, x in enumerate(b48):
+            ftn.gen_fill(x, SEED, 2 + q, ftn.GEN_U11)
+        out = torch.empty((), dtype=torch.float64, device="cuda")
+        ops = {"muladd_r=s*c+d": lambda: ftn.muladd(r, s, c, e),
+               "sum_s": lambda: ftn.sum(s, out),
+               "maxval_s": lambda: ftn.maxval(s, out),
+               "minval_s": lambda: ftn.minval(s, out),
+               "transpose_s": lambda: ftn.transpose(st, s),
+               "matmul_transpose(s)_s_48x48x32": lambda: ftn.matmul(m48, s, s, transpose_a=True),
+               "matmul_48^3": lambda: ftn.matmul(m48, b48[0], b48[1])}
+        lat = {}
+        for name, fn in ops.items():
+            for _ in range(20):
+                fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(1000):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+            ts.sort()
+            lat[name] = round(ts[len(ts) // 2], 2)
+        # closed forms: SUM(s) = 2357760, MAXVAL = 3070 (s holds the even i),
+        # MINVAL = 0; MATMUL(TRANSPOSE(s), s)(p,q) = 41664 + 63488(p+q-2) + 131072(p-1)(q-1)
+        checks = {"sum": ftn.sum(s).item() == 2357760.0, "maxval": ftn.maxval(s).item() == 3070.0,
+                  "minval": ftn.minval(s).item() == 0.0}
+        ftn.matmul(m48, s, s, transpose_a=True)
+        p_ = torch.arange(1, 49, dtype=torch.float64, device="cuda")
+        cf = 41664 + 63488 * (p_[:, None] + p_[None, :] - 2) + 131072 * (p_[:, None] - 1) * (p_[None, :] - 1)
+        checks["matmul_transpose"] = bool(torch.equal(m48.tensor, cf))
+        ftn.transpose(st, s)
+        checks["transpose"] = bool(torch.equal(st.tensor, s.view_tensor().t()))
+        rows["c1_latency"] = {"value": lat["sum_s"], "unit": "us (median of 1000, SUM(a(::2,:)))",
+                              "latency_us": lat, "closed_forms_ok": checks}
+        del a, s, c, e, r, st, m48, b48
+
     # C4: 1024^3 arrays x(-511:512, 0:1023, 1:1024); at N>1 slabs of 1024/N planes (strong scaling)
     if "c4" in args.rows:
         nk = 1024 // N
@@ -303,6 +356,19 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             gbs_row("c4_section_sum", 8 * n_el, lambda: ftn.sum(secs[0], out))
         del parents, secs
         torch.cuda.empty_cache()
+        # dim-1-strided variant: parents (0:2047,1024,1024/N), sections (0:2047:2,:,:):
+        # every 32-byte sector carries 2 used elements of 4, so DRAM moves ~2x the algorithmic bytes
+        if N == 1:
+            parents = [ftn.FArray.empty((2048, 1024, nk), lbounds=[0, 1, 1]) for _ in range(4)]
+            for k, p in enumerate(parents):
+                ftn.gen_fill(p, SEED, 30 + k, ftn.GEN_U01)
+            secs = [p.section((0, 2047, 2), (1, 1024), (1, nk)) for p in parents]
+            gbs_row("c4_dim1_strided_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2]))
+            gbs_row("c4_dim1_strided_sum", 8 * n_el, lambda: ftn.sum(secs[0], out))
+            for nm in ("c4_dim1_strided_muladd", "c4_dim1_strided_sum"):
+                rows[nm]["roofline"]["note"] = "sector-limited: 2 of every 4 elements of a 32-byte sector are used"
+            del parents, secs
+            torch.cuda.empty_cache()
 
     # C3: MATMUL 8192^3, column blocks of b and c over the ranks (a replicated)
     if "c3" in args.rows:
@@ -369,6 +435,17 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                                      "roofline": {"bound": "fp64 tensor (DMMA)", "frac": tf / FP64_PEAK_TFLOPS}}
         del A, B, C
         torch.cuda.empty_cache()
+        # jacobi 1024^2 x 10^5 sweeps: the 16 MiB working set stays in L2, so GLUPS only (no HBM fraction)
+        nj, sw = 1024, 100000
+        U, W = ftn.FArray.empty((nj, nj)), ftn.FArray.empty((nj, nj))
+        ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
+        jacobi_faces(ftn, U, nj, nj)
+        ftn.assign(W, U)
+        t = timed(torch, lambda: ftn.jacobi(U, W, sw), 1, 1, None, None)
+        rows["paper_jacobi_1024_1e5"] = {"value": (nj - 2) ** 2 * sw / t / 1e9, "unit": "GLUPS", "ms": t * 1e3,
+                                         "roofline": {"bound": "l2-resident (16 MiB working set): not an HBM case",
+                                                      "frac": None}}
+        del U, W
 
     # C5: 3-D 7-point Jacobi 2048^3 (slabs of 2048/N planes + halos at N > 1), 100 sweeps per step
     # (an even number of 2-sweep launches, so no single sweep in the plan)
@@ -512,7 +589,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
-    ap.add_argument("--rows", default="c4,c3,paper,c5,f4", help="comma list of extra rows, or 'none'")
+    ap.add_argument("--rows", default="c1,c4,c3,paper,c5,f4", help="comma list of extra rows, or 'none'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")

@@ -241,6 +241,18 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
 
+/* Tuning (not semantics), opt-in: a rank-2 grid small enough for the aggregate shared memory
+ * of the GPU (both iterates of a 1/num_SMs row slab plus K halo rows per side in <= 227 KB per
+ * SM, e.g. the paper's 1024 x 1024) can be advanced by ftn_jacobi in ONE cooperative
+ * launch when sweeps >= min_sweeps: each CTA keeps its rows resident, runs K
+ * sweeps between exchanges of K boundary rows with its two neighbours only (flags in global
+ * memory, no grid barrier).  Bit-identical results; the result array as for ftn_jacobi, the
+ * other array holds iterate sweeps-1.  min_sweeps = 0 disables the path (the default, or
+ * FTN_JACOBI_RES_MIN: on B200 it is slower than the streaming kernels at 1024^2, §4.6);
+ * halo_depth K in 1..8, or 0 for the largest K <= 4 that fits.  Process-wide.  FTN_ERR_SHAPE
+ * for a negative min_sweeps or K outside 0..8. */
+ftn_status_t ftn_jacobi_set_resident(int64_t min_sweeps, int32_t halo_depth);
+
 /* ftn_jacobi with the data on the host: host_u -> u (host-to-device copy), u -> unew
  * (device copy, presets the boundary of unew), `sweeps` sweeps, then the result -> host_result
  * (device-to-host copy), all enqueued on `stream` in that order.  host_u and host_result are

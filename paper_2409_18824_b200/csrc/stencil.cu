@@ -49,6 +49,10 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 }
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
+bool jacobi2d_resident_fits(const ftn_desc_t* u);
+int64_t jacobi_resident_min();
+ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
+                                   cudaStream_t s);
 ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s);
 ftn_status_t jacobi3d_fused2_planes(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t plane_lo,
                                     int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
@@ -595,6 +599,16 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     FTN_CHECK(make_stencil_map(&mw, unew));
   }
   const int64_t nlast = u->dim[u->rank - 1].extent;
+  // Opt-in (ftn_jacobi_set_resident): grids that fit the aggregate shared memory (e.g. the
+  // paper's 1024^2), all sweeps in one cooperative launch with neighbour-only synchronisation
+  // (stencil_res.cu); same results, same result array, the other array holds iterate
+  // sweeps-1 as after the swapped DO nest.
+  const int64_t res_min = jacobi_resident_min();
+  if (u->rank == 2 && res_min > 0 && sweeps >= res_min && jacobi2d_resident_fits(u)) {
+    FTN_CHECK(jacobi2d_resident_run(u, unew, sweeps, coeff, s));
+    if (result_in_unew) *result_in_unew = (int32_t)(sweeps & 1);
+    return FTN_OK;
+  }
   // Arrays the TMA kernels cannot address (odd leading dimension, sections with a non-unit
   // first stride or unaligned strides): for enough sweeps, run the temporally blocked kernels
   // on padded packed copies (copy both arrays in, the sweeps, copy both back: 4 extra passes

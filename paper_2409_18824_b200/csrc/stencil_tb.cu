@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_
       L[t][sm][1] = v1;
     };
     auto chunk = [&](const double* st, int s0, bool fastpath) {
+      char* orow = outp + (int64_t)(s0 - (C::LAG + 1) * T) * p.d_sm2;  // formed, stored only when ok
 #pragma unroll
       for (int rr = 0; rr < WF_R; ++rr) {
         const int s = s0 + rr;
@@ -247,12 +248,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_
           L[0][sl0][0] = in0;
           L[0][sl0][1] = in1;
         }
-        // level T row s - LAG*T is output row ja + (s - (LAG+1)T) when (LAG+1)T <= s < nr + (LAG-1)T
+        // level T row s - LAG*T is output row ja + (s - (LAG+1)T) when (LAG+1)T <= s < nr + (LAG-1)T;
+        // the destination has unit stride in dim 1 (TMA-able, checked on the host): the
+        // lane's second column is at +8 bytes.  The fast path only runs on chunks whose rows
+        // are all stored, so its stores need no row test and walk a row pointer.
         const int so = ((rr - C::LAG * T) % 3 + 3) % 3;
         const bool ok = s >= (C::LAG + 1) * T && s < nri + C::EXTRA;
-        char* o = outp + (int64_t)(s - (C::LAG + 1) * T) * p.d_sm2;
-        if (ok && store[0]) *reinterpret_cast<double*>(o) = L[T][so][0];
-        if (ok && store[1]) *reinterpret_cast<double*>(o + p.d_sm1) = L[T][so][1];
+        if (ok && store[0]) *reinterpret_cast<double*>(orow) = L[T][so][0];
+        if (ok && store[1]) *reinterpret_cast<double*>(orow + 8) = L[T][so][1];
+        orow += p.d_sm2;
       }
     };
     for (int64_t q = 0; q < nch; ++q, ++k) {
@@ -297,6 +301,7 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     FTN_CUDA(cudaFuncSetAttribute(jacobi2d_wf<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr[dev & 63] = true;
   }
+  if (dst->dim[0].sm != 8) return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_wf: destination must have unit stride in dim 1");
   CUtensorMap m;
   uint64_t dims[2] = {(uint64_t)src->dim[0].extent, (uint64_t)src->dim[1].extent};
   uint64_t strides[1] = {(uint64_t)src->dim[1].sm};

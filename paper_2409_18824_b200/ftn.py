@@ -104,6 +104,7 @@ def _load():
         "ftn_bcast": [vp, P, ctypes.c_int32, vp],
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
         "ftn_jacobi_set_fusion": [ctypes.c_int32],
+        "ftn_jacobi_set_resident": [ctypes.c_int64, ctypes.c_int32],
         "ftn_jacobi_host": [vp, vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_pw_advection": [P, P, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_double, vp],
     }
@@ -438,8 +439,14 @@ def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FA
 
 
 def jacobi_set_fusion(sweeps_per_launch: int):
-    """Temporal-blocking factor of the 2-D Jacobi kernels (1..4, default 4); results are identical."""
+    """Temporal-blocking factor of the Jacobi kernels (1..6, default 5; 3-D uses min(T, 2)); results are identical."""
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
+
+
+def jacobi_set_resident(min_sweeps: int, halo_depth: int = 0):
+    """SMEM-resident Jacobi for small rank-2 grids (one cooperative launch for all sweeps) when
+    sweeps >= min_sweeps (0 disables); halo_depth K = sweeps per neighbour exchange (0: auto)."""
+    _call("ftn_jacobi_set_resident", ctypes.c_int64(min_sweeps), halo_depth)
 
 
 def maxval_absdiff(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:

@@ -19,6 +19,15 @@ def ftn():
     return ftn
 
 
+@pytest.fixture
+def streaming(ftn):
+    """The streaming (temporally blocked) kernels only: the SMEM-resident path for small grids
+    (tests/test_gpu_jacobi_resident.py) is switched off for the test."""
+    ftn.jacobi_set_resident(0)
+    yield
+    ftn.jacobi_set_resident(0)
+
+
 def _run_both(ftn, u0, sweeps, coeff, lbs=None):
     U, W = ftn.FArray.from_numpy(u0, lbs), ftn.FArray.from_numpy(u0, lbs)
     in_new = ftn.jacobi(U, W, sweeps, coeff)
@@ -133,7 +142,7 @@ def test_c2_full_size_sampled(ftn):
 @pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("shape", [(3, 3), (5, 40), (40, 5), (129, 31), (200, 301), (257, 77), (1000, 130)])
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 7, 8, 9])
-def test_2d_temporal_blocking(ftn, T, shape, sweeps):
+def test_2d_temporal_blocking(ftn, streaming, T, shape, sweeps):
     """Fused launches of T sweeps are bit-identical to the oracle's
     sweep-by-sweep DO nest, and the result lands where the sweep parity says."""
     ftn.jacobi_set_fusion(T)
@@ -288,7 +297,7 @@ def test_error_paths_launch_nothing(ftn):
     np.testing.assert_array_equal(W.to_numpy(), u0)
 
 
-def test_random_shapes_fusions_and_sweeps(ftn):
+def test_random_shapes_fusions_and_sweeps(ftn, streaming):
     """Fuzz: random 2-D / 3-D shapes, lower bounds, sweep counts and fusion settings, all
     bit-identical to the oracle (covers unit / segment / strip remainders the fixed cases miss)."""
     rng = np.random.default_rng(2409)
