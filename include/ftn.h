@@ -207,6 +207,11 @@ ftn_status_t ftn_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
  * SURVEY §8(f) f3).  Workspace: ftn_matmul_ex_workspace_size. */
 #define FTN_MATMUL_TRANSPOSE_A 1u
 #define FTN_MATMUL_TRANSPOSE_B 2u
+/* Small rank-2 products (M*N*K <= 2^21, K <= 4096, e.g. C1's 48 x 48 x 32) run one thread per
+ * c(i,j) folding l = 1..K in order with one rounding per product and per sum (the literal
+ * definition: bit-identical to a sequential fold; no packing, any strides); the DMMA path
+ * serves the rest.  FTN_MATMUL_FORCE_DMMA (tuning / testing) takes the DMMA path always. */
+#define FTN_MATMUL_FORCE_DMMA 4u
 ftn_status_t ftn_matmul_ex_workspace_size(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b,
                                           uint32_t flags, size_t* bytes);
 ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, uint32_t flags,

@@ -266,9 +266,59 @@ ftn_status_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const MPa
   return after_launch("dmma_gemm_kernel");
 }
 
+// Small products (M*N*K <= 2^21, e.g. C1's 48 x 48 x 32): one thread per c(i, j) folding
+// l = 1..K in ascending order with one rounding per product and per sum -- the literal
+// definition (F2018 16.9.124) and therefore bit-identical to the oracle's
+// sequential fold; no packing, any strides (op = TRANSPOSE by swapping a's or b's strides).
+// A DMMA tile pipeline has nothing to amortise its TMA / mbarrier latency over at this size.
+struct SmallMM {
+  const char* a;
+  int64_t a_si, a_sl;  // byte strides of op(a) along i and l
+  const char* b;
+  int64_t b_sl, b_sj;  // byte strides of op(b) along l and j
+  char* c;
+  int64_t c_si, c_sj;
+  int64_t M, N, K;
+};
+
+__global__ void __launch_bounds__(256) small_matmul_kernel(const __grid_constant__ SmallMM p) {
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t >= p.M * p.N) return;
+  const int64_t i = t % p.M, j = t / p.M;
+  const char* ap = p.a + i * p.a_si;
+  const char* bp = p.b + j * p.b_sj;
+  double s = 0.0;
+#pragma unroll 8
+  for (int64_t l = 0; l < p.K; ++l)
+    s = __dadd_rn(s, __dmul_rn(*reinterpret_cast<const double*>(ap + l * p.a_sl),
+                               *reinterpret_cast<const double*>(bp + l * p.b_sl)));
+  *reinterpret_cast<double*>(p.c + i * p.c_si + j * p.c_sj) = s;
+}
+
+bool small_matmul(int64_t M, int64_t N, int64_t K) { return M * N * K <= (1ll << 21) && K <= 4096; }
+
+ftn_status_t run_small_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb,
+                              int64_t M, int64_t N, int64_t K, cudaStream_t s) {
+  SmallMM p;
+  p.a = (const char*)a->base_addr;
+  p.a_si = ta ? a->dim[1].sm : a->dim[0].sm;
+  p.a_sl = ta ? a->dim[0].sm : a->dim[1].sm;
+  p.b = (const char*)b->base_addr;
+  p.b_sl = tb ? b->dim[1].sm : b->dim[0].sm;
+  p.b_sj = tb ? b->dim[0].sm : b->dim[1].sm;
+  p.c = (char*)c->base_addr;
+  p.c_si = c->dim[0].sm;
+  p.c_sj = c->dim[1].sm;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  small_matmul_kernel<<<(unsigned)((M * N + 255) / 256), 256, 0, s>>>(p);
+  return after_launch("small_matmul_kernel");
+}
+
 // c = MATMUL(op(a), op(b)), op = TRANSPOSE when ta / tb.  op(a) is (M, K), op(b) is (K, N).
 ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool force_dmma = false) {
   const int64_t M = ta ? a->dim[1].extent : a->dim[0].extent;
   const int64_t K = ta ? a->dim[0].extent : a->dim[1].extent;
   const int64_t N = tb ? b->dim[0].extent : b->dim[1].extent;
@@ -277,6 +327,7 @@ ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
     const double zero = 0.0;
     return ftn_fill(c, &zero, s);
   }
+  if (!force_dmma && small_matmul(M, N, K)) return run_small_matmul(c, a, b, ta, tb, M, N, K, s);
   ftn_desc_t ap = *a, bp = *b;
   char* w = ws;
   if (!tma_able(a)) {
@@ -642,12 +693,12 @@ size_t ws_bytes_for(const ftn_desc_t* a, const ftn_desc_t* b) {
 }
 
 ftn_status_t dispatch(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool force_dmma = false) {
   switch (form_of(a, b)) {
     case 1: return run_matvec(c, a, b, ws, s);
     case 2: return run_vecmat(c, a, b, s);
   }
-  return run_matmul(c, a, b, ta, tb, ws, s);
+  return run_matmul(c, a, b, ta, tb, ws, s, force_dmma);
 }
 
 }  // namespace
@@ -658,15 +709,16 @@ ftn_status_t matmul_local_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn
                              size_t ws_bytes, cudaStream_t s) {
   NvtxRange nvtx_("ftn_matmul");
   const bool ta = flags & FTN_MATMUL_TRANSPOSE_A, tb = flags & FTN_MATMUL_TRANSPOSE_B;
+  const bool force = flags & FTN_MATMUL_FORCE_DMMA;
   const size_t need = ws_bytes_for(a, b);
   if (need > 512 && (!ws || ws_bytes < need))
     return fail(FTN_ERR_WORKSPACE, "ftn_matmul: workspace too small (see ftn_matmul_workspace_size)");
-  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return dispatch(c, a, b, ta, tb, (char*)ws, s);
+  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return dispatch(c, a, b, ta, tb, (char*)ws, s, force);
   StreamTemp tmp;  // R#5: the product is formed before c is defined
   FTN_CHECK(tmp.alloc((size_t)desc_size(c) * 8, s));
   ftn_desc_t t;
   FTN_CHECK(make_packed(&t, tmp.ptr, c));
-  FTN_CHECK(dispatch(&t, a, b, ta, tb, (char*)ws, s));
+  FTN_CHECK(dispatch(&t, a, b, ta, tb, (char*)ws, s, force));
   return launch_copy(c, &t, s);
 }
 
@@ -683,7 +735,7 @@ ftn_status_t check_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_de
   FTN_CHECK(check_desc(b, "ftn_matmul(b)", 1, 2));
   if (a->type != FTN_F64 || b->type != FTN_F64 || c->type != FTN_F64)
     return fail(FTN_ERR_TYPE, "ftn_matmul: real(8) operands only");
-  if (flags & ~(uint32_t)(FTN_MATMUL_TRANSPOSE_A | FTN_MATMUL_TRANSPOSE_B))
+  if (flags & ~(uint32_t)(FTN_MATMUL_TRANSPOSE_A | FTN_MATMUL_TRANSPOSE_B | FTN_MATMUL_FORCE_DMMA))
     return fail(FTN_ERR_UNSUPPORTED, "ftn_matmul: unknown flags");
   const bool ta = flags & FTN_MATMUL_TRANSPOSE_A, tb = flags & FTN_MATMUL_TRANSPOSE_B;
   if ((ta && a->rank != 2) || (tb && b->rank != 2))

@@ -391,10 +391,12 @@ def matmul_workspace_size(c: FArray, a: FArray, b: FArray) -> int:
     return n.value
 
 
-def matmul(c: FArray, a: FArray, b: FArray, transpose_a: bool = False, transpose_b: bool = False, stream=None):
+def matmul(c: FArray, a: FArray, b: FArray, transpose_a: bool = False, transpose_b: bool = False, stream=None,
+           force_dmma: bool = False):
     """c = MATMUL(a, b); with transpose_a / transpose_b: MATMUL(TRANSPOSE(a), ...) without a copy.
-    Rank-1 operands give the matrix-vector / vector-matrix forms."""
-    flags = (1 if transpose_a else 0) | (2 if transpose_b else 0)
+    Rank-1 operands give the matrix-vector / vector-matrix forms.  Small rank-2 products run the
+    sequential-fold kernel unless force_dmma (FTN_MATMUL_FORCE_DMMA) asks for the DMMA path."""
+    flags = (1 if transpose_a else 0) | (2 if transpose_b else 0) | (4 if force_dmma else 0)
     if flags:
         n = ctypes.c_size_t()
         _call("ftn_matmul_ex_workspace_size", c.ref(), a.ref(), b.ref(), flags, ctypes.byref(n))

@@ -69,15 +69,22 @@ def test_transpose_int32_large(ftn):
     np.testing.assert_array_equal(t, (i + n1 * j).astype(np.int32))
 
 
-def _mm_check(ftn, a, b, lba=(1, 1), lbb=(1, 1), exact=False, csec=None):
+def _small(m, n, k):
+    """ftn_matmul's small-product rule (matmul.cu small_matmul): the sequential-fold kernel."""
+    return m * n * k <= (1 << 21) and k <= 4096
+
+
+def _mm_check(ftn, a, b, lba=(1, 1), lbb=(1, 1), exact=False, csec=None, force_dmma=False):
     m, k = a.shape
     n = b.shape[1]
     A, B = ftn.FArray.from_numpy(a, lba), ftn.FArray.from_numpy(b, lbb)
     C = ftn.FArray.empty((m, n))
-    ftn.matmul(C, A, B)
+    ftn.matmul(C, A, B, force_dmma=force_dmma)
     co, t = np.zeros((m, n), order="F"), np.zeros((m, n), order="F")
     oracle.matmul(OA(co), OA(a, lba), OA(b, lbb), OA(t))
     got = C.to_numpy()
+    if not force_dmma and _small(m, n, k):
+        exact = True              # the sequential fold IS the oracle's order: bit-identical
     if exact:
         np.testing.assert_array_equal(got, co)
     else:
@@ -87,18 +94,53 @@ def _mm_check(ftn, a, b, lba=(1, 1), lbb=(1, 1), exact=False, csec=None):
 
 @pytest.mark.parametrize("mnk", [(1, 1, 1), (2, 3, 5), (16, 8, 4), (33, 17, 65), (48, 48, 48), (128, 128, 32),
                                  (129, 127, 33), (127, 129, 31), (200, 300, 100), (255, 257, 97), (512, 384, 640)])
-def test_matmul_random(ftn, mnk):
+@pytest.mark.parametrize("force_dmma", [False, True])
+def test_matmul_random(ftn, mnk, force_dmma):
     m, n, k = mnk
-    _mm_check(ftn, synth.farray((m, k), array_id=1, mode=synth.U11), synth.farray((k, n), array_id=2, mode=synth.U11))
+    _mm_check(ftn, synth.farray((m, k), array_id=1, mode=synth.U11), synth.farray((k, n), array_id=2, mode=synth.U11),
+              force_dmma=force_dmma)
 
 
-def test_matmul_small_grid_all(ftn):
-    """(m, n, k) over a sweep of small sizes around the m16n8k4 and 128-tile edges."""
+@pytest.mark.parametrize("force_dmma", [False, True])
+def test_matmul_small_grid_all(ftn, force_dmma):
+    """(m, n, k) over a sweep of small sizes around the m16n8k4 and 128-tile edges; the
+    sequential-fold kernel bit-identical to the oracle, the forced DMMA path within the bound."""
     for m in (1, 7, 16, 17, 33):
         for n in (1, 8, 9, 31):
             for k in (1, 3, 4, 5, 32, 33):
                 _mm_check(ftn, synth.farray((m, k), array_id=m, mode=synth.U11),
-                          synth.farray((k, n), array_id=n + 100, mode=synth.U11))
+                          synth.farray((k, n), array_id=n + 100, mode=synth.U11), force_dmma=force_dmma)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_small_matmul_sections_transposes_bit_exact(ftn, ta, tb):
+    """The small-product kernel on strided / reversed sections with lbounds and TRANSPOSE flags:
+    bit-identical to the oracle's sequential fold of MATMUL(op(a), op(b)) formed explicitly."""
+    rng = np.random.default_rng(11 + 2 * ta + tb)
+    pa = np.asfortranarray(rng.uniform(-1, 1, (61, 47)))
+    pb = np.asfortranarray(rng.uniform(-1, 1, (53, 59)))
+    A, B = ftn.FArray.from_numpy(pa, [-3, 2]), ftn.FArray.from_numpy(pb, [0, 0])
+    As = A.section((55, -3, -2), (2, 48, 2))            # 30 x 24
+    Bs = B.section((0, 48, 2), (58, 0, -2))             # 25 x 30
+    a_op = np.asfortranarray(pa[58::-2, 0:47:2])         # As as numpy (30 x 24)
+    b_op = np.asfortranarray(pb[0:49:2, 58::-2])         # Bs as numpy (25 x 30)
+    # op(a) (m x k) and op(b) (k x n) with a common k; a / b are stored transposed when flagged
+    k = 24
+    a_mat = np.asfortranarray(a_op[:, :k])               # 30 x 24
+    b_mat = np.asfortranarray(b_op[:k, :])               # 24 x 30
+    Am, Bm = ftn.FArray.from_numpy(a_mat.T if ta else a_mat), ftn.FArray.from_numpy(b_mat.T if tb else b_mat)
+    C = ftn.FArray.empty((a_mat.shape[0], b_mat.shape[1]))
+    ftn.matmul(C, Am, Bm, transpose_a=ta, transpose_b=tb)
+    co, t = np.zeros(C.shape, order="F"), np.zeros(C.shape, order="F")
+    oracle.matmul(OA(co), OA(a_mat), OA(b_mat), OA(t))
+    np.testing.assert_array_equal(C.to_numpy(), co)
+    # and the strided sections themselves (no transpose flags): As (30 x 24) x Bs-rows (24 x 30)
+    Bs2 = B.section((0, 46, 2), (58, 0, -2))            # 24 x 30
+    C2 = ftn.FArray.empty((30, 30))
+    ftn.matmul(C2, As, Bs2)
+    co2, t2 = np.zeros((30, 30), order="F"), np.zeros((30, 30), order="F")
+    oracle.matmul(OA(co2), OA(a_op), OA(np.asfortranarray(pb[0:47:2, 58::-2])), OA(t2))
+    np.testing.assert_array_equal(C2.to_numpy(), co2)
 
 
 def test_matmul_exact_cases(ftn):
