@@ -43,8 +43,16 @@ struct ResParams {
   double* xbuf;     // exchange rows: [epoch parity][CTA][side: first / last K owned rows][K][pitch]
 };
 
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Publish: a release reduction (the flag counts the epochs).  A plain st.release measured
+// ~4.5 us per neighbour handshake with 148 polling CTAs, the reduction ~1.4 us
+// (tools/microbench/flag_probe.cu).
+__device__ __forceinline__ void publish(uint32_t* p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
@@ -52,17 +60,15 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   return v;
 }
 
-// thread 0: wait until the flags of CTAs b-1 and b+1 (those that exist) reach `epoch`; relaxed
-// polling (an acquire load would invalidate L1 on every poll), one acquire fence at the end
+// thread 0: wait until the flags of CTAs b-1 and b+1 (those that exist) reach `epoch`
 __device__ void wait_neighbours(const ResParams& p, int b, uint32_t epoch) {
   for (int nb = b - 1; nb <= b + 1; nb += 2) {
     if (nb < 0 || nb >= (int)gridDim.x) continue;
     uint64_t spins = 0;
-    while (ld_relaxed(&p.flags[nb]) < epoch) {
+    while (ld_acquire(&p.flags[nb]) < epoch) {
       if (++spins > (1ull << 24)) __trap();  // a neighbour that never arrives: fail, do not hang
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // n double2 from global (L2, never a stale L1 line) to shared memory: batches of 8 loads in
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) jacobi2d_resident(const __grid
       if (tid == 0) {
         if (FTN_RES_TRACE) tr_c1 += gtimer() - tr_c0, tr_c0 = gtimer();
         if (FTN_RES_TRACE && epoch <= 64) p.trace[(size_t)b * 64 + epoch - 1] = tr_c0;
-        st_release(&p.flags[b], epoch);
+        publish(&p.flags[b]);
         wait_neighbours(p, b, epoch);
         if (FTN_RES_TRACE) tr_w += gtimer() - tr_c0, tr_c0 = gtimer();
       }
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) jacobi2d_resident(const __grid
   ++epoch;
   __syncthreads();
   if (tid == 0) {
-    st_release(&p.flags[b], epoch);
+    publish(&p.flags[b]);
     wait_neighbours(p, b, epoch);
   }
   __syncthreads();
@@ -245,6 +251,208 @@ __global__ void __launch_bounds__(RES_THREADS, 1) jacobi2d_resident(const __grid
     for (int idx = tid; idx < (hi - lo + 1) * cols; idx += RES_THREADS) {
       const int r = lo + idx / cols, c = 1 + idx % cols;
       *gptr(arr, r, c) = srow(parity, r)[c];
+    }
+  }
+}
+
+// Register-resident variant (n1 <= 2 * RES_THREADS, slab rows <= RR_MAX): thread = column pair
+// (c, c+1) holding its two columns of every slab row in registers, so a sweep reads no shared
+// memory except the two warp-edge columns; the i-1 / i+1 neighbours come from the adjacent
+// lanes.  The boundary columns / rows take the values of the array of the new iterate's parity
+// from small shared tables (u's and unew's rings may differ, as in the swapped DO nest).
+constexpr int RR_MAX = 16;
+constexpr int RES_WARPS = RES_THREADS / 32;
+
+__global__ void __launch_bounds__(RES_THREADS, 1) jacobi2d_resident_reg(const __grid_constant__ ResParams p) {
+  extern __shared__ __align__(16) double sm[];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int interior = p.n2 - 2;
+  const int lo = 1 + (int)((int64_t)interior * b / G);
+  const int hi = (int)((int64_t)interior * (b + 1) / G);
+  const int K = p.K;
+  const int rb = max(0, lo - K), re = min(p.n2 - 1, hi + K);
+  const int nr = re - rb + 1;  // <= RR_MAX
+  const int pitch = p.pitch;
+  const int n1 = p.n1;
+  const int c = 2 * tid;
+  const bool valid = c < n1, has1 = c + 1 < n1;
+  // shared tables: bcol[array][side: column 0 / n1-1][RR_MAX], brow[array][side: row 0 / n2-1][pitch],
+  // edge[sweep parity][warp][lane 0 .x / lane 31 .y][RR_MAX]
+  double* bcol = sm;
+  double* brow = bcol + 2 * 2 * RR_MAX;
+  double* edge = brow + 2 * 2 * (size_t)pitch;
+  auto gptr = [&](int arr, int r, int col) -> double* {
+    return arr == 0 ? reinterpret_cast<double*>(p.u + (int64_t)col * p.u_sm1 + (int64_t)r * p.u_sm2)
+                    : reinterpret_cast<double*>(p.w + (int64_t)col * p.w_sm1 + (int64_t)r * p.w_sm2);
+  };
+  auto xrow = [&](int e, int cta, int side) {
+    return p.xbuf + ((((size_t)e * G + cta) * 2 + side) * K) * pitch;
+  };
+  double x[RR_MAX][2];
+#pragma unroll
+  for (int i = 0; i < RR_MAX; ++i) {
+    x[i][0] = x[i][1] = 0.0;
+    if (i < nr && valid) {
+      x[i][0] = __ldcg(gptr(0, rb + i, c));
+      if (has1) x[i][1] = __ldcg(gptr(0, rb + i, c + 1));
+    }
+  }
+  for (int idx = tid; idx < 2 * 2 * nr; idx += RES_THREADS) {
+    const int arr = idx / (2 * nr), side = (idx / nr) % 2, i = idx % nr;
+    bcol[(arr * 2 + side) * RR_MAX + i] = __ldcg(gptr(arr, rb + i, side ? n1 - 1 : 0));
+  }
+  for (int idx = tid; idx < 2 * n1; idx += RES_THREADS) {
+    const int arr = idx / n1, col = idx % n1;
+    if (rb == 0) brow[(arr * 2 + 0) * pitch + col] = __ldcg(gptr(arr, 0, col));
+    if (re == p.n2 - 1) brow[(arr * 2 + 1) * pitch + col] = __ldcg(gptr(arr, p.n2 - 1, col));
+  }
+  __syncthreads();
+  uint32_t epoch = 0;
+  if (p.sweeps <= K) {  // no exchange will order the neighbours' initial loads before our writes
+    ++epoch;
+    if (tid == 0) {
+      publish(&p.flags[b]);
+      wait_neighbours(p, b, epoch);
+    }
+    __syncthreads();
+  }
+  const double coeff = p.coeff;
+  int64_t done = 0;
+  uint64_t tr0 = 0, trc = 0, trw = 0, trh = 0;
+  while (done < p.sweeps) {
+    const int k = (int)min((int64_t)K, p.sweeps - done);
+    if (FTN_RES_TRACE && tid == 0) tr0 = gtimer();
+    for (int q = 1; q <= k; ++q) {
+      const int64_t t = done + q - 1;  // iterate t -> t + 1
+      const int np = (int)((t + 1) & 1);  // parity (array) of the new iterate
+      const int ia = max(1, lo - (K - q)) - rb, iz = min(p.n2 - 2, hi + (K - q)) - rb;
+      uint64_t ts0 = 0;
+      if (FTN_RES_TRACE && tid == 0) ts0 = gtimer();
+      double* ed = edge + (size_t)(t & 1) * RES_WARPS * 2 * RR_MAX;
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < RR_MAX; ++i) ed[(warp * 2 + 0) * RR_MAX + i] = x[i][0];
+      }
+      if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < RR_MAX; ++i) ed[(warp * 2 + 1) * RR_MAX + i] = x[i][1];
+      }
+      __syncthreads();
+      if (FTN_RES_TRACE && tid == 0) trh += gtimer() - ts0;
+      if (t + 1 == p.sweeps) {  // last sweep: iterate S-1 of the owned rows -> its array
+#pragma unroll
+        for (int i = 0; i < RR_MAX; ++i) {
+          const int r = rb + i;
+          if (r >= lo && r <= hi) {
+            if (valid && c >= 1 && c <= n1 - 2) *gptr(np ^ 1, r, c) = x[i][0];
+            if (has1 && c + 1 <= n1 - 2) *gptr(np ^ 1, r, c + 1) = x[i][1];
+          }
+        }
+      }
+      // every row 1 .. RR_MAX-2 is computed (no divergent branches around the shuffles); rows
+      // outside [ia, iz] keep their value through a select
+      const double* edL = ed + (max(warp - 1, 0) * 2 + 1) * RR_MAX;
+      const double* edR = ed + (min(warp + 1, RES_WARPS - 1) * 2 + 0) * RR_MAX;
+      const bool in0 = valid && c >= 1 && c <= n1 - 2, in1 = has1 && c + 1 <= n1 - 2;
+      double pv0 = x[0][0], pv1 = x[0][1];  // old values of the row above
+#pragma unroll
+      for (int i = 1; i < RR_MAX - 1; ++i) {
+        const double o0 = x[i][0], o1 = x[i][1];
+        double left = __shfl_up_sync(0xffffffffu, o1, 1);
+        double right = __shfl_down_sync(0xffffffffu, o0, 1);
+        const double eL = edL[i], eR = edR[i];
+        left = lane == 0 ? eL : left;    // warp 0 lane 0 holds column 0: its left is never used
+        right = lane == 31 ? eR : right;
+        // R#16: coeff * (((u(i-1,j) + u(i+1,j)) + u(i,j-1)) + u(i,j+1))
+        double v0 = left + o1;
+        v0 = v0 + pv0;
+        v0 = v0 + x[i + 1][0];
+        v0 = coeff * v0;
+        double v1 = o0 + right;
+        v1 = v1 + pv1;
+        v1 = v1 + x[i + 1][1];
+        v1 = coeff * v1;
+        const bool act = i >= ia && i <= iz;
+        x[i][0] = act && in0 ? v0 : o0;
+        x[i][1] = act && in1 ? v1 : o1;
+        pv0 = o0;
+        pv1 = o1;
+      }
+      // boundary columns (the lanes holding column 0 or n1-1) switch to the new iterate's array
+      if (valid && (c == 0 || c == n1 - 1 || c + 1 == n1 - 1)) {
+        const double* b0 = bcol + (np * 2 + (c == 0 ? 0 : 1)) * RR_MAX;
+        const double* b1 = bcol + (np * 2 + 1) * RR_MAX;
+#pragma unroll
+        for (int i = 1; i < RR_MAX - 1; ++i)
+          if (i >= ia && i <= iz) {
+            if (!in0) x[i][0] = b0[i];
+            if (has1 && !in1) x[i][1] = b1[i];
+          }
+      }
+      // boundary rows switch to the new iterate's array
+      if (rb == 0 && valid) {
+        x[0][0] = brow[(np * 2 + 0) * pitch + c];
+        if (has1) x[0][1] = brow[(np * 2 + 0) * pitch + c + 1];
+      }
+      if (re == p.n2 - 1 && valid) {
+#pragma unroll
+        for (int i = 0; i < RR_MAX; ++i)
+          if (i == nr - 1) {
+            x[i][0] = brow[(np * 2 + 1) * pitch + c];
+            if (has1) x[i][1] = brow[(np * 2 + 1) * pitch + c + 1];
+          }
+      }
+    }
+    done += k;
+    if (done < p.sweeps) {
+      const int e = (int)(epoch & 1);
+      // first / last K owned rows -> exchange slots (whole pairs, incl. the boundary columns)
+#pragma unroll
+      for (int i = 0; i < RR_MAX; ++i) {
+        const int r = rb + i;
+        if (valid && b > 0 && r >= lo && r < lo + K)
+          *reinterpret_cast<double2*>(xrow(e, b, 0) + (size_t)(r - lo) * pitch + c) = make_double2(x[i][0], x[i][1]);
+        if (valid && b < G - 1 && r > hi - K && r <= hi)
+          *reinterpret_cast<double2*>(xrow(e, b, 1) + (size_t)(r - (hi - K + 1)) * pitch + c) =
+              make_double2(x[i][0], x[i][1]);
+      }
+      ++epoch;
+      __syncthreads();
+      if (tid == 0) {
+        if (FTN_RES_TRACE) trc += gtimer() - tr0, tr0 = gtimer();
+        publish(&p.flags[b]);
+        wait_neighbours(p, b, epoch);
+        if (FTN_RES_TRACE) trw += gtimer() - tr0, tr0 = gtimer();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < RR_MAX; ++i) {
+        const int r = rb + i;
+        if (valid && b > 0 && r < lo) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(xrow(e, b - 1, 1) + (size_t)(r - (lo - K)) * pitch + c));
+          x[i][0] = v.x;
+          x[i][1] = v.y;
+        }
+        if (valid && b < G - 1 && r > hi && i < nr) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(xrow(e, b + 1, 0) + (size_t)(r - (hi + 1)) * pitch + c));
+          x[i][0] = v.x;
+          x[i][1] = v.y;
+        }
+      }
+    }
+  }
+  if (FTN_RES_TRACE && tid == 0 && (b % 37 == 1 || b == G - 1))
+    printf("reg CTA %d: phases %u compute+write %.2f us wait %.2f us; per sweep edge+barrier %.2f us\n", b, epoch,
+           trc / 1e3 / epoch, trw / 1e3 / epoch, trh / 1e3 / p.sweeps);
+  // iterate S of the owned rows -> its array (unew iff S odd)
+  const int fa = (int)(p.sweeps & 1);
+#pragma unroll
+  for (int i = 0; i < RR_MAX; ++i) {
+    const int r = rb + i;
+    if (r >= lo && r <= hi) {
+      if (valid && c >= 1 && c <= n1 - 2) *gptr(fa, r, c) = x[i][0];
+      if (has1 && c + 1 <= n1 - 2) *gptr(fa, r, c + 1) = x[i][1];
     }
   }
 }
@@ -266,51 +474,61 @@ int64_t jacobi_resident_min() {
   return v;
 }
 
-// Plan for the resident kernel: grid, halo depth and shared memory; false when the grid does
-// not fit (then the caller uses the streaming kernels).
-static bool resident_plan(int64_t n1, int64_t n2, int* grid, int* K, int* rows_max, int* pitch, size_t* smem) {
+// Plan for the resident kernels: grid, halo depth, shared memory and the variant (register
+// slab when n1 <= 2 * RES_THREADS and owned + 2K rows <= RR_MAX, else the shared-memory slab);
+// false when the grid does not fit (then the caller uses the streaming kernels).
+struct ResPlan {
+  int grid, K, rows_max, pitch;
+  size_t smem;
+  bool reg;
+};
+
+static bool resident_plan(int64_t n1, int64_t n2, ResPlan* pl) {
   if (n1 < 3 || n2 < 3 || n1 > (1 << 20) || n2 > (1 << 20)) return false;
   const int64_t interior = n2 - 2;
   const int pt = (int)((n1 + 1) & ~int64_t(1));
   const int kenv = g_res_k.load();
-  for (int k = (kenv > 0 ? kenv : 4); k >= 1; --k) {
-    const int64_t G = std::min<int64_t>(num_sms(), interior / k);  // every CTA owns >= k rows
-    if (G < 1) continue;
-    const int64_t own_max = (interior + G - 1) / G;
-    const int64_t rows = own_max + 2 * k;
-    const size_t bytes = 2 * (size_t)rows * pt * 8;
-    if (bytes <= (size_t)RES_SMEM_MAX) {
-      *grid = (int)G;
-      *K = k;
-      *rows_max = (int)rows;
-      *pitch = pt;
-      *smem = bytes;
-      return true;
+  for (int pass = 0; pass < 2; ++pass) {  // 0: register slab, 1: shared-memory slab
+    if (pass == 0 && n1 > 2 * RES_THREADS) continue;
+    for (int k = (kenv > 0 ? kenv : 4); k >= 1; --k) {
+      const int64_t G = std::min<int64_t>(num_sms(), interior / k);  // every CTA owns >= k rows
+      if (G >= 1) {
+        const int64_t own_max = (interior + G - 1) / G;
+        const int64_t rows = own_max + 2 * k;
+        const size_t bytes = pass == 0 ? (size_t)(4 * RR_MAX + 4 * (size_t)pt + 2 * RES_WARPS * 2 * RR_MAX) * 8
+                                       : 2 * (size_t)rows * pt * 8;
+        if ((pass == 0 ? rows <= RR_MAX : true) && bytes <= (size_t)RES_SMEM_MAX) {
+          *pl = {(int)G, k, (int)rows, pt, bytes, pass == 0};
+          return true;
+        }
+      }
+      if (kenv > 0) break;
     }
-    if (kenv > 0) break;
   }
   return false;
 }
 
 bool jacobi2d_resident_fits(const ftn_desc_t* u) {
-  int g, k, r, pt;
-  size_t sm;
-  return u->rank == 2 && resident_plan(u->dim[0].extent, u->dim[1].extent, &g, &k, &r, &pt, &sm);
+  ResPlan pl;
+  return u->rank == 2 && resident_plan(u->dim[0].extent, u->dim[1].extent, &pl);
 }
 
 // All `sweeps` of the DO nest in one cooperative launch (sweeps >= 1); the result lands in
 // unew iff sweeps is odd, the other array holds iterate sweeps-1.
 ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                                    cudaStream_t s) {
-  int grid, K, rows_max, pitch;
-  size_t smem;
-  if (!resident_plan(u->dim[0].extent, u->dim[1].extent, &grid, &K, &rows_max, &pitch, &smem))
+  ResPlan pl;
+  if (!resident_plan(u->dim[0].extent, u->dim[1].extent, &pl))
     return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_resident: grid does not fit the aggregate shared memory");
+  const int grid = pl.grid, K = pl.K, rows_max = pl.rows_max, pitch = pl.pitch;
+  const size_t smem = pl.smem;
+  const void* fn = pl.reg ? (const void*)jacobi2d_resident_reg : (const void*)jacobi2d_resident;
   static std::atomic<bool> attr[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
     FTN_CUDA(cudaFuncSetAttribute(jacobi2d_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, RES_SMEM_MAX));
+    FTN_CUDA(cudaFuncSetAttribute(jacobi2d_resident_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, RES_SMEM_MAX));
     attr[dev & 63] = true;
   }
   // one stream-ordered temporary: flags (zeroed) + exchange slots (2 parities x grid x 2 x K rows)
@@ -337,7 +555,7 @@ ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, 
   p.xbuf = (double*)((char*)tmp.ptr + flag_bytes);
   p.trace = (uint64_t*)((char*)tmp.ptr + flag_bytes + (size_t)2 * grid * 2 * K * pitch * sizeof(double));
   void* args[] = {&p};
-  FTN_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi2d_resident, dim3(grid), dim3(RES_THREADS), args, smem, s));
+  FTN_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(RES_THREADS), args, smem, s));
   return after_launch("jacobi2d_resident");
 }
 

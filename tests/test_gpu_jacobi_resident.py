@@ -22,15 +22,24 @@ def ftn():
 
 
 def _fits(shape, K):
-    """The resident planner's rule (stencil_res.cu resident_plan): both iterates of the largest
-    row slab plus K halo rows per side in 227 KB, every CTA owning >= K rows."""
+    """The resident planner's rule (stencil_res.cu resident_plan): the register slab (n1 <= 1024,
+    owned + 2K rows <= 16) or both iterates of the largest row slab plus K halo rows per side in
+    227 KB of shared memory; every CTA owning >= K rows."""
     n1, n2 = shape
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     pitch = (n1 + 1) & ~1
-    for k in ([K] if K else [4, 3, 2, 1]):
-        g = min(sms, (n2 - 2) // k)
-        if g >= 1 and 2 * (-(-(n2 - 2) // g) + 2 * k) * pitch * 8 <= 227 * 1024:
-            return True
+    for reg in (True, False):
+        if reg and n1 > 1024:
+            continue
+        for k in ([K] if K else [4, 3, 2, 1]):
+            g = min(sms, (n2 - 2) // k)
+            if g < 1:
+                continue
+            rows = -(-(n2 - 2) // g) + 2 * k
+            if reg and rows <= 16:
+                return True
+            if not reg and 2 * rows * pitch * 8 <= 227 * 1024:
+                return True
     return False
 
 
