@@ -242,7 +242,8 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
  * DESIGN.md §4.3), rank-3 sweeps up to min(T, 2) at a time (§4.4).  Results are
  * bit-identical for every T; the array that does not hold the result holds an earlier
  * iterate.  T in 1..6 (1 = one sweep per launch); default 5 or the FTN_JACOBI_FUSE
- * environment variable.  Process-wide. */
+ * environment variable; unless T is set explicitly, rank-2 grids of <= 2^21 points use 6
+ * (their launches are latency bound, so fewer launches win).  Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
 

@@ -475,10 +475,12 @@ static std::atomic<bool> g_attr_done[64] = {};  // per device (idempotent)
 // register-ring kernel: T=2 ~640, T=3 955-975, T=4 1230-1254, T=5 1484-1501, T=6 1190-1330
 // GLUPS).
 static std::atomic<int> g_fuse{0};
+static std::atomic<bool> g_fuse_explicit{false};  // set by ftn_jacobi_set_fusion or FTN_JACOBI_FUSE
 int jacobi_fuse_T() {
   int t = g_fuse.load();
   if (t == 0) {
     const char* e = getenv("FTN_JACOBI_FUSE");
+    if (e) g_fuse_explicit.store(true);
     t = e ? atoi(e) : 5;
     t = t < 1 ? 1 : (t > 6 ? 6 : t);
     g_fuse.store(t);
@@ -486,13 +488,17 @@ int jacobi_fuse_T() {
   return t;
 }
 
-// Sweeps per launch for this array: T (<= 4) for TMA-able rank-2 arrays, min(T, 2) for
-// TMA-able rank-3 arrays (jacobi3d_tb2), 1 otherwise.
+// Sweeps per launch for this array: T for TMA-able rank-2 arrays, 2 for TMA-able rank-3 arrays
+// (jacobi3d_tb2, when T >= 2), 1 otherwise.  Unless T was set explicitly, small rank-2 grids
+// (<= 2^21 points, e.g. the paper's 1024^2) use 6: a launch there is bound by the ~10-12 us of
+// per-launch latency, not by its work, so fewer launches win (1024^2: T=5 364, T=6 506 GLUPS;
+// 2048^2: equal).
 int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
-  const int T = jacobi_fuse_T();
+  int T = jacobi_fuse_T();
   if (T < 2 || !stencil_tma_able(u) || !stencil_tma_able(unew)) return 1;
   for (int d = 0; d < u->rank; ++d)
     if (u->dim[d].extent < 3) return 1;
+  if (u->rank == 2 && !g_fuse_explicit.load() && u->dim[0].extent * u->dim[1].extent <= (int64_t(1) << 21)) T = 6;
   return u->rank == 2 ? T : 2;
 }
 
@@ -556,6 +562,7 @@ extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
   if (sweeps_per_launch < 1 || sweeps_per_launch > 6)
     return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..6 sweeps per launch");
   g_fuse.store(sweeps_per_launch);
+  g_fuse_explicit.store(true);
   return FTN_OK;
 }
 

@@ -302,12 +302,35 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     attr[dev & 63] = true;
   }
   if (dst->dim[0].sm != 8) return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_wf: destination must have unit stride in dim 1");
-  CUtensorMap m;
-  uint64_t dims[2] = {(uint64_t)src->dim[0].extent, (uint64_t)src->dim[1].extent};
-  uint64_t strides[1] = {(uint64_t)src->dim[1].sm};
-  uint32_t box[2] = {(uint32_t)C::BW, (uint32_t)WF_R};
-  FTN_CHECK(encode_tma(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, src->base_addr, dims, strides, box,
-                       CU_TENSOR_MAP_SWIZZLE_NONE));
+  // host cost per launch matters for small grids (a launch of 5 sweeps of 1024^2 is ~10 us of
+  // device time): the tensor map, the occupancy and the unit plan are cached per thread
+  struct MapEntry {
+    const void* base;
+    int64_t n1, n2, sm2;
+    CUtensorMap map;
+  };
+  thread_local MapEntry maps[4] = {};
+  thread_local int next_map = 0;
+  const CUtensorMap* mp = nullptr;
+  for (auto& e : maps)
+    if (e.base == src->base_addr && e.n1 == src->dim[0].extent && e.n2 == src->dim[1].extent &&
+        e.sm2 == src->dim[1].sm)
+      mp = &e.map;
+  if (!mp) {
+    MapEntry& e = maps[next_map];
+    next_map = (next_map + 1) % 4;
+    uint64_t dims[2] = {(uint64_t)src->dim[0].extent, (uint64_t)src->dim[1].extent};
+    uint64_t strides[1] = {(uint64_t)src->dim[1].sm};
+    uint32_t box[2] = {(uint32_t)C::BW, (uint32_t)WF_R};
+    e.base = nullptr;
+    FTN_CHECK(encode_tma(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, src->base_addr, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_NONE));
+    e.base = src->base_addr;
+    e.n1 = src->dim[0].extent;
+    e.n2 = src->dim[1].extent;
+    e.sm2 = src->dim[1].sm;
+    mp = &e.map;
+  }
   WFParams p;
   p.dst = (char*)dst->base_addr;
   p.d_sm1 = dst->dim[0].sm;
@@ -321,13 +344,32 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   p.fix_hi = fix_hi;
   p.coeff = coeff;
   if (p.nrows <= 0 || p.n1 < 3) return FTN_OK;
-  int occ = 0;
-  FTN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi2d_wf<T, C>, C::THREADS, C::SMEM));
-  if (occ < 1) occ = 1;
+  static std::atomic<int> occ_cache[64] = {};
+  int occ = occ_cache[dev & 63].load();
+  if (occ == 0) {
+    FTN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi2d_wf<T, C>, C::THREADS, C::SMEM));
+    if (occ < 1) occ = 1;
+    occ_cache[dev & 63].store(occ);
+  }
   int64_t grid = (int64_t)num_sms() * occ;
-  plan_units_halo(p.strips, p.nrows, grid, 2 * T, &p.seg, &p.units);
+  struct PlanEntry {
+    int64_t strips = -1, nrows, grid, seg, units;
+  };
+  thread_local PlanEntry pc;
+  if (pc.strips == p.strips && pc.nrows == p.nrows && pc.grid == grid) {
+    p.seg = pc.seg;
+    p.units = pc.units;
+  } else {
+    plan_units_halo(p.strips, p.nrows, grid, 2 * T, &p.seg, &p.units);
+    pc = {p.strips, p.nrows, grid, p.seg, p.units};
+  }
+  static const int64_t nseg_env = getenv("FTN_WF_NSEG") ? atoll(getenv("FTN_WF_NSEG")) : 0;  // tuning probe
+  if (nseg_env > 0) {
+    p.seg = (p.nrows + nseg_env - 1) / nseg_env;
+    p.units = p.strips * ((p.nrows + p.seg - 1) / p.seg);
+  }
   if (grid > p.units) grid = p.units;
-  jacobi2d_wf<T, C><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, p);
+  jacobi2d_wf<T, C><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(*mp, p);
   return after_launch("jacobi2d_wf");
 }
 
