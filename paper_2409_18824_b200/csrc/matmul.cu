@@ -638,6 +638,57 @@ __global__ void __launch_bounds__(256) vecmat_v4_kernel(const __grid_constant__ 
   }
 }
 
+// Column per block (default): the 8 warps of a block split one column of b into 8 contiguous
+// l ranges (multiples of 128), each folds its range as vecmat_v4_kernel does, and the 8
+// partials are combined in a fixed tree -- ~1 K concurrent 64 KB streams instead of one per
+// warp.  Deterministic; a different (bound-only) order than vecmat_v4_kernel.
+template <int VU>
+__global__ void __launch_bounds__(256) vecmat_blk_kernel(const __grid_constant__ VMParams p) {
+  __shared__ double part[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* x = reinterpret_cast<const double*>(p.x);
+  const int64_t kfull = p.k / 128 * 128;
+  const int64_t seg = (kfull / 128 + 7) / 8 * 128;
+  const int64_t la = min(kfull, warp * seg), lz = min(kfull, la + seg);
+  for (int64_t j = blockIdx.x; j < p.n; j += gridDim.x) {
+    const double* bp = reinterpret_cast<const double*>(p.b + j * p.b_sm1);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t l = la + 4 * lane;
+    for (; l + 128 * (VU - 1) < lz; l += 128 * VU) {
+      double bv[VU][4], xv[VU][4];
+#pragma unroll
+      for (int u = 0; u < VU; ++u) dev::ld_v4(bp + l + 128 * u, bv[u][0], bv[u][1], bv[u][2], bv[u][3]);
+#pragma unroll
+      for (int u = 0; u < VU; ++u) dev::ldg_v4(x + l + 128 * u, xv[u][0], xv[u][1], xv[u][2], xv[u][3]);
+#pragma unroll
+      for (int u = 0; u < VU; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[v] = acc[v] + xv[u][v] * bv[u][v];
+    }
+    for (; l < lz; l += 128) {
+      double b0, b1, b2, b3, x0, x1, x2, x3;
+      dev::ld_v4(bp + l, b0, b1, b2, b3);
+      dev::ldg_v4(x + l, x0, x1, x2, x3);
+      acc[0] = acc[0] + x0 * b0;
+      acc[1] = acc[1] + x1 * b1;
+      acc[2] = acc[2] + x2 * b2;
+      acc[3] = acc[3] + x3 * b3;
+    }
+    if (warp == 7)
+      for (int64_t e = kfull + 4 * lane; e < p.k; e += 128)
+        for (int v = 0; v < 4 && e + v < p.k; ++v) acc[0] = acc[0] + x[e + v] * bp[e + v];
+    double sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int mask = 16; mask >= 1; mask >>= 1) sum = sum + __shfl_xor_sync(0xffffffffu, sum, mask);
+    if (lane == 0) part[warp] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      *reinterpret_cast<double*>(p.y + j * p.y_sm) =
+          ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+    __syncthreads();
+  }
+}
+
 ftn_status_t run_vecmat(const ftn_desc_t* y, const ftn_desc_t* x, const ftn_desc_t* b, cudaStream_t s) {
   VMParams p;
   p.x = (const char*)x->base_addr;
@@ -655,6 +706,18 @@ ftn_status_t run_vecmat(const ftn_desc_t* y, const ftn_desc_t* x, const ftn_desc
   const bool v4 = p.b_sm0 == 8 && p.x_sm == 8 && (p.b_sm1 % 32) == 0 && ((uintptr_t)p.b % 32) == 0 &&
                   ((uintptr_t)p.x % 32) == 0;
   static const int vu = getenv("FTN_VM_UNROLL") ? atoi(getenv("FTN_VM_UNROLL")) : 16;  // 8192^2: 16 -> 5650, 8 -> 5190, 4 -> 4510 GB/s
+  static const int blk = getenv("FTN_VM_BLK") ? atoi(getenv("FTN_VM_BLK")) : 8;  // 8192^2: 5.95-6.0 vs 5.72 TB/s (one warp per column)
+  if (v4 && blk) {
+    static const int gm = getenv("FTN_VM_GRIDM") ? atoi(getenv("FTN_VM_GRIDM")) : 8;
+    const unsigned g = (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms() * gm);
+    if (blk == 4)
+      vecmat_blk_kernel<4><<<g, 256, 0, s>>>(p);
+    else if (blk == 16)
+      vecmat_blk_kernel<16><<<g, 256, 0, s>>>(p);
+    else
+      vecmat_blk_kernel<8><<<g, 256, 0, s>>>(p);
+    return after_launch("vecmat_blk_kernel");
+  }
   if (v4) {
     if (vu == 8)
       vecmat_v4_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(p);
