@@ -107,6 +107,26 @@ def _worker(rank, world, port, q, shape2, shape3, sweeps):
         gathered = [torch.empty(1, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(gathered, t)
         out["sum"] = oracle.tree_combine([g.item() for g in gathered], oracle.SUM)
+        # global MAXVAL: local value, all-reduce MAX (order-free)
+        tm = torch.tensor([oracle.reduce_orderR(oracle.FArray(v[rank * per:(rank + 1) * per].copy()), oracle.MAX)],
+                          dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        out["max"] = tm.item()
+        # column-sharded MATMUL (ftn_matmul_colsharded's plan): A broadcast from rank 0, rank r
+        # owns the column block J_r of b and c; blocks gathered in rank order
+        m, k, n = 23, 17, 4 * world + 3
+        a_full = synth.farray((m, k), array_id=31, mode=synth.U11) if rank == 0 else np.zeros((m, k), order="F")
+        ta = torch.from_numpy(np.ascontiguousarray(a_full.ravel(order="F")))
+        dist.broadcast(ta, 0)
+        a_loc = np.asfortranarray(ta.numpy().reshape((m, k), order="F"))
+        b_full = synth.farray((k, n), array_id=32, mode=synth.U11)
+        cols = D.slab(n, world, rank)
+        c_loc = np.zeros((m, cols.owned), order="F")
+        oracle.matmul(oracle.FArray(c_loc), oracle.FArray(a_loc),
+                      oracle.FArray(np.asfortranarray(b_full[:, cols.lo:cols.hi])))
+        blocks = [None] * world
+        dist.all_gather_object(blocks, (cols.lo, c_loc))
+        out["matmul"] = blocks
         if rank == 0:
             q.put(out)
     finally:
@@ -136,3 +156,13 @@ def test_distributed_protocol_matches_undivided(world):
     n = 4 * 65536 * world
     v = synth.values(n, mode=synth.U11)
     assert out["sum"] == oracle.reduce_orderR(oracle.FArray(v), oracle.SUM)   # decomposition independent
+    assert out["max"] == oracle.reduce_orderR(oracle.FArray(v), oracle.MAX)
+    m, k, n = 23, 17, 4 * world + 3
+    a = synth.farray((m, k), array_id=31, mode=synth.U11)
+    b = synth.farray((k, n), array_id=32, mode=synth.U11)
+    c = np.zeros((m, n), order="F")
+    oracle.matmul(oracle.FArray(c), oracle.FArray(a), oracle.FArray(b))
+    got = np.zeros((m, n), order="F")
+    for lo, blk in out["matmul"]:
+        got[:, lo:lo + blk.shape[1]] = blk
+    np.testing.assert_array_equal(got, c)      # every element's fold is local to one rank
