@@ -397,6 +397,8 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 59: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
     case 69: return launch_wf<6, WFCfg<6, 4, 6, 4, 1>>(WF_ARGS);
     case 58: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3>>(WF_ARGS);   // producer warp, 3 CTAs/SM
+    case 52: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3, 1>>(WF_ARGS);  // no producer, 3 CTAs/SM (168 regs)
+    case 53: return launch_wf<5, WFCfg<5, 4, 12, 3, 1, 3, 1>>(WF_ARGS); // 12-row boxes, 3 CTAs/SM
     case 51: return launch_wf<5, WFCfg<5, 4, 6, 4, 1>>(WF_ARGS);
     case 50: return launch_wf<5, WFCfg<5, 4, 6, 5, 1, 4, 1>>(WF_ARGS);
     case 40: return launch_wf<4, WFCfg<4, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
