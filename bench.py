@@ -556,9 +556,24 @@ def cpu_oracle_jacobi(budget_s=12.0, max_sweeps=100):
     t = time.perf_counter() - t0
     cores = len(os.sched_getaffinity(0))
     threads = int(os.environ.get("OMP_NUM_THREADS", cores))
+    # the plain single-thread oracle: one full sweep
+    prev = oracle.set_threads(1)
+    t0 = time.perf_counter()
+    oracle.jacobi(U, Wd, 1, 0.25)
+    t1s = time.perf_counter() - t0
+    oracle.set_threads(prev)
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     del u, w, np
     return {"value": (n - 2) ** 2 * sweeps / t / 1e9, "unit": "GLUPS", "cores": threads, "kind": "oracle",
-            "sample": f"full 8192^2 grid, {sweeps} of the 100 sweeps ({t:.1f} s), OpenMP over rows"}
+            "sample": f"full 8192^2 grid, {sweeps} of the 100 sweeps ({t:.1f} s), OpenMP over rows",
+            "single_thread": {"value": (n - 2) ** 2 / t1s / 1e9, "unit": "GLUPS",
+                              "sample": f"one full 8192^2 sweep ({t1s:.2f} s), 1 thread"},
+            "cpu_model": model}
 
 
 def run_reference(args):

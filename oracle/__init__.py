@@ -106,6 +106,7 @@ def lib():
                                                     ctypes.c_double, ctypes.POINTER(ctypes.c_int64),
                                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]),
             "orc_vecmat_f64": (ctypes.c_int, [P, P, P, P]),
+            "orc_set_threads": (ctypes.c_int, [ctypes.c_int]),
             "orc_pw_advection_f64": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_void_p, ctypes.c_void_p,
                                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                                     ctypes.c_double]),
@@ -314,6 +315,11 @@ def matmul_element(a: FArray, b: FArray, i: int, j: int) -> tuple[float, float]:
     t = ctypes.c_double()
     v = lib().orc_matmul_element_f64(a.ref(), b.ref(), i, j, ctypes.byref(t))
     return v, t.value
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's parallel loops (timing only; results do not depend on it)."""
+    return lib().orc_set_threads(n)
 
 
 def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float) -> bool:

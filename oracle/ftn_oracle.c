@@ -31,6 +31,9 @@
 #include <string.h>
 #include <math.h>
 #include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define ORC_MAXRANK 3
 
@@ -911,4 +914,17 @@ int orc_pw_advection_f64(const orc_array* su, const orc_array* sv, const orc_arr
         st3(sw, k, j, i, s);
       }
   return ORC_OK;
+}
+
+/* Timing helper for bench.py's cpu_baseline (not part of any computed result): the number of
+ * OpenMP threads the parallel loops above use; returns the previous setting (1 without OpenMP). */
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+  const int prev = omp_get_max_threads();
+  if (n > 0) omp_set_num_threads(n);
+  return prev;
+#else
+  (void)n;
+  return 1;
+#endif
 }
