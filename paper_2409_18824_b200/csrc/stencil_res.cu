@@ -533,7 +533,7 @@ ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, 
   }
   // one stream-ordered temporary: flags (zeroed) + exchange slots (2 parities x grid x 2 x K rows)
   const size_t flag_bytes = ((size_t)grid * sizeof(uint32_t) + 255) / 256 * 256;
-  const size_t xbytes = (size_t)2 * grid * 2 * K * pitch * sizeof(double) + (size_t)grid * 64 * 8;
+  const size_t xbytes = (size_t)2 * grid * 2 * K * pitch * sizeof(double) + (FTN_RES_TRACE ? (size_t)grid * 64 * 8 : 0);
   StreamTemp tmp;
   FTN_CHECK(tmp.alloc(flag_bytes + xbytes, s));
   FTN_CUDA(cudaMemsetAsync(tmp.ptr, 0, (size_t)grid * sizeof(uint32_t), s));
@@ -553,7 +553,7 @@ ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, 
   p.coeff = coeff;
   p.flags = (uint32_t*)tmp.ptr;
   p.xbuf = (double*)((char*)tmp.ptr + flag_bytes);
-  p.trace = (uint64_t*)((char*)tmp.ptr + flag_bytes + (size_t)2 * grid * 2 * K * pitch * sizeof(double));
+  p.trace = FTN_RES_TRACE ? (uint64_t*)((char*)tmp.ptr + flag_bytes + (size_t)2 * grid * 2 * K * pitch * sizeof(double)) : nullptr;
   void* args[] = {&p};
   FTN_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(RES_THREADS), args, smem, s));
   return after_launch("jacobi2d_resident");
