@@ -329,7 +329,25 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         checks["matmul_transpose"] = bool(torch.equal(m48.tensor, cf))
         ftn.transpose(st, s)
         checks["transpose"] = bool(torch.equal(st.tensor, s.view_tensor().t()))
+        # the same calls from plain C through the ABI (examples/c1_latency.c): no Python in the loop
+        c_abi = None
+        try:
+            import tempfile
+            cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+            lib = os.path.join(ROOT, "paper_2409_18824_b200")
+            with tempfile.TemporaryDirectory() as td:
+                exe = os.path.join(td, "c1_latency")
+                subprocess.run(["gcc", "-O2", os.path.join(ROOT, "examples", "c1_latency.c"), "-I",
+                                os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"), "-L", lib, "-lftn",
+                                "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{lib}",
+                                f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", exe], check=True,
+                               capture_output=True, timeout=120)
+                out_c = subprocess.run([exe], capture_output=True, text=True, timeout=120, check=True)
+                c_abi = json.loads(out_c.stdout.strip().splitlines()[-1])
+        except Exception as e:  # report, do not fail the bench line
+            c_abi = {"unavailable": str(e)[:200]}
         rows["c1_latency"] = {"value": lat["sum_s"], "unit": "us (median of 1000, SUM(a(::2,:)))",
+                              "c_abi": c_abi,
                               "latency_us": lat, "latency_graph_us": lat_graph,
                               "note": "latency_us: one Python call each (ctypes marshalling + launch + kernel); "
                                       "latency_graph_us: per call inside a CUDA graph of 100 calls (device time)",

@@ -37,3 +37,21 @@ def test_c_program_matches_oracle(tmp_path):
     assert in_unew == new
     np.testing.assert_array_equal(got, ref)
     assert total == oracle.reduce_orderR(OA(ref, [0, -5]).section((0, n1 - 1, 2), (-5, n2 - 6, 1)), oracle.SUM)
+
+
+def test_c1_latency_program(tmp_path):
+    """examples/c1_latency.c (the bench's C-ABI latency leg) builds, runs and finds the C1
+    closed form SUM(a(::2,:)) = 2357760 through plain C calls."""
+    import json
+    exe = tmp_path / "c1_latency"
+    lib = os.path.join(ROOT, "paper_2409_18824_b200")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run(["gcc", "-O2", os.path.join(ROOT, "examples", "c1_latency.c"), "-I", os.path.join(ROOT, "include"),
+                    "-I", os.path.join(cuda, "include"), "-L", lib, "-lftn", "-L", os.path.join(cuda, "lib64"),
+                    "-lcudart", f"-Wl,-rpath,{lib}", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["sum_closed_form_ok"] is True
+    assert set(d["sync_median_us"]) == set(d["back_to_back_mean_us"]) and len(d["sync_median_us"]) == 6
