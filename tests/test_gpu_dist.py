@@ -76,7 +76,8 @@ def _slabs(u0, p, halo, rng_fill=True):
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("shape,halo", [((300, 203), 1), ((300, 203), 3), ((140, 33, 45), 1), ((130, 301), 4),
                                         ((260, 407), 5), ((200, 500), 6),
-                                        ((129, 201), 2), ((70, 40, 61), 2), ((64, 33, 50), 3), ((65, 33, 50), 2)])
+                                        ((129, 201), 2), ((70, 40, 61), 2), ((64, 33, 50), 3), ((65, 33, 50), 2),
+                                        ((70, 40, 10), 1), ((90, 10), 1)])   # 1-plane slabs at p = 8
 def test_jacobi_decomposition_independence(ftn, p, shape, halo):
     """p slabs with `halo` halo planes; k owned planes exchanged per step (device copies standing
     in for ncclSend/Recv), ftn_jacobi_slab advancing k sweeps; == the undivided ftn_jacobi."""

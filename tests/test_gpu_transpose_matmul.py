@@ -276,3 +276,27 @@ def test_matmul_ieee_specials(ftn):
     fin = np.isfinite(co)
     assert np.all(np.abs(got[fin] - co[fin]) <= 4 * k * U * t[fin])
     assert np.isnan(got[3, 0]) and np.isnan(got[10, 4]) and np.isneginf(got[40, 9])
+
+
+def test_transpose_every_shape_to_70(ftn):
+    """SURVEY §8(c.4) tails: every (n1, n2) in [1, 70]^2 (tile remainders in both dimensions)."""
+    rng = np.random.default_rng(70)
+    for n1 in range(1, 71):
+        for n2 in range(1, 71):
+            a = np.asfortranarray(rng.uniform(-1, 1, (n1, n2)))
+            r = ftn.FArray.empty((n2, n1))
+            ftn.transpose(r, ftn.FArray.from_numpy(a, [1, -1]))
+            ro = np.zeros((n2, n1), order="F")
+            oracle.transpose(OA(ro), OA(a, [1, -1]))
+            np.testing.assert_array_equal(r.to_numpy(), ro, err_msg=str((n1, n2)))
+
+
+@pytest.mark.parametrize("force_dmma", [False, True])
+def test_matmul_cube_33_sampled(ftn, force_dmma):
+    """SURVEY §8(c.4) tails: 300 (m, n, k) drawn from {1..33}^3 (the small-product kernel is
+    bit-identical to the oracle; the DMMA path within the bound)."""
+    rng = np.random.default_rng(33 + force_dmma)
+    for _ in range(300):
+        m, n, k = (int(v) for v in rng.integers(1, 34, 3))
+        _mm_check(ftn, np.asfortranarray(rng.uniform(-1, 1, (m, k))), np.asfortranarray(rng.uniform(-1, 1, (k, n))),
+                  force_dmma=force_dmma)
