@@ -119,6 +119,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wf(const __grid_
     for (int s = 0; s < WF_NS; ++s) relcnt[s] = 0;
   }
   __syncthreads();
+  // programmatic dependent launch: the next launch of the plan may start its prologue now;
+  // nothing of this grid touches global memory before the previous grid has completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t G = gridDim.x;
   WFCursor<T, C> icur;  // NOPROD: NS boxes ahead of the consumed one
   if (C::NOPROD) {
@@ -369,7 +373,18 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     p.units = p.strips * ((p.nrows + p.seg - 1) / p.seg);
   }
   if (grid > p.units) grid = p.units;
-  jacobi2d_wf<T, C><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(*mp, p);
+  static const bool pdl = !getenv("FTN_WF_PDL") || atoi(getenv("FTN_WF_PDL")) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = pdl ? 1 : 0;
+  FTN_CUDA(cudaLaunchKernelEx(&cfg, jacobi2d_wf<T, C>, *mp, p));
   return after_launch("jacobi2d_wf");
 }
 
