@@ -40,6 +40,9 @@ namespace {
 #ifndef FTN_J3_BOX_Y
 #define FTN_J3_BOX_Y 32
 #endif
+#ifndef FTN_J3_JFAST
+#define FTN_J3_JFAST 0
+#endif
 #ifndef FTN_J3_CTAS
 #define FTN_J3_CTAS 1
 #endif
@@ -72,8 +75,16 @@ struct J3Geom {
   int32_t ntile, tiles_i, seg, plane_lo, plane_end;  // output planes [plane_lo, plane_end)
   __device__ __forceinline__ void unit(uint32_t u, int32_t& i0, int32_t& j0, int32_t& ka, int32_t& kb) const {
     const uint32_t t = u % (uint32_t)ntile, sgi = u / (uint32_t)ntile;
+#if FTN_J3_JFAST
+    // j fastest: CTAs launched together hold j-neighbour tiles, whose 4 shared halo rows
+    // (of 32 per box) can then come from L2
+    const uint32_t tiles_j = (uint32_t)ntile / (uint32_t)tiles_i;
+    i0 = (int32_t)(t / tiles_j) * B3_OX - 2;
+    j0 = (int32_t)(t % tiles_j) * B3_OY - 2;
+#else
     i0 = (int32_t)(t % (uint32_t)tiles_i) * B3_OX - 2;
     j0 = (int32_t)(t / (uint32_t)tiles_i) * B3_OY - 2;
+#endif
     ka = plane_lo + (int32_t)sgi * seg;
     kb = min(ka + seg, plane_end);
   }
