@@ -98,6 +98,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- timing helpers
 LAST_LAUNCHES = [0]
+LAST_STEP_MS = [0.0, 0.0]   # min, median of the last timed() call's steps (this rank)
 
 
 def timed(torch, fn, steps, warmup, clocks=None, dist=None, counter=None):
@@ -115,15 +116,21 @@ def timed(torch, fn, steps, warmup, clocks=None, dist=None, counter=None):
     if clocks:
         clocks.timing(True)
     c0 = counter() if counter else 0
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps - 1)]
     a.record()
-    for _ in range(steps):
+    for k in range(steps):
         fn()
+        if k < steps - 1:
+            marks[k].record()
     b.record()
     LAST_LAUNCHES[0] = (counter() - c0) if counter else 0
     torch.cuda.synchronize()
     if clocks:
         clocks.timing(False)
     t = a.elapsed_time(b) / 1e3
+    ev = [a] + marks + [b]   # per-step device times (median and min beside the mean)
+    per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(steps))
+    LAST_STEP_MS[:] = [per[0], per[len(per) // 2]]
     if dist is not None:
         tt = torch.tensor([t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -170,6 +177,7 @@ def bench_jacobi2d(torch, ftn, args, ctx):
         interior = (n - 2) * n * N
     t = timed(torch, step, args.steps, args.warmup, ctx["clocks"], ctx["dist"], counter=ftn.launch_count)
     launches = LAST_LAUNCHES[0]
+    step_min, step_med = LAST_STEP_MS
     glups = interior * sweeps * args.steps / t / 1e9
     # launch plan of ftn_jacobi: F launches of T fused sweeps + S1 single sweeps per step
     halo_T = max(1, ftn.jacobi_fusion())
@@ -178,6 +186,7 @@ def bench_jacobi2d(torch, ftn, args, ctx):
     stencil_launches = len(plan) * args.steps
     achieved = per_launch_bytes * stencil_launches / t / 1e9          # GB/s, launches back to back
     res = {"value": glups, "ms_per_step": t / args.steps * 1e3, "launches": launches,
+           "ms_step_min": step_min, "ms_step_median": step_med,
            "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes,
            "plan": {"max_sweeps_per_launch": halo_T, "launches_per_step": len(plan),
                     "sweeps_per_launch": {str(k): plan.count(k) for k in sorted(set(plan))}}}
@@ -256,7 +265,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
     def gbs_row(name, nbytes, fn, units=None):
         t = timed(torch, fn, steps, warm, None, dist)
         gbs = nbytes * N * steps / t / 1e9
-        rows[name] = {"value": gbs, "unit": "GB/s", "ms": t / steps * 1e3,
+        rows[name] = {"value": gbs, "unit": "GB/s", "ms": t / steps * 1e3, "ms_min": LAST_STEP_MS[0],
+                      "ms_median": LAST_STEP_MS[1],
                       "roofline": {"bound": "hbm", "frac": gbs / N / hbm_peak}}
 
     # C1: real(8) a(0:63,1:48) = its 0-based offset, s = a(::2,:); latency of each call (median of
@@ -694,7 +704,9 @@ def main():
         frac = head["achieved_gbs"] / hbm_peak
         line = {
             "metric": METRIC, "value": head["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "ms_per_step_min": head["ms_step_min"], "ms_per_step_median": head["ms_step_median"],
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(CONFIG, parallelism=f"slab{world}" if world > 1 else "1 GPU",
                            global_grid=f"8192x{8192 * world + (2 if world > 1 else 0)}"),
