@@ -171,3 +171,24 @@ def test_resident_on_side_stream_and_graph(ftn):
     ftn.jacobi(U2, W2, 6)
     np.testing.assert_array_equal(U.to_numpy(), U2.to_numpy())
     np.testing.assert_array_equal(W.to_numpy(), W2.to_numpy())
+
+
+def test_resident_fuzz(ftn):
+    """Random shapes (both the register and the shared-memory slab), halo depths, sweep counts
+    and lower bounds; both arrays bit-exact vs the oracle whenever the resident path runs."""
+    rng = np.random.default_rng(1824)
+    ran = 0
+    try:
+        for it in range(120):
+            shape = (int(rng.integers(3, 1200)), int(rng.integers(3, 700)))
+            K = int(rng.integers(0, 5))
+            sweeps = int(rng.integers(1, 40))
+            lbs = [int(v) for v in rng.integers(-4, 5, 2)]
+            ftn.jacobi_set_resident(1, K)
+            u0 = synth.jacobi_init(shape, array_id=it)
+            fits = _fits(shape, K)
+            _both(ftn, u0, _w0(u0, it, fits), sweeps, lbs, resident=fits)
+            ran += fits
+    finally:
+        ftn.jacobi_set_resident(0, 0)
+    assert ran > 60
