@@ -318,6 +318,15 @@ typedef struct ftn_comm_s* ftn_comm_t;
 ftn_status_t ftn_comm_unique_id(uint8_t id[FTN_COMM_ID_BYTES]);
 ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank,
                            const uint8_t id[FTN_COMM_ID_BYTES], int32_t device);
+/* nranks communicators of ONE process ("virtual ranks"): comms[r] is rank r, on device
+ * devices[r] (all ranks may share one GPU).  Each rank must be driven by its own host thread
+ * (its calls block until the matching calls of its peers arrive, at most 300 s, then
+ * FTN_ERR_NCCL).  Every message is one cudaMemcpyAsync on the receiver's stream, ordered by
+ * CUDA events after the sender's stream; a send completes, in stream order, once the
+ * receiver's copy has (the semantics of grouped ncclSend/ncclRecv).  The distributed calls
+ * below run exactly the same loops as over NCCL: this is how their p > 1 paths are tested on
+ * one GPU.  Destroy each comm with ftn_comm_destroy. */
+ftn_status_t ftn_comm_init_virtual(ftn_comm_t* comms, int32_t nranks, const int32_t* devices);
 ftn_status_t ftn_comm_destroy(ftn_comm_t comm);
 /* Overlap of the Jacobi halo exchange with the interior sweeps in ftn_jacobi_dist: the owned
  * planes whose dependence cone stays inside the owned planes are advanced on a side stream
@@ -325,6 +334,9 @@ ftn_status_t ftn_comm_destroy(ftn_comm_t comm);
  * the halos follow the exchange.  mode 0 = off, 1 = when nranks > 1 (default), 2 = always
  * (also at nranks = 1, for testing).  Results are identical in every mode. */
 ftn_status_t ftn_comm_set_overlap(ftn_comm_t comm, int32_t mode);
+/* SMs the interior sweeps on the side stream leave free for the exchange's kernels while
+ * the overlap runs (persistent grids are sized for num_SMs - sms); 0..64, default 8. */
+ftn_status_t ftn_comm_set_sm_reserve(ftn_comm_t comm, int32_t sms);
 
 /* Global reductions of an array slab-distributed over the ranks along its
  * last dimension (x_local is this rank's slab).  The result, identical on

@@ -68,12 +68,18 @@ ftn_status_t require_sm100() {
   return FTN_OK;
 }
 
+thread_local int t_sm_reserve = 0;  // ScopedSmReserve (dist.cu): SMs left free for concurrent kernels
+
 int num_sms() {
   int d = 0;
   cudaGetDevice(&d);
   std::lock_guard<std::mutex> lk(g_dev_mu);
-  return g_dev[d].sms > 0 ? g_dev[d].sms : 148;
+  const int n = g_dev[d].sms > 0 ? g_dev[d].sms : 148;
+  return n - t_sm_reserve > 1 ? n - t_sm_reserve : 1;
 }
+
+ScopedSmReserve::ScopedSmReserve(int n) : saved(t_sm_reserve) { t_sm_reserve = n; }
+ScopedSmReserve::~ScopedSmReserve() { t_sm_reserve = saved; }
 
 int64_t type_len(int32_t type) {
   switch (type) {

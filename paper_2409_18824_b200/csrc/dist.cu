@@ -6,36 +6,51 @@
 //     (deterministic; equal to the 1-GPU result when slabs are equal power-of-two
 //     multiples of the R chunk);
 //   * Jacobi: last-dimension slabs with `halo` planes per side; per launch of the plan the
-//     k owned planes next to each neighbour go out with grouped ncclSend/ncclRecv and the
-//     slab advances k fused sweeps (k <= halo: deep halos, one exchange per k sweeps);
+//     k owned planes next to each neighbour go out (grouped send/recv) and the slab
+//     advances k fused sweeps (k <= halo: deep halos, one exchange per k sweeps);
 //   * MATMUL: column blocks of b and c, a replicated (ftn_bcast once).
+//
+// The exchange sits behind a small transport interface with two implementations:
+//   * NcclTransport: ncclSend/ncclRecv in a group, ncclAllGather, ncclBroadcast;
+//   * VirtualTransport: p ranks of ONE process (one host thread per rank, any devices,
+//     typically all on one GPU) -- every message is one cudaMemcpyAsync on the receiver's
+//     stream, ordered by CUDA events against the sender's stream, with the same blocking
+//     semantics as NCCL's grouped send/recv (a send completes, in stream order, once the
+//     receiver's copy has).  It runs the library's own distributed loops -- plans, deep
+//     halos, buffer offsets, the interior/halo overlap on the side stream -- at p > 1 on a
+//     single GPU (ftn_comm_init_virtual).
 #include "ftn_internal.cuh"
 
 #include <algorithm>
-
-#include <nccl.h>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <vector>
 
-struct ftn_comm_s {
-  ncclComm_t nccl;
-  int nranks, rank, device;
-  int overlap = 1;                 // 0 off, 1 when nranks > 1, 2 always (ftn_comm_set_overlap)
-  cudaStream_t side = nullptr;     // interior sweeps while the halo exchange runs
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-};
+#include <nccl.h>
 
 namespace ftn {
-size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b);
-ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws, size_t ws_bytes,
-                          cudaStream_t s);
-ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew);
-ftn_status_t jacobi_prepare();
-int jacobi_fuse_T();
-bool stencil_tma_able(const ftn_desc_t* d);
-ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
-                              int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
-                              cudaStream_t s);
+
+// One message of a grouped exchange (bytes of contiguous device memory to / from `peer`).
+struct P2POp {
+  bool send;
+  void* buf;
+  size_t bytes;
+  int peer;
+};
+
+struct Transport {
+  virtual ~Transport() {}
+  // All sends and receives of one exchange step; every rank posts the matching ops.
+  virtual ftn_status_t group(const P2POp* ops, int n, cudaStream_t s) = 0;
+  // recv[r * bytes .. (r+1) * bytes) = rank r's send (every rank).
+  virtual ftn_status_t allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // buf on every rank = buf on root.
+  virtual ftn_status_t bcast(void* buf, size_t bytes, int root, cudaStream_t s) = 0;
+};
 
 namespace {
 
@@ -48,13 +63,219 @@ ftn_status_t nccl_fail(ncclResult_t r, const char* what) {
     if (r__ != ncclSuccess) return nccl_fail(r__, #expr);      \
   } while (0)
 
-ncclDataType_t nccl_type(int32_t t) {
-  switch (t) {
-    case FTN_I32: return ncclInt32;
-    case FTN_I64: return ncclInt64;
-    case FTN_F32: return ncclFloat32;
-    default: return ncclFloat64;
+struct NcclTransport : Transport {
+  ncclComm_t nccl = nullptr;
+  ~NcclTransport() override {
+    if (nccl) ncclCommDestroy(nccl);
   }
+  ftn_status_t group(const P2POp* ops, int n, cudaStream_t s) override {
+    FTN_NCCL(ncclGroupStart());
+    for (int i = 0; i < n; ++i) {
+      if (ops[i].send)
+        FTN_NCCL(ncclSend(ops[i].buf, ops[i].bytes, ncclUint8, ops[i].peer, nccl, s));
+      else
+        FTN_NCCL(ncclRecv(ops[i].buf, ops[i].bytes, ncclUint8, ops[i].peer, nccl, s));
+    }
+    FTN_NCCL(ncclGroupEnd());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FTN_OK;
+  }
+  ftn_status_t allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    FTN_NCCL(ncclAllGather(send, recv, bytes, ncclUint8, nccl, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FTN_OK;
+  }
+  ftn_status_t bcast(void* buf, size_t bytes, int root, cudaStream_t s) override {
+    FTN_NCCL(ncclBroadcast(buf, buf, bytes, ncclUint8, root, nccl, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FTN_OK;
+  }
+};
+
+// ---------------------------------------------------------------- virtual ranks
+// Channel a -> b of a virtual group: a queue of posted messages.  Per group the sender
+// records `ready` on its stream once and posts its messages (buf, bytes, sequence number);
+// the receiver waits for each post, makes its stream wait on `ready`, copies, records `done`
+// on its stream and acknowledges; once every message of the group is acknowledged the
+// sender's stream waits on `done` (recorded after the last copy).  Event reuse is safe:
+// `ready` is re-recorded only in the sender's next group, after every receiver's wait on it
+// was enqueued; `done` only for a message of the next group, after the sender's wait on it
+// was enqueued.
+struct VMsg {
+  const void* buf;
+  size_t bytes;
+  uint64_t seq;
+};
+
+struct VChannel {
+  cudaEvent_t ready = nullptr, done = nullptr;
+  std::vector<VMsg> q;   // posted, not yet taken
+  uint64_t acked = 0;    // highest acknowledged sequence number
+};
+
+struct VGroup {
+  int n;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<VChannel> ch;  // ch[a * n + b]: a -> b
+  explicit VGroup(int n_) : n(n_), ch((size_t)n_ * n_) {}
+  ~VGroup() {
+    for (auto& c : ch) {
+      if (c.ready) cudaEventDestroy(c.ready);
+      if (c.done) cudaEventDestroy(c.done);
+    }
+  }
+};
+
+constexpr auto kVirtualTimeout = std::chrono::seconds(300);
+
+struct VirtualTransport : Transport {
+  std::shared_ptr<VGroup> g;
+  int rank, device;
+  std::vector<uint64_t> sent, recvd;  // per peer: messages sent to / received from it
+
+  VirtualTransport(std::shared_ptr<VGroup> g_, int rank_, int device_)
+      : g(std::move(g_)), rank(rank_), device(device_), sent((size_t)g->n, 0), recvd((size_t)g->n, 0) {}
+
+  ftn_status_t wait_for(std::unique_lock<std::mutex>& lk, const char* what, int peer,
+                        const std::function<bool()>& pred) {
+    if (!g->cv.wait_for(lk, kVirtualTimeout, pred))
+      return fail(FTN_ERR_NCCL, std::string("virtual transport: rank ") + std::to_string(rank) + " timed out waiting for " +
+                                    what + " of rank " + std::to_string(peer));
+    return FTN_OK;
+  }
+
+  ftn_status_t group(const P2POp* ops, int n, cudaStream_t s) override {
+    for (int i = 0; i < n; ++i)
+      if (ops[i].peer < 0 || ops[i].peer >= g->n || ops[i].peer == rank)
+        return fail(FTN_ERR_NCCL, "virtual transport: bad peer");
+    // 1. post every send (never blocks)
+    std::vector<char> to(g->n, 0);
+    for (int i = 0; i < n; ++i)
+      if (ops[i].send && !to[(size_t)ops[i].peer]) {
+        to[(size_t)ops[i].peer] = 1;
+        FTN_CUDA(cudaEventRecord(g->ch[(size_t)rank * g->n + ops[i].peer].ready, s));
+      }
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      for (int i = 0; i < n; ++i) {
+        if (!ops[i].send) continue;
+        const int b = ops[i].peer;
+        g->ch[(size_t)rank * g->n + b].q.push_back({ops[i].buf, ops[i].bytes, ++sent[(size_t)b]});
+      }
+    }
+    g->cv.notify_all();
+    // 2. every receive, in posting order per peer: wait for the post, copy on this rank's
+    //    stream, acknowledge
+    for (int i = 0; i < n; ++i) {
+      if (ops[i].send) continue;
+      const int a = ops[i].peer;
+      VChannel& c = g->ch[(size_t)a * g->n + rank];
+      const uint64_t seq = ++recvd[(size_t)a];
+      VMsg m{};
+      {
+        std::unique_lock<std::mutex> lk(g->mu);
+        FTN_CHECK(wait_for(lk, "a send", a, [&] {
+          for (const VMsg& x : c.q)
+            if (x.seq == seq) return true;
+          return false;
+        }));
+        for (size_t j = 0; j < c.q.size(); ++j)
+          if (c.q[j].seq == seq) {
+            m = c.q[j];
+            c.q.erase(c.q.begin() + (long)j);
+            break;
+          }
+      }
+      if (m.bytes != ops[i].bytes)
+        return fail(FTN_ERR_NCCL, "virtual transport: message size differs between sender and receiver");
+      FTN_CUDA(cudaStreamWaitEvent(s, c.ready, 0));
+      if (m.bytes) FTN_CUDA(cudaMemcpyAsync(ops[i].buf, m.buf, m.bytes, cudaMemcpyDefault, s));
+      FTN_CUDA(cudaEventRecord(c.done, s));
+      {
+        std::lock_guard<std::mutex> lk(g->mu);
+        c.acked = seq;
+      }
+      g->cv.notify_all();
+    }
+    // 3. the sends complete (in stream order) when their receivers' copies have
+    for (int b = 0; b < g->n; ++b) {
+      if (!to[(size_t)b]) continue;
+      VChannel& c = g->ch[(size_t)rank * g->n + b];
+      const uint64_t seq = sent[(size_t)b];
+      {
+        std::unique_lock<std::mutex> lk(g->mu);
+        FTN_CHECK(wait_for(lk, "the acknowledgement", b, [&] { return c.acked >= seq; }));
+      }
+      FTN_CUDA(cudaStreamWaitEvent(s, c.done, 0));
+    }
+    return FTN_OK;
+  }
+
+  ftn_status_t allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    std::vector<P2POp> ops;
+    for (int r = 0; r < g->n; ++r) {
+      if (r == rank) continue;
+      ops.push_back({true, const_cast<void*>(send), bytes, r});
+      ops.push_back({false, (char*)recv + (size_t)r * bytes, bytes, r});
+    }
+    if (bytes) FTN_CUDA(cudaMemcpyAsync((char*)recv + (size_t)rank * bytes, send, bytes, cudaMemcpyDefault, s));
+    return group(ops.data(), (int)ops.size(), s);
+  }
+
+  ftn_status_t bcast(void* buf, size_t bytes, int root, cudaStream_t s) override {
+    std::vector<P2POp> ops;
+    if (rank == root) {
+      for (int r = 0; r < g->n; ++r)
+        if (r != root) ops.push_back({true, buf, bytes, r});
+    } else {
+      ops.push_back({false, buf, bytes, root});
+    }
+    return group(ops.data(), (int)ops.size(), s);
+  }
+};
+
+}  // namespace
+}  // namespace ftn
+
+struct ftn_comm_s {
+  std::unique_ptr<ftn::Transport> tr;
+  int nranks, rank, device;
+  bool is_virtual = false;
+  int overlap = 1;                 // 0 off, 1 when nranks > 1, 2 always (ftn_comm_set_overlap)
+  int sm_reserve = 8;              // SMs left free by the interior sweeps while the exchange runs
+  cudaStream_t side = nullptr;     // interior sweeps while the halo exchange runs
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+};
+
+namespace ftn {
+size_t matmul_ws(const ftn_desc_t* a, const ftn_desc_t* b);
+ftn_status_t matmul_local(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, void* ws, size_t ws_bytes,
+                          cudaStream_t s);
+ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew);
+ftn_status_t jacobi_prepare();
+int jacobi_fuse_T();
+int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew);
+bool stencil_tma_able(const ftn_desc_t* d);
+ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
+                              int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
+                              cudaStream_t s);
+
+namespace {
+
+ftn_status_t comm_streams(ftn_comm_s* c) {
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess)
+    return fail(FTN_ERR_CUDA, "ftn_comm_init: stream / event creation failed");
+  return FTN_OK;
+}
+
+void comm_free(ftn_comm_s* c) {
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
 }
 
 ftn_status_t global_reduce(int kind, ftn_comm_t comm, const ftn_desc_t* x, const ftn_desc_t* y, void* result,
@@ -70,18 +291,110 @@ ftn_status_t global_reduce(int kind, ftn_comm_t comm, const ftn_desc_t* x, const
   void* local = w;
   void* gathered = w + 8;
   FTN_CHECK(reduce_local(kind, x, y, local, w + head, ws_bytes - head, s));
-  FTN_NCCL(ncclAllGather(local, gathered, 1, nccl_type(x->type), comm->nccl, s));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  FTN_CHECK(comm->tr->allgather(local, gathered, 8, s));
   return tree_combine_launch(kind, x->type, gathered, comm->nranks, result, s);
 }
 
+// Each last-dimension plane is one packed block (dims 1..r-1 packed column-major).
 bool plane_contiguous(const ftn_desc_t* d) {
   int64_t expect = d->elem_len;
   for (int k = 0; k < d->rank - 1; ++k) {
     if (d->dim[k].sm != expect) return false;
     expect *= d->dim[k].extent;
   }
-  return true;
+  return d->dim[d->rank - 1].sm > 0;
+}
+
+// The sends / receives that move the k planes [from, from + k) of `a` to / from `peer`: one
+// message for k adjacent planes, else one per plane (a padded leading dimension leaves gaps
+// between the planes of a 2-D slab).
+void plane_ops(std::vector<P2POp>& ops, bool send, const ftn_desc_t* a, int64_t from, int k, int peer) {
+  const int r = a->rank;
+  const int64_t sm = a->dim[r - 1].sm;
+  const size_t plane = (size_t)(desc_size(a) / a->dim[r - 1].extent) * (size_t)a->elem_len;
+  char* b = (char*)a->base_addr;
+  if ((size_t)sm == plane) {
+    ops.push_back({send, b + from * sm, plane * (size_t)k, peer});
+  } else {
+    for (int q = 0; q < k; ++q) ops.push_back({send, b + (from + q) * sm, plane, peer});
+  }
+}
+
+// Exchange of the k owned planes next to each neighbour into its k halo planes next to its
+// owned planes (array `a`, local planes [halo, nl - halo) owned).
+ftn_status_t halo_exchange(ftn_comm_t comm, const ftn_desc_t* a, int halo, int k, cudaStream_t s) {
+  if (comm->nranks == 1) return FTN_OK;
+  const int r = a->rank;
+  const int64_t nl = a->dim[r - 1].extent;
+  std::vector<P2POp> ops;
+  if (comm->rank > 0) {
+    plane_ops(ops, true, a, halo, k, comm->rank - 1);
+    plane_ops(ops, false, a, halo - k, k, comm->rank - 1);
+  }
+  if (comm->rank < comm->nranks - 1) {
+    plane_ops(ops, true, a, nl - halo - k, k, comm->rank + 1);
+    plane_ops(ops, false, a, nl - halo, k, comm->rank + 1);
+  }
+  NvtxRange r_("jacobi_dist halo exchange");
+  return comm->tr->group(ops.data(), (int)ops.size(), s);
+}
+
+ftn_status_t dist_check(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int32_t halo, const char* who) {
+  if (!comm) return fail(FTN_ERR_NULL, std::string(who) + ": comm NULL");
+  FTN_CHECK(jacobi_check(u, unew));
+  if (!plane_contiguous(u) || !plane_contiguous(unew))
+    return fail(FTN_ERR_UNSUPPORTED, std::string(who) + ": each last-dimension plane must be packed");
+  const int r = u->rank;
+  const int64_t nl = u->dim[r - 1].extent;
+  if (halo < 1 || nl - 2 * (int64_t)halo < 1)
+    return fail(FTN_ERR_SHAPE, std::string(who) + ": a slab needs >= 1 owned plane + halo planes on each side");
+  return FTN_OK;
+}
+
+// Sweeps per exchange: the local fusion factor for the slab (as ftn_jacobi), at most the
+// halo depth.
+int dist_T(const ftn_desc_t* u, const ftn_desc_t* unew, int32_t halo) {
+  int T = stencil_tma_able(u) && stencil_tma_able(unew) ? jacobi_fuse_for(u, unew) : 1;
+  return T > halo ? halo : T;
+}
+
+// The launches `plan` of the distributed DO nest starting from the array `*cur` (0: u holds
+// the newest iterate), each preceded by the exchange of its k planes; flips *cur per launch.
+ftn_status_t dist_run(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, const std::vector<int32_t>& plan,
+                      double coeff, int32_t halo, int* cur, cudaStream_t s) {
+  const int r = u->rank;
+  const int64_t nl = u->dim[r - 1].extent;
+  const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
+  const bool overlap = comm->overlap == 2 || (comm->overlap == 1 && comm->nranks > 1);
+  const int64_t lo = halo, hi = nl - halo - 1;
+  for (const int32_t k : plan) {
+    const ftn_desc_t* src = *cur ? unew : u;
+    const ftn_desc_t* dst = *cur ? u : unew;
+    // Overlap: the owned planes whose k-sweep dependence cone stays inside the owned planes,
+    // [lo + k, hi - k], are advanced on the side stream (leaving sm_reserve SMs for the
+    // exchange kernels) while the halos travel; the k planes next to each halo follow on the
+    // caller's stream after the exchange.
+    const bool split = overlap && hi - lo + 1 >= 4 * (int64_t)k;
+    if (split) {
+      NvtxRange r_("jacobi_dist interior (side stream)");
+      FTN_CUDA(cudaEventRecord(comm->ev_in, s));
+      FTN_CUDA(cudaStreamWaitEvent(comm->side, comm->ev_in, 0));
+      ScopedSmReserve reserve(comm->nranks > 1 ? comm->sm_reserve : 0);
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side));
+      FTN_CUDA(cudaEventRecord(comm->ev_out, comm->side));
+    }
+    FTN_CHECK(halo_exchange(comm, src, halo, k, s));
+    if (split) {
+      NvtxRange r_("jacobi_dist halo-adjacent planes");
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s));
+      FTN_CUDA(cudaStreamWaitEvent(s, comm->ev_out, 0));
+    } else {
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, hi, s));
+    }
+    *cur ^= 1;
+  }
+  return FTN_OK;
 }
 
 }  // namespace
@@ -108,23 +421,63 @@ ftn_status_t ftn_comm_init(ftn_comm_t* comm, int32_t nranks, int32_t rank, const
   FTN_CHECK(require_sm100());
   ncclUniqueId u;
   memcpy(&u, id, sizeof(u));
+  auto t = std::make_unique<NcclTransport>();
+  FTN_NCCL(ncclCommInitRank(&t->nccl, nranks, u, rank));
   ftn_comm_s* c = new ftn_comm_s();
+  c->tr = std::move(t);
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
-  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
-  if (r != ncclSuccess) {
-    delete c;
-    return nccl_fail(r, "ncclCommInitRank");
-  }
-  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess) {
-    ncclCommDestroy(c->nccl);
-    delete c;
-    return fail(FTN_ERR_CUDA, "ftn_comm_init: stream / event creation failed");
+  ftn_status_t st = comm_streams(c);
+  if (st != FTN_OK) {
+    comm_free(c);
+    return st;
   }
   *comm = c;
+  return FTN_OK;
+}
+
+ftn_status_t ftn_comm_init_virtual(ftn_comm_t* comms, int32_t nranks, const int32_t* devices) {
+  if (!comms || !devices) return fail(FTN_ERR_NULL, "ftn_comm_init_virtual: NULL argument");
+  if (nranks < 1 || nranks > 1024) return fail(FTN_ERR_SHAPE, "ftn_comm_init_virtual: nranks must be 1..1024");
+  int saved = 0;
+  FTN_CUDA(cudaGetDevice(&saved));
+  auto g = std::make_shared<VGroup>(nranks);
+  std::vector<ftn_comm_s*> made;
+  ftn_status_t st = FTN_OK;
+  for (int a = 0; a < nranks && st == FTN_OK; ++a) {
+    if (cudaSetDevice(devices[a]) != cudaSuccess) {
+      st = fail(FTN_ERR_DEVICE, "ftn_comm_init_virtual: bad device");
+      break;
+    }
+    st = require_sm100();
+    if (st != FTN_OK) break;
+    for (int b = 0; b < nranks && st == FTN_OK; ++b) {
+      VChannel& c = g->ch[(size_t)a * nranks + b];  // a's events live on a's device (ready); done on b's
+      if (cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming) != cudaSuccess)
+        st = fail(FTN_ERR_CUDA, "ftn_comm_init_virtual: event creation failed");
+    }
+    for (int b = 0; b < nranks && st == FTN_OK; ++b) {
+      VChannel& c = g->ch[(size_t)b * nranks + a];
+      if (cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming) != cudaSuccess)
+        st = fail(FTN_ERR_CUDA, "ftn_comm_init_virtual: event creation failed");
+    }
+    if (st != FTN_OK) break;
+    ftn_comm_s* c = new ftn_comm_s();
+    c->tr = std::make_unique<VirtualTransport>(g, a, devices[a]);
+    c->nranks = nranks;
+    c->rank = a;
+    c->device = devices[a];
+    c->is_virtual = true;
+    st = comm_streams(c);
+    made.push_back(c);
+  }
+  cudaSetDevice(saved);
+  if (st != FTN_OK) {
+    for (auto* c : made) comm_free(c);
+    return st;
+  }
+  for (int a = 0; a < nranks; ++a) comms[a] = made[(size_t)a];
   return FTN_OK;
 }
 
@@ -135,14 +488,16 @@ ftn_status_t ftn_comm_set_overlap(ftn_comm_t comm, int32_t mode) {
   return FTN_OK;
 }
 
+ftn_status_t ftn_comm_set_sm_reserve(ftn_comm_t comm, int32_t sms) {
+  if (!comm) return fail(FTN_ERR_NULL, "ftn_comm_set_sm_reserve: comm NULL");
+  if (sms < 0 || sms > 64) return fail(FTN_ERR_SHAPE, "ftn_comm_set_sm_reserve: 0..64 SMs");
+  comm->sm_reserve = sms;
+  return FTN_OK;
+}
+
 ftn_status_t ftn_comm_destroy(ftn_comm_t comm) {
   if (!comm) return FTN_OK;
-  if (comm->ev_in) cudaEventDestroy(comm->ev_in);
-  if (comm->ev_out) cudaEventDestroy(comm->ev_out);
-  if (comm->side) cudaStreamDestroy(comm->side);
-  ncclResult_t r = ncclCommDestroy(comm->nccl);
-  delete comm;
-  if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+  comm_free(comm);  // the transport's destructor releases the NCCL communicator / virtual group
   return FTN_OK;
 }
 
@@ -177,76 +532,18 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local, 
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
                              double coeff, int32_t halo, int32_t* result_in_unew, ftn_stream_t stream) {
   NvtxRange nvtx_("ftn_jacobi_dist");
-  if (!comm) return fail(FTN_ERR_NULL, "ftn_jacobi_dist: comm NULL");
-  FTN_CHECK(jacobi_check(u, unew));
-  if (!plane_contiguous(u) || !plane_contiguous(unew))
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_dist: last-dimension planes must be contiguous");
+  FTN_CHECK(dist_check(comm, u, unew, halo, "ftn_jacobi_dist"));
   if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: negative sweep count");
-  const int r = u->rank;
-  const int64_t nl = u->dim[r - 1].extent;
-  if (halo < 1 || nl - 2 * (int64_t)halo < 1)
-    return fail(FTN_ERR_SHAPE, "ftn_jacobi_dist: a slab needs >= 1 owned plane + halo planes on each side");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
-  cudaStream_t s = (cudaStream_t)stream;
-  // temporal blocking: up to T sweeps per exchange (rank 2: the fusion setting, rank 3: 2),
-  // at most the halo depth
-  int T = 1;
-  if (stencil_tma_able(u) && stencil_tma_able(unew)) {
-    T = r == 2 ? jacobi_fuse_T() : std::min(2, jacobi_fuse_T());
-    if (T > halo) T = halo;
-  }
+  // temporal blocking: up to T sweeps per exchange, at most the halo depth
+  const int T = dist_T(u, unew, halo);
   const int64_t nplan = ftn_jacobi_plan(sweeps, T, nullptr, 0);
   std::vector<int32_t> plan((size_t)nplan);
   ftn_jacobi_plan(sweeps, T, plan.data(), nplan);
-  const size_t plane = (size_t)(desc_size(u) / nl);
-  const int lower = comm->rank - 1, upper = comm->rank + 1;
-  const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
-  const bool overlap = comm->overlap == 2 || (comm->overlap == 1 && comm->nranks > 1);
-  const int64_t lo = halo, hi = nl - halo - 1;
-  int64_t launches = 0;
-  for (; launches < nplan; ++launches) {
-    const int k = plan[(size_t)launches];
-    const ftn_desc_t* src = (launches % 2 == 0) ? u : unew;
-    const ftn_desc_t* dst = (launches % 2 == 0) ? unew : u;
-    char* b = (char*)src->base_addr;
-    const int64_t sm = src->dim[r - 1].sm;
-    // Overlap: the owned planes whose k-sweep dependence cone stays inside the owned planes,
-    // [lo + k, hi - k], are advanced on the side stream while the halos travel; the k planes
-    // next to each halo follow on the caller's stream after the exchange.
-    const bool split = overlap && hi - lo + 1 >= 4 * (int64_t)k;
-    if (split) {
-      NvtxRange r_("jacobi_dist interior (side stream)");
-      FTN_CUDA(cudaEventRecord(comm->ev_in, s));
-      FTN_CUDA(cudaStreamWaitEvent(comm->side, comm->ev_in, 0));
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side));
-      FTN_CUDA(cudaEventRecord(comm->ev_out, comm->side));
-    }
-    if (comm->nranks > 1) {
-      NvtxRange r_("jacobi_dist halo exchange");
-      // the k owned planes next to each neighbour -> its k halo planes next to its owned planes
-      FTN_NCCL(ncclGroupStart());
-      if (lower >= 0) {
-        FTN_NCCL(ncclSend(b + halo * sm, plane * k, ncclFloat64, lower, comm->nccl, s));
-        FTN_NCCL(ncclRecv(b + (halo - k) * sm, plane * k, ncclFloat64, lower, comm->nccl, s));
-      }
-      if (upper < comm->nranks) {
-        FTN_NCCL(ncclSend(b + (nl - halo - k) * sm, plane * k, ncclFloat64, upper, comm->nccl, s));
-        FTN_NCCL(ncclRecv(b + (nl - halo) * sm, plane * k, ncclFloat64, upper, comm->nccl, s));
-      }
-      FTN_NCCL(ncclGroupEnd());
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
-    if (split) {
-      NvtxRange r_("jacobi_dist halo-adjacent planes");
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s));
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s));
-      FTN_CUDA(cudaStreamWaitEvent(s, comm->ev_out, 0));
-    } else {
-      FTN_CHECK(ftn_jacobi_slab(src, dst, k, coeff, halo, first, last, stream));
-    }
-  }
-  if (result_in_unew) *result_in_unew = (int32_t)(launches % 2);
+  int cur = 0;
+  FTN_CHECK(dist_run(comm, u, unew, plan, coeff, halo, &cur, (cudaStream_t)stream));
+  if (result_in_unew) *result_in_unew = cur;
   return FTN_OK;
 }
 
@@ -264,10 +561,7 @@ ftn_status_t ftn_bcast(ftn_comm_t comm, const ftn_desc_t* x, int32_t root, ftn_s
   FTN_CHECK(check_desc(x, "ftn_bcast(x)", 1, FTN_MAX_RANK));
   if (!desc_contiguous(x)) return fail(FTN_ERR_UNSUPPORTED, "ftn_bcast: array must be contiguous");
   if (root < 0 || root >= comm->nranks) return fail(FTN_ERR_SHAPE, "ftn_bcast: bad root");
-  FTN_NCCL(ncclBroadcast(x->base_addr, x->base_addr, (size_t)desc_size(x), nccl_type(x->type), root, comm->nccl,
-                         (cudaStream_t)stream));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return FTN_OK;
+  return comm->tr->bcast(x->base_addr, (size_t)desc_size(x) * (size_t)x->elem_len, root, (cudaStream_t)stream);
 }
 
 }  // extern "C"

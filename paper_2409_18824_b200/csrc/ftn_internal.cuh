@@ -46,7 +46,18 @@ extern std::atomic<uint64_t> g_launches;
 
 // FTN_ERR_DEVICE unless the current device is sm_100.
 ftn_status_t require_sm100();
+// SM count of the current device, minus the calling thread's reserve (ScopedSmReserve):
+// persistent grids are sized from it.
 int num_sms();
+// While alive, kernels this thread sizes by num_sms() leave n SMs free (e.g. for the NCCL
+// kernels of a halo exchange that runs concurrently on another stream).
+struct ScopedSmReserve {
+  explicit ScopedSmReserve(int n);
+  ~ScopedSmReserve();
+  ScopedSmReserve(const ScopedSmReserve&) = delete;
+  ScopedSmReserve& operator=(const ScopedSmReserve&) = delete;
+  int saved;
+};
 
 // ---------------------------------------------------------------- descriptors
 int64_t type_len(int32_t type);
@@ -183,6 +194,29 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// *slot = fmax(*slot, v) atomically (maxNum: a NaN v leaves the slot, a NaN slot takes v), for
+// the Jacobi residual MAXVAL(ABS(u_s - u_{s-1})) accumulated by the sweep kernels themselves.
+// fmax over non-negative values is exact and order-independent, so any accumulation order
+// gives the bits of the sequential fold.
+__device__ __forceinline__ void atomic_fmax_slot(double* slot, double v) {
+  if (v != v) return;
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
+  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(a);
+  for (;;) {
+    const double o = __longlong_as_double(old);
+    if (o == o && o >= v) return;
+    const unsigned long long prev = atomicCAS(a, old, __double_as_longlong(v));
+    if (prev == old) return;
+    old = prev;
+  }
+}
+// fmax over the 32 lanes of a warp (every lane gets the result)
+__device__ __forceinline__ double warp_fmax(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
 }
 
 // 256-bit global accesses (sm_100a, PTX 8.8)

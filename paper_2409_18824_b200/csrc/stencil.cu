@@ -482,7 +482,7 @@ int jacobi_fuse_T() {
     const char* e = getenv("FTN_JACOBI_FUSE");
     if (e) g_fuse_explicit.store(true);
     t = e ? atoi(e) : 5;
-    t = t < 1 ? 1 : (t > 6 ? 6 : t);
+    t = t < 1 ? 1 : (t > 8 ? 8 : t);
     g_fuse.store(t);
   }
   return t;
@@ -559,8 +559,8 @@ static bool padded_pair(const ftn_desc_t* u, const ftn_desc_t* unew, cudaStream_
 }
 
 extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
-  if (sweeps_per_launch < 1 || sweeps_per_launch > 6)
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..6 sweeps per launch");
+  if (sweeps_per_launch < 1 || sweeps_per_launch > 8)
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..8 sweeps per launch");
   g_fuse.store(sweeps_per_launch);
   g_fuse_explicit.store(true);
   return FTN_OK;

@@ -393,8 +393,12 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
 // T fused sweeps src -> dst (rank 2, TMA-able src) on output rows [row_lo, row_hi], with
 // rows <= fix_lo and >= fix_hi held fixed (the global boundary): see the header comment.
 // Input rows [row_lo - T, row_hi + T] are read.
+ftn_status_t jacobi2d_wq_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
+                              int64_t row_hi, int64_t fix_lo, int64_t fix_hi, double* res, cudaStream_t s);
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                                  int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
+  static const bool old = getenv("FTN_WF_OLD") && atoi(getenv("FTN_WF_OLD")) != 0;
+  if (!old || T > 6) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, nullptr, s);
   // FTN_WF_CFG selects a tuning variant for every T that has one; other T use the default
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
   int key = cfg < 0 ? T * 10 + 9 : T * 10 + cfg;

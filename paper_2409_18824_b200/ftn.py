@@ -16,7 +16,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libftn.so")
+# FTN_LIBFTN: load another build of the library (A/B timing of tuning variants, tools/variants.py)
+LIB_PATH = os.environ.get("FTN_LIBFTN") or os.path.join(_HERE, "libftn.so")
 
 I32, I64, F32, F64 = 1, 2, 3, 4
 ADD, SUB, MUL, DIV, MULADD = 1, 2, 3, 4, 5
@@ -93,6 +94,8 @@ def _load():
                           ctypes.c_int32],
         "ftn_comm_destroy": [vp],
         "ftn_comm_set_overlap": [vp, ctypes.c_int32],
+        "ftn_comm_set_sm_reserve": [vp, ctypes.c_int32],
+        "ftn_comm_init_virtual": [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
         "ftn_sum_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_maxval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
         "ftn_minval_global": [vp, P, vp, vp, ctypes.c_size_t, vp],
@@ -504,13 +507,28 @@ def launch_count() -> int:
 
 # ------------------------------------------------------------------------------ a8
 class Comm:
-    """An NCCL communicator for one rank (bootstrapped through torch.distributed)."""
+    """A communicator for one rank: NCCL (bootstrapped through torch.distributed), or one of
+    the virtual ranks of this process (Comm.virtual; each rank driven by its own thread)."""
 
-    def __init__(self, nranks: int, rank: int, uid: bytes, device: int):
+    def __init__(self, nranks: int, rank: int, uid: bytes | None, device: int, handle=None):
         self.nranks, self.rank, self.device = nranks, rank, device
+        if handle is not None:
+            self.handle = handle
+            return
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         self.handle = ctypes.c_void_p()
         _call("ftn_comm_init", ctypes.byref(self.handle), nranks, rank, buf, device)
+
+    @staticmethod
+    def virtual(nranks: int, devices=None) -> list["Comm"]:
+        """nranks virtual ranks in this process (ftn_comm_init_virtual), all on the current
+        device unless `devices` lists one device per rank."""
+        if devices is None:
+            devices = [torch.cuda.current_device()] * nranks
+        arr = (ctypes.c_void_p * nranks)()
+        devs = (ctypes.c_int32 * nranks)(*devices)
+        _call("ftn_comm_init_virtual", arr, nranks, devs)
+        return [Comm(nranks, r, None, devices[r], handle=ctypes.c_void_p(arr[r])) for r in range(nranks)]
 
     @staticmethod
     def unique_id() -> bytes:
@@ -534,6 +552,10 @@ class Comm:
     def set_overlap(self, mode: int):
         """Halo exchange / interior sweep overlap in jacobi(): 0 off, 1 when nranks > 1, 2 always."""
         _call("ftn_comm_set_overlap", self.handle, mode)
+
+    def set_sm_reserve(self, sms: int):
+        """SMs the side-stream interior sweeps leave free for the exchange kernels."""
+        _call("ftn_comm_set_sm_reserve", self.handle, sms)
 
     def _ws(self, x: FArray, stream=None) -> torch.Tensor:
         return workspace(reduce_workspace_size(x) + 8 * (self.nranks + 1) + 64, x.tensor.device, "global", stream)

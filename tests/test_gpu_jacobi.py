@@ -139,7 +139,7 @@ def test_c2_full_size_sampled(ftn):
         assert got == ref, (i, j)
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("shape", [(3, 3), (5, 40), (40, 5), (129, 31), (200, 301), (257, 77), (1000, 130)])
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 7, 8, 9])
 def test_2d_temporal_blocking(ftn, streaming, T, shape, sweeps):
@@ -156,7 +156,7 @@ def test_2d_temporal_blocking(ftn, streaming, T, shape, sweeps):
 
 def test_2d_temporal_blocking_long_strip(ftn):
     """Many units per CTA, uneven segments, 60 sweeps."""
-    for T in (2, 3, 4, 5, 6):
+    for T in (2, 3, 4, 5, 6, 7, 8):
         ftn.jacobi_set_fusion(T)
         u0 = synth.jacobi_init((3000, 2000), array_id=T)
         got, ref = _run_both(ftn, u0, 12, C2)
@@ -280,7 +280,7 @@ def test_error_paths_launch_nothing(ftn):
                            ftn.FArray.empty((20, 16), dtype=torch.float32), 1),  # real(4)
         lambda: ftn.jacobi_slab(U, W, 2, 1, True, True),                       # sweeps > halo
         lambda: ftn.jacobi_slab(U, W, 1, 8, True, True),                       # no owned plane
-        lambda: ftn.jacobi_set_fusion(7),
+        lambda: ftn.jacobi_set_fusion(9),
         lambda: ftn.jacobi_set_fusion(0),
     ]
     for f in cases:
@@ -303,7 +303,7 @@ def test_random_shapes_fusions_and_sweeps(ftn, streaming):
     rng = np.random.default_rng(2409)
     try:
         for it in range(40):
-            T = int(rng.integers(1, 7))
+            T = int(rng.integers(1, 9))
             ftn.jacobi_set_fusion(T)
             if it % 4 == 3:
                 shape = tuple(int(v) for v in rng.integers(3, 90, 3))
