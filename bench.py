@@ -139,6 +139,19 @@ def timed(torch, fn, steps, warmup, clocks=None, dist=None, counter=None):
     return t
 
 
+def c5_checksum(torch, ftn, R, p_lo, p_hi, comm):
+    """Decomposition-independent checksum of the C5 result: the integer SUM (mod 2^64, order
+    free) of the bit patterns of the global interior planes 2..2047 -- on one GPU the section
+    R(:, :, 2:2047), on N ranks the owned planes p_lo..p_hi of each slab, combined by the
+    global integer SUM.  Equal across N iff every owned value is bit-identical (the result is
+    the same whatever the slab count: R#16 + the exchange)."""
+    bits = ftn.FArray(R.tensor.view(torch.int64))
+    sec = bits.section((1, bits.shape[0]), (1, bits.shape[1]), (p_lo, p_hi))
+    v = comm.sum(sec) if comm is not None else ftn.sum(sec)
+    return {"kind": "SUM of int64 bit patterns of global planes 2..2047 (mod 2^64)",
+            "value": int(v.item()) & 0xFFFFFFFFFFFFFFFF}
+
+
 def jacobi_faces(ftn, U, n1, n2):
     """synth.jacobi_init recipe on the device: interior U[0,1), j=1 face 1.0, other faces 0."""
     ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
@@ -504,26 +517,45 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
     if "c5" in args.rows:
         n, sweeps = 2048, 100
         free = torch.cuda.mem_get_info()[0]
+        plane = n * n
+        checksum = None
         if not distmode:
             need = 2 * n ** 3 * 8
             if free > need + (2 << 30):
                 U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
                 ftn.gen_fill(U, SEED, 7, ftn.GEN_U01)
                 ftn.assign(W, U)
-                t = timed(torch, lambda: ftn.jacobi(U, W, sweeps), max(2, steps // 2), 1, ctx["clocks"], dist)
+                new = [False]
+
+                def c5_step():
+                    new[0] = ftn.jacobi(U, W, sweeps)
+                t = timed(torch, c5_step, max(2, steps // 2), 1, ctx["clocks"], dist)
                 interior = (n - 2) ** 3
-                del U, W
+                R = W if new[0] else U
+                checksum = c5_checksum(torch, ftn, R, 2, n - 1, None)
+                del U, W, R
             else:
                 t, interior = None, 0
         else:
             from paper_2409_18824_b200 import dist as D
-            g0, nl = D.jacobi_slab(n, N, rank, halo=2)   # 2 halo planes: 2 fused sweeps per exchange
+            halo = 2                                     # 2 halo planes: 2 fused sweeps per exchange
+            g0, nl = D.jacobi_slab(n, N, rank, halo=halo)
             U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
-            ftn.gen_fill(U, SEED, 7 + rank, ftn.GEN_U01)
+            # the global array's values where they live (decomposition-independent input):
+            # local plane q holds global plane g0 + q; planes beyond the global array are never read
+            q0, q1 = max(0, -g0), min(nl, n - g0)
+            ftn.fill(U, 0.0)
+            ftn.gen_fill(U.section((1, n), (1, n), (q0 + 1, q1)), SEED, 7, ftn.GEN_U01, t0=(g0 + q0) * plane)
             ftn.assign(W, U)
-            t = timed(torch, lambda: comm.jacobi(U, W, sweeps, halo=2), max(2, steps // 2), 1, ctx["clocks"], dist)
+            new = [False]
+
+            def c5_step():
+                new[0] = comm.jacobi(U, W, sweeps, halo=halo)
+            t = timed(torch, c5_step, max(2, steps // 2), 1, ctx["clocks"], dist)
             interior = (n - 2) ** 3
-            del U, W
+            R = W if new[0] else U
+            checksum = c5_checksum(torch, ftn, R, halo + 1, nl - halo, comm)
+            del U, W, R
         torch.cuda.empty_cache()
         if t:
             ns = max(2, steps // 2)
@@ -535,7 +567,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             rows["c5_jacobi3d_2048"] = {"value": gl, "unit": "GLUPS", "ms_per_sweep": t / ns / sweeps * 1e3,
                                         "launches_per_step": nl3,
                                         "roofline": {"bound": "hbm", "achieved_gbs_per_gpu": gbs,
-                                                     "frac": gbs / hbm_peak}}
+                                                     "frac": gbs / hbm_peak},
+                                        "checksum": checksum}
 
     # f4: pw-advection, three fields (k, j, i) = 2048 x 1024 x 1024 (R#26/R#27); at N > 1
     # every rank owns 1024/N i-planes plus one halo plane per side (inputs do not change

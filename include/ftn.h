@@ -226,16 +226,28 @@ ftn_status_t ftn_matmul_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_d
  *   for every interior point, then swap(u, unew).
  * u, unew: real(8), rank 2 (5-point) or rank 3 (7-point), conformable, not
  * overlapping.  Only interior points are written: the caller presets the
- * boundary of both arrays.  *result_in_unew (host) receives 1 when the final
+ * boundary of both arrays to the SAME values (R#16: then the swap equals u = unew; the
+ * fused kernels carry the source's ring through their intermediate sweeps).  *result_in_unew (host) receives 1 when the final
  * values are in unew (odd sweeps), else 0.  Bit-exact vs the oracle.
- * Arrays the TMA kernels cannot address (odd leading dimension, strided or reversed
- * sections) are, for sweeps >= 8, copied to padded packed temporaries, advanced there by the
- * temporally blocked kernels and copied back (both arrays; stream-ordered temporaries from
- * the device's default memory pool, whose release threshold the library raises so that
- * freed temporaries are reused); if the temporaries cannot be allocated the generic kernel
- * runs instead.  Results are identical either way. */
+ * Allocates nothing: arrays the TMA kernels cannot address (odd leading dimension, strided
+ * or reversed sections) run the generic one-point-per-thread kernel (see ftn_jacobi_ws for
+ * the faster path with a caller workspace).  Results are identical either way. */
 ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                         int32_t* result_in_unew, ftn_stream_t stream);
+
+/* Bytes of caller workspace with which ftn_jacobi_ws runs `sweeps` sweeps of these arrays
+ * through the temporally blocked kernels: 0 when u / unew are TMA-able (or sweeps < 8, or
+ * an extent is < 3), else two padded packed copies (even leading dimension).  Host-only. */
+ftn_status_t ftn_jacobi_workspace_size(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
+                                       size_t* bytes);
+
+/* ftn_jacobi with a caller workspace ws (256-byte aligned, or NULL): when ws_bytes >=
+ * ftn_jacobi_workspace_size(u, unew, sweeps) > 0, both arrays are copied into padded packed
+ * copies in ws, advanced there by the temporally blocked kernels and copied back (4 extra
+ * passes instead of `sweeps` passes of the generic kernel); otherwise as ftn_jacobi.  Same
+ * results and result array either way.  FTN_ERR_WORKSPACE for a misaligned ws. */
+ftn_status_t ftn_jacobi_ws(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
+                           void* ws, size_t ws_bytes, int32_t* result_in_unew, ftn_stream_t stream);
 
 /* Tuning (not semantics): rank-2 sweeps are executed up to T at a time by one kernel that
  * keeps the intermediate iterates in registers (temporal blocking, SURVEY §8(f) f2,
@@ -246,18 +258,6 @@ ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t swe
  * (their launches are latency bound, so fewer launches win).  Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
-
-/* Tuning (not semantics), opt-in: a rank-2 grid small enough for the aggregate shared memory
- * of the GPU (both iterates of a 1/num_SMs row slab plus K halo rows per side in <= 227 KB per
- * SM, e.g. the paper's 1024 x 1024) can be advanced by ftn_jacobi in ONE cooperative
- * launch when sweeps >= min_sweeps: each CTA keeps its rows resident, runs K
- * sweeps between exchanges of K boundary rows with its two neighbours only (flags in global
- * memory, no grid barrier).  Bit-identical results; the result array as for ftn_jacobi, the
- * other array holds iterate sweeps-1.  min_sweeps = 0 disables the path (the default, or
- * FTN_JACOBI_RES_MIN: on B200 it is slower than the streaming kernels at 1024^2, §4.6);
- * halo_depth K in 1..8, or 0 for the largest K <= 4 that fits.  Process-wide.  FTN_ERR_SHAPE
- * for a negative min_sweeps or K outside 0..8. */
-ftn_status_t ftn_jacobi_set_resident(int64_t min_sweeps, int32_t halo_depth);
 
 /* ftn_jacobi with the data on the host: host_u -> u (host-to-device copy), u -> unew
  * (device copy, presets the boundary of unew), `sweeps` sweeps, then the result -> host_result
@@ -278,11 +278,17 @@ int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, int64_t cap);
 
 /* Jacobi iteration to convergence (R#25): sweeps in blocks of
  * check_every (the last block may be shorter); after each block the residual
- * res = MAXVAL(ABS(u_s - u_{s-1})) of the last two iterates is computed on the device and
- * read back (one stream synchronisation per block); stop when res <= tol or after
- * max_sweeps.  *sweeps_done, *residual (0 when no sweep ran) and *result_in_unew are
+ * res = MAXVAL(ABS(u_s - u_{s-1})) of the last two iterates over the INTERIOR points (the
+ * points a sweep updates; -inf when there are none) is computed on the device and read back
+ * (one stream synchronisation per block); stop when res <= tol or after max_sweeps.  For
+ * rank-2 TMA-able arrays the residual is fused into the block's last launch (no extra pass
+ * over the arrays).  *sweeps_done, *residual (0 when no sweep ran) and *result_in_unew are
  * written on the host; the result is in unew iff sweeps_done is odd (as for ftn_jacobi).
- * ws: ftn_reduce_workspace_size(u) + 16 bytes, 8-byte aligned. */
+ * ws: 256-byte aligned, at least ftn_reduce_workspace_size(u) + 16 bytes; with
+ * ftn_jacobi_solve_workspace_size bytes, arrays the TMA kernels cannot address run on padded
+ * copies in ws (as ftn_jacobi_ws). */
+ftn_status_t ftn_jacobi_solve_workspace_size(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
+                                             int64_t check_every, size_t* bytes);
 ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
                               int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
                               int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
@@ -370,6 +376,19 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const f
                              int64_t sweeps, double coeff, int32_t halo, int32_t* result_in_unew,
                              ftn_stream_t stream);
 
+/* Distributed Jacobi to convergence (SURVEY §8(f) f2 with the a8 exchange; R#25): slabs as
+ * for ftn_jacobi_dist; blocks of check_every sweeps by its plan; each rank's residual
+ * MAXVAL(ABS(u_s - u_{s-1})) over its owned interior points (fused into the block's last
+ * launch for rank-2 TMA-able slabs), all-gathered; the global residual is the maximum of the
+ * p values (exact, so identical on every rank and equal to ftn_jacobi_solve's on the
+ * undivided array).  Stops when it is <= tol or after max_sweeps; one stream synchronisation
+ * per block.  ws: 8*(nranks+2) + ftn_reduce_workspace_size(u_local) bytes, 16-byte aligned.
+ * Outputs as for ftn_jacobi_solve; results bit-identical to it on the undivided array. */
+ftn_status_t ftn_jacobi_solve_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const ftn_desc_t* unew_local,
+                                   int32_t halo, int64_t max_sweeps, int64_t check_every, double tol,
+                                   double coeff, void* ws, size_t ws_bytes, int64_t* sweeps_done,
+                                   double* residual, int32_t* result_in_unew, ftn_stream_t stream);
+
 /* One local step of the distributed Jacobi without communication (for callers with their
  * own exchange, e.g. MPI): `sweeps` (1 <= sweeps <= halo) sweeps of the owned planes of a
  * slab laid out as for ftn_jacobi_dist whose halo planes are current, src -> dst.  Reads src
@@ -399,6 +418,10 @@ typedef enum { FTN_GEN_U01 = 1, FTN_GEN_U11 = 2, FTN_GEN_INT8 = 3, FTN_GEN_LINEA
                FTN_GEN_MOD1024 = 5, FTN_GEN_RAW = 6 } ftn_gen_mode_t;
 ftn_status_t ftn_gen_fill(const ftn_desc_t* dst, uint64_t seed, uint64_t array_id, int32_t mode,
                           ftn_stream_t stream);
+/* ftn_gen_fill with the sequence starting at element t0: element t of dst gets the value of
+ * element t0 + t (a slab of a larger array generated where it lives; mode 4/5 use t0 + t too). */
+ftn_status_t ftn_gen_fill_at(const ftn_desc_t* dst, uint64_t seed, uint64_t array_id, int32_t mode, uint64_t t0,
+                             ftn_stream_t stream);
 
 /* Number of kernels this library has launched in this process (all devices). */
 uint64_t ftn_launch_count(void);

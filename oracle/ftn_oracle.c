@@ -818,8 +818,29 @@ double orc_maxabsdiff_f64(const orc_array* x, const orc_array* y) {
   return r;
 }
 
+/* max |x - y| over the interior points of two conformable arrays (the section
+ * (lb+1 : ub-1) in every dimension): the points a Jacobi sweep updates (R#16, R#25).
+ * An empty interior gives -inf (R#10). */
+static double interior_maxabsdiff(const orc_array* x, const orc_array* y) {
+  int64_t lo[ORC_MAXRANK], hi[ORC_MAXRANK], st[ORC_MAXRANK];
+  orc_array ix, iy;
+  for (int d = 0; d < x->rank; ++d) {
+    lo[d] = x->dim[d].lb + 1;
+    hi[d] = x->dim[d].lb + x->dim[d].ext - 2;
+    st[d] = 1;
+  }
+  orc_section(x, lo, hi, st, &ix);
+  for (int d = 0; d < y->rank; ++d) {
+    lo[d] = y->dim[d].lb + 1;
+    hi[d] = y->dim[d].lb + y->dim[d].ext - 2;
+  }
+  orc_section(y, lo, hi, st, &iy);
+  return orc_maxabsdiff_f64(&ix, &iy);
+}
+
 /* Jacobi to convergence (R#25): the DO nest of orc_jacobi_f64 one sweep at a time; after
- * every check_every-th sweep (and after max_sweeps) res = max |u_s - u_{s-1}| over all points;
+ * every check_every-th sweep (and after max_sweeps) res = max |u_s - u_{s-1}| over the
+ * interior points (the points the sweep updates; the boundary rings are never changed);
  * stop when res <= tol. */
 int orc_jacobi_solve_f64(const orc_array* u, const orc_array* unew, int64_t max_sweeps, int64_t check_every,
                          double tol, double coeff, int64_t* sweeps_done, double* residual, int32_t* in_unew) {
@@ -834,7 +855,7 @@ int orc_jacobi_solve_f64(const orc_array* u, const orc_array* unew, int64_t max_
     const orc_array* t = a; a = b; b = t;   /* a holds u_s */
     ++s;
     if (s % check_every == 0 || s == max_sweeps) {
-      res = orc_maxabsdiff_f64(a, b);
+      res = interior_maxabsdiff(a, b);
       if (res <= tol) break;
     }
   }
@@ -847,21 +868,24 @@ int orc_jacobi_solve_f64(const orc_array* u, const orc_array* unew, int64_t max_
 /* ------------------------------------------------------------------------ */
 /* pw-advection (R#26): the 3-field advection stencil of the  */
 /* paper's pw-advection benchmark.  Its body is NOT in the paper;    */
-/* this is the public MONC-derived kernel as reproduced in DESIGN.md R#26, written as the */
-/* Fortran DO nest with the fields indexed (k, j, i) = dims (1, 2, 3), k contiguous:      */
+/* this is the MONC pw_advection kernel (advect_flow_fields) as reproduced in DESIGN.md   */
+/* R#26, written as the Fortran DO nest with the fields indexed (k, j, i) = dims (1, 2, 3), */
+/* k contiguous.  Every tendency is built in the same order: the x term (tcx), the y term  */
+/* (tcy), then the vertical term, whose two fluxes are differenced inside one parenthesis:  */
 /*   do i = 2, nx-1; do j = 2, ny-1; do k = 2, nz-1                                      */
 /*     su = tcx*(u(k,j,i-1)*(u(k,j,i)+u(k,j,i-1)) - u(k,j,i+1)*(u(k,j,i)+u(k,j,i+1)))    */
 /*     su = su + tcy*(u(k,j-1,i)*(v(k,j-1,i)+v(k,j-1,i+1)) - u(k,j+1,i)*(v(k,j,i)+v(k,j,i+1))) */
-/*     su = su + tzc1(k)*u(k-1,j,i)*(w(k-1,j,i)+w(k-1,j,i+1))                             */
-/*             - tzc2(k)*u(k+1,j,i)*(w(k,j,i)+w(k,j,i+1))                                 */
-/*     sv = tcy*(v(k,j-1,i)*(v(k,j,i)+v(k,j-1,i)) - v(k,j+1,i)*(v(k,j,i)+v(k,j+1,i)))    */
-/*     sv = sv + tcx*(v(k,j,i-1)*(u(k,j,i-1)+u(k,j+1,i-1)) - v(k,j,i+1)*(u(k,j,i)+u(k,j+1,i))) */
-/*     sv = sv + tzc1(k)*v(k-1,j,i)*(w(k-1,j,i)+w(k-1,j+1,i))                             */
-/*             - tzc2(k)*v(k+1,j,i)*(w(k,j,i)+w(k,j+1,i))                                 */
-/*     sw = tzd1(k)*w(k-1,j,i)*(w(k,j,i)+w(k-1,j,i)) - tzd2(k)*w(k+1,j,i)*(w(k,j,i)+w(k+1,j,i)) */
-/*     sw = sw + tcx*(w(k,j,i-1)*(u(k,j,i-1)+u(k+1,j,i-1)) - w(k,j,i+1)*(u(k,j,i)+u(k+1,j,i))) */
+/*     su = su + (tzc1(k)*u(k-1,j,i)*(w(k-1,j,i)+w(k-1,j,i+1))                            */
+/*              - tzc2(k)*u(k+1,j,i)*(w(k,j,i)+w(k,j,i+1)))                               */
+/*     sv = tcx*(v(k,j,i-1)*(u(k,j,i-1)+u(k,j+1,i-1)) - v(k,j,i+1)*(u(k,j,i)+u(k,j+1,i))) */
+/*     sv = sv + tcy*(v(k,j-1,i)*(v(k,j,i)+v(k,j-1,i)) - v(k,j+1,i)*(v(k,j,i)+v(k,j+1,i))) */
+/*     sv = sv + (tzc1(k)*v(k-1,j,i)*(w(k-1,j,i)+w(k-1,j+1,i))                            */
+/*              - tzc2(k)*v(k+1,j,i)*(w(k,j,i)+w(k,j+1,i)))                               */
+/*     sw = tcx*(w(k,j,i-1)*(u(k,j,i-1)+u(k+1,j,i-1)) - w(k,j,i+1)*(u(k,j,i)+u(k+1,j,i))) */
 /*     sw = sw + tcy*(w(k,j-1,i)*(v(k,j-1,i)+v(k+1,j-1,i)) - w(k,j+1,i)*(v(k,j,i)+v(k+1,j,i))) */
-/* Fortran evaluation: a*b*c = (a*b)*c, x + a - b = (x + a) - b; one rounding per operation. */
+/*     sw = sw + (tzd1(k)*w(k-1,j,i)*(w(k,j,i)+w(k-1,j,i))                                */
+/*              - tzd2(k)*w(k+1,j,i)*(w(k,j,i)+w(k+1,j,i)))                               */
+/* Fortran evaluation: a*b*c = (a*b)*c, x + (a - b) as parenthesised; one rounding per op. */
 /* Boundary points of su, sv, sw are not written.                                          */
 /* ------------------------------------------------------------------------ */
 int orc_pw_advection_f64(const orc_array* su, const orc_array* sv, const orc_array* sw, const orc_array* u,
@@ -879,38 +903,44 @@ int orc_pw_advection_f64(const orc_array* su, const orc_array* sv, const orc_arr
     for (int64_t j = 1; j < ny - 1; ++j)
       for (int64_t k = 1; k < nz - 1; ++k) {
         double a, b, s;
-        /* su */
+        /* su(k,j,i) = tcx*(u(k,j,i-1)*(u(k,j,i)+u(k,j,i-1)) - u(k,j,i+1)*(u(k,j,i)+u(k,j,i+1))) */
         a = ld3(u, k, j, i - 1) * (ld3(u, k, j, i) + ld3(u, k, j, i - 1));
         b = ld3(u, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k, j, i + 1));
         s = tcx * (a - b);
+        /* su = su + tcy*(u(k,j-1,i)*(v(k,j-1,i)+v(k,j-1,i+1)) - u(k,j+1,i)*(v(k,j,i)+v(k,j,i+1))) */
         a = ld3(u, k, j - 1, i) * (ld3(v, k, j - 1, i) + ld3(v, k, j - 1, i + 1));
         b = ld3(u, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k, j, i + 1));
         s = s + tcy * (a - b);
+        /* su = su + (tzc1(k)*u(k-1,j,i)*(w(k-1,j,i)+w(k-1,j,i+1)) - tzc2(k)*u(k+1,j,i)*(w(k,j,i)+w(k,j,i+1))) */
         a = (tzc1[k] * ld3(u, k - 1, j, i)) * (ld3(w, k - 1, j, i) + ld3(w, k - 1, j, i + 1));
         b = (tzc2[k] * ld3(u, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k, j, i + 1));
-        s = (s + a) - b;
+        s = s + (a - b);
         st3(su, k, j, i, s);
-        /* sv */
-        a = ld3(v, k, j - 1, i) * (ld3(v, k, j, i) + ld3(v, k, j - 1, i));
-        b = ld3(v, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k, j + 1, i));
-        s = tcy * (a - b);
+        /* sv(k,j,i) = tcx*(v(k,j,i-1)*(u(k,j,i-1)+u(k,j+1,i-1)) - v(k,j,i+1)*(u(k,j,i)+u(k,j+1,i))) */
         a = ld3(v, k, j, i - 1) * (ld3(u, k, j, i - 1) + ld3(u, k, j + 1, i - 1));
         b = ld3(v, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k, j + 1, i));
-        s = s + tcx * (a - b);
+        s = tcx * (a - b);
+        /* sv = sv + tcy*(v(k,j-1,i)*(v(k,j,i)+v(k,j-1,i)) - v(k,j+1,i)*(v(k,j,i)+v(k,j+1,i))) */
+        a = ld3(v, k, j - 1, i) * (ld3(v, k, j, i) + ld3(v, k, j - 1, i));
+        b = ld3(v, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k, j + 1, i));
+        s = s + tcy * (a - b);
+        /* sv = sv + (tzc1(k)*v(k-1,j,i)*(w(k-1,j,i)+w(k-1,j+1,i)) - tzc2(k)*v(k+1,j,i)*(w(k,j,i)+w(k,j+1,i))) */
         a = (tzc1[k] * ld3(v, k - 1, j, i)) * (ld3(w, k - 1, j, i) + ld3(w, k - 1, j + 1, i));
         b = (tzc2[k] * ld3(v, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k, j + 1, i));
-        s = (s + a) - b;
+        s = s + (a - b);
         st3(sv, k, j, i, s);
-        /* sw */
-        a = (tzd1[k] * ld3(w, k - 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k - 1, j, i));
-        b = (tzd2[k] * ld3(w, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k + 1, j, i));
-        s = a - b;
+        /* sw(k,j,i) = tcx*(w(k,j,i-1)*(u(k,j,i-1)+u(k+1,j,i-1)) - w(k,j,i+1)*(u(k,j,i)+u(k+1,j,i))) */
         a = ld3(w, k, j, i - 1) * (ld3(u, k, j, i - 1) + ld3(u, k + 1, j, i - 1));
         b = ld3(w, k, j, i + 1) * (ld3(u, k, j, i) + ld3(u, k + 1, j, i));
-        s = s + tcx * (a - b);
+        s = tcx * (a - b);
+        /* sw = sw + tcy*(w(k,j-1,i)*(v(k,j-1,i)+v(k+1,j-1,i)) - w(k,j+1,i)*(v(k,j,i)+v(k+1,j,i))) */
         a = ld3(w, k, j - 1, i) * (ld3(v, k, j - 1, i) + ld3(v, k + 1, j - 1, i));
         b = ld3(w, k, j + 1, i) * (ld3(v, k, j, i) + ld3(v, k + 1, j, i));
         s = s + tcy * (a - b);
+        /* sw = sw + (tzd1(k)*w(k-1,j,i)*(w(k,j,i)+w(k-1,j,i)) - tzd2(k)*w(k+1,j,i)*(w(k,j,i)+w(k+1,j,i))) */
+        a = (tzd1[k] * ld3(w, k - 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k - 1, j, i));
+        b = (tzd2[k] * ld3(w, k + 1, j, i)) * (ld3(w, k, j, i) + ld3(w, k + 1, j, i));
+        s = s + (a - b);
         st3(sw, k, j, i, s);
       }
   return ORC_OK;

@@ -17,7 +17,7 @@
 // fastest, round-robin (plan_units_halo).
 // Generic path (any strides): one thread per output point, direct loads.
 //
-// Arithmetic: exactly the DO-nest expression of R#26 in Fortran order ((a*b)*c, (x+a)-b), one
+// Arithmetic: exactly the DO-nest expression of R#26 in Fortran order ((a*b)*c, x+(a-b)), one
 // rounding per operation (-fmad=false), so results are bit-identical to the oracle.
 #include "ftn_internal.cuh"
 
@@ -74,7 +74,7 @@ template <class P>
 __device__ __forceinline__ void adv_point(const P& F, double tzc1, double tzc2, double tzd1, double tzd2, double tcx,
                                           double tcy, double& su, double& sv, double& sw) {
   double a, b, s;
-  // su
+  // su = tcx*(x flux) ; su = su + tcy*(y flux) ; su = su + (tzc1*(z flux in) - tzc2*(z flux out))
   a = F(0, 0, 0, -1) * (F(0, 0, 0, 0) + F(0, 0, 0, -1));
   b = F(0, 0, 0, 1) * (F(0, 0, 0, 0) + F(0, 0, 0, 1));
   s = tcx * (a - b);
@@ -83,27 +83,27 @@ __device__ __forceinline__ void adv_point(const P& F, double tzc1, double tzc2, 
   s = s + tcy * (a - b);
   a = (tzc1 * F(0, -1, 0, 0)) * (F(2, -1, 0, 0) + F(2, -1, 0, 1));
   b = (tzc2 * F(0, 1, 0, 0)) * (F(2, 0, 0, 0) + F(2, 0, 0, 1));
-  su = (s + a) - b;
-  // sv
-  a = F(1, 0, -1, 0) * (F(1, 0, 0, 0) + F(1, 0, -1, 0));
-  b = F(1, 0, 1, 0) * (F(1, 0, 0, 0) + F(1, 0, 1, 0));
-  s = tcy * (a - b);
+  su = s + (a - b);
+  // sv: the same three terms in the same order (x, y, z)
   a = F(1, 0, 0, -1) * (F(0, 0, 0, -1) + F(0, 0, 1, -1));
   b = F(1, 0, 0, 1) * (F(0, 0, 0, 0) + F(0, 0, 1, 0));
-  s = s + tcx * (a - b);
+  s = tcx * (a - b);
+  a = F(1, 0, -1, 0) * (F(1, 0, 0, 0) + F(1, 0, -1, 0));
+  b = F(1, 0, 1, 0) * (F(1, 0, 0, 0) + F(1, 0, 1, 0));
+  s = s + tcy * (a - b);
   a = (tzc1 * F(1, -1, 0, 0)) * (F(2, -1, 0, 0) + F(2, -1, 1, 0));
   b = (tzc2 * F(1, 1, 0, 0)) * (F(2, 0, 0, 0) + F(2, 0, 1, 0));
-  sv = (s + a) - b;
-  // sw
-  a = (tzd1 * F(2, -1, 0, 0)) * (F(2, 0, 0, 0) + F(2, -1, 0, 0));
-  b = (tzd2 * F(2, 1, 0, 0)) * (F(2, 0, 0, 0) + F(2, 1, 0, 0));
-  s = a - b;
+  sv = s + (a - b);
+  // sw: x, y, then the z term with tzd1 / tzd2
   a = F(2, 0, 0, -1) * (F(0, 0, 0, -1) + F(0, 1, 0, -1));
   b = F(2, 0, 0, 1) * (F(0, 0, 0, 0) + F(0, 1, 0, 0));
-  s = s + tcx * (a - b);
+  s = tcx * (a - b);
   a = F(2, 0, -1, 0) * (F(1, 0, -1, 0) + F(1, 1, -1, 0));
   b = F(2, 0, 1, 0) * (F(1, 0, 0, 0) + F(1, 1, 0, 0));
-  sw = s + tcy * (a - b);
+  s = s + tcy * (a - b);
+  a = (tzd1 * F(2, -1, 0, 0)) * (F(2, 0, 0, 0) + F(2, -1, 0, 0));
+  b = (tzd2 * F(2, 1, 0, 0)) * (F(2, 0, 0, 0) + F(2, 1, 0, 0));
+  sw = s + (a - b);
 }
 
 __device__ __forceinline__ double tz_at(const AdvParams& p, int q, int k) {

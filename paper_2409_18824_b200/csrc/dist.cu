@@ -259,7 +259,7 @@ int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew);
 bool stencil_tma_able(const ftn_desc_t* d);
 ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
                               int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
-                              cudaStream_t s);
+                              cudaStream_t s, double* res);
 
 namespace {
 
@@ -360,14 +360,18 @@ int dist_T(const ftn_desc_t* u, const ftn_desc_t* unew, int32_t halo) {
 
 // The launches `plan` of the distributed DO nest starting from the array `*cur` (0: u holds
 // the newest iterate), each preceded by the exchange of its k planes; flips *cur per launch.
+// res_last != nullptr: the last launch also folds MAXVAL(ABS(last two iterates)) over the
+// owned interior into that fmax slot (rank-2 TMA-able slabs).
 ftn_status_t dist_run(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, const std::vector<int32_t>& plan,
-                      double coeff, int32_t halo, int* cur, cudaStream_t s) {
+                      double coeff, int32_t halo, int* cur, cudaStream_t s, double* res_last = nullptr) {
   const int r = u->rank;
   const int64_t nl = u->dim[r - 1].extent;
   const int first = comm->rank == 0, last = comm->rank == comm->nranks - 1;
   const bool overlap = comm->overlap == 2 || (comm->overlap == 1 && comm->nranks > 1);
   const int64_t lo = halo, hi = nl - halo - 1;
-  for (const int32_t k : plan) {
+  for (size_t q = 0; q < plan.size(); ++q) {
+    const int32_t k = plan[q];
+    double* res = q + 1 == plan.size() ? res_last : nullptr;
     const ftn_desc_t* src = *cur ? unew : u;
     const ftn_desc_t* dst = *cur ? u : unew;
     // Overlap: the owned planes whose k-sweep dependence cone stays inside the owned planes,
@@ -380,17 +384,17 @@ ftn_status_t dist_run(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* un
       FTN_CUDA(cudaEventRecord(comm->ev_in, s));
       FTN_CUDA(cudaStreamWaitEvent(comm->side, comm->ev_in, 0));
       ScopedSmReserve reserve(comm->nranks > 1 ? comm->sm_reserve : 0);
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo + k, hi - k, comm->side, res));
       FTN_CUDA(cudaEventRecord(comm->ev_out, comm->side));
     }
     FTN_CHECK(halo_exchange(comm, src, halo, k, s));
     if (split) {
       NvtxRange r_("jacobi_dist halo-adjacent planes");
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s));
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, lo + k - 1, s, res));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, hi - k + 1, hi, s, res));
       FTN_CUDA(cudaStreamWaitEvent(s, comm->ev_out, 0));
     } else {
-      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, hi, s));
+      FTN_CHECK(jacobi_slab_part(src, dst, k, coeff, halo, first, last, lo, hi, s, res));
     }
     *cur ^= 1;
   }
@@ -543,6 +547,79 @@ ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_des
   ftn_jacobi_plan(sweeps, T, plan.data(), nplan);
   int cur = 0;
   FTN_CHECK(dist_run(comm, u, unew, plan, coeff, halo, &cur, (cudaStream_t)stream));
+  if (result_in_unew) *result_in_unew = cur;
+  return FTN_OK;
+}
+
+// Distributed Jacobi to convergence: blocks of check_every sweeps by
+// the plan of ftn_jacobi_dist; each rank's residual over its owned interior points (fused
+// into the block's last launch for rank-2 TMA-able slabs, else a single last sweep and a
+// MAXVAL(ABS(x - y)) pass over the owned interior section), all-gathered, and the maximum of
+// the p values (exact, identical on every rank) decides the stop.  One stream synchronisation
+// per block.
+ftn_status_t ftn_jacobi_solve_dist(ftn_comm_t comm, const ftn_desc_t* u, const ftn_desc_t* unew, int32_t halo,
+                                   int64_t max_sweeps, int64_t check_every, double tol, double coeff, void* ws,
+                                   size_t ws_bytes, int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
+                                   ftn_stream_t stream) {
+  NvtxRange nvtx_("ftn_jacobi_solve_dist");
+  FTN_CHECK(dist_check(comm, u, unew, halo, "ftn_jacobi_solve_dist"));
+  if (max_sweeps < 0 || check_every < 1)
+    return fail(FTN_ERR_SHAPE, "ftn_jacobi_solve_dist: need max_sweeps >= 0, check_every >= 1");
+  size_t rws = 0;
+  FTN_CHECK(ftn_reduce_workspace_size(u, &rws));
+  const size_t head = 8 * ((size_t)comm->nranks + 2);
+  if (!ws || ws_bytes < head + rws || ((uintptr_t)ws % 16))
+    return fail(FTN_ERR_WORKSPACE,
+                "ftn_jacobi_solve_dist: workspace must hold 8*(nranks+2) + ftn_reduce_workspace_size(u) bytes, 16-byte aligned");
+  FTN_CHECK(require_sm100());
+  FTN_CHECK(jacobi_prepare());
+  cudaStream_t s = (cudaStream_t)stream;
+  const int r = u->rank;
+  const int T = dist_T(u, unew, halo);
+  const bool fused_res = r == 2 && stencil_tma_able(u) && stencil_tma_able(unew);
+  double* slot = reinterpret_cast<double*>(ws);
+  double* gathered = slot + 2;
+  char* rw = reinterpret_cast<char*>(ws) + head;
+  // owned interior sections (local planes [halo, nl - halo), interior in the other dims)
+  ftn_desc_t iu, iw;
+  bool have_interior = true;
+  {
+    int64_t lo[3], hi[3], st[3] = {1, 1, 1};
+    for (int d = 0; d < r; ++d) {
+      const int64_t lb = u->dim[d].lower_bound, ext = u->dim[d].extent;
+      lo[d] = d == r - 1 ? lb + halo : lb + 1;
+      hi[d] = d == r - 1 ? lb + ext - halo - 1 : lb + ext - 2;
+      if (hi[d] < lo[d]) have_interior = false;
+    }
+    if (have_interior) {
+      FTN_CHECK(ftn_desc_section(&iu, u, lo, hi, st));
+      FTN_CHECK(ftn_desc_section(&iw, unew, lo, hi, st));
+    }
+  }
+  std::vector<double> host((size_t)comm->nranks);
+  int cur = 0;
+  int64_t done = 0;
+  double res = INFINITY;
+  while (done < max_sweeps) {
+    const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
+    FTN_CUDA(cudaMemsetAsync(slot, 0xff, sizeof(double), s));  // NaN: the empty fmax slot
+    const int64_t np = ftn_jacobi_plan(fused_res ? k : k - 1, T, nullptr, 0);
+    std::vector<int32_t> plan((size_t)np);
+    ftn_jacobi_plan(fused_res ? k : k - 1, T, plan.data(), np);
+    if (!fused_res) plan.push_back(1);  // consecutive iterates in u / unew for the residual pass
+    FTN_CHECK(dist_run(comm, u, unew, plan, coeff, halo, &cur, s, fused_res ? slot : nullptr));
+    if (!fused_res && have_interior) FTN_CHECK(ftn_maxval_absdiff(&iu, &iw, slot, rw, ws_bytes - head, stream));
+    FTN_CHECK(comm->tr->allgather(slot, gathered, 8, s));
+    FTN_CUDA(cudaMemcpyAsync(host.data(), gathered, 8 * (size_t)comm->nranks, cudaMemcpyDeviceToHost, s));
+    FTN_CUDA(cudaStreamSynchronize(s));
+    done += k;
+    res = -INFINITY;  // max over the ranks' values, empty (NaN) ones skipped: exact, the same on every rank
+    for (double v : host)
+      if (v == v && v > res) res = v;
+    if (res <= tol) break;
+  }
+  if (sweeps_done) *sweeps_done = done;
+  if (residual) *residual = done ? res : 0.0;
   if (result_in_unew) *result_in_unew = cur;
   return FTN_OK;
 }

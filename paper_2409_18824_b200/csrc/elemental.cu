@@ -36,6 +36,7 @@ struct EwParams {
   int64_t items;       // nchunk0 * e1 * e2
   // generator
   uint64_t key;
+  uint64_t t0;         // index of the first element in the generator's sequence
   int32_t mode;
 };
 
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(EW_THREADS, 6) ew_kernel(const __grid_constant
 #pragma unroll
       for (int e = 0; e < EW_GROUP; ++e) {
         if constexpr (OP == OP_GEN) {
-          const uint64_t t = (uint64_t)(i0 + e) + (uint64_t)p.e0 * (uint64_t)(i1 + p.e1 * i2);
+          const uint64_t t = p.t0 + (uint64_t)(i0 + e) + (uint64_t)p.e0 * (uint64_t)(i1 + p.e1 * i2);
           out[e] = gen_value<T>(p.key, p.mode, t);
         } else {
           out[e] = apply<T, OP, CONTRACT>(v[g][1][e], NOPS >= 2 ? v[g][2][e] : T(0), NOPS >= 3 ? v[g][3][e] : T(0));
@@ -242,7 +243,8 @@ ftn_status_t dispatch_op(int op, bool contract, const EwParams& p, bool vec, cud
 // Build params from dst + operands (operands may be rank 0 = device scalar or
 // value scalars passed via sval/sc) and launch.
 ftn_status_t run(int op, bool contract, const ftn_desc_t* dst, const ftn_desc_t* const* ops, int nops,
-                 const uint64_t* svals, const int* sc_override, uint64_t key, int mode, cudaStream_t stream) {
+                 const uint64_t* svals, const int* sc_override, uint64_t key, int mode, cudaStream_t stream,
+                 uint64_t t0 = 0) {
   EwParams p;
   memset(&p, 0, sizeof(p));
   const ftn_desc_t* arrays[4] = {dst, nullptr, nullptr, nullptr};
@@ -275,6 +277,7 @@ ftn_status_t run(int op, bool contract, const ftn_desc_t* dst, const ftn_desc_t*
   p.items = p.nchunk0 * p.e1 * p.e2;
   if (desc_size(dst) == 0) p.items = 0;
   p.key = key;
+  p.t0 = t0;
   p.mode = mode;
   // vector fast path: every array has unit-stride dim 0 and group-aligned rows
   const int64_t el = dst->elem_len, va = EW_GROUP * el;
@@ -381,6 +384,11 @@ ftn_status_t ftn_elemental(int32_t op, const ftn_desc_t* dst, const ftn_desc_t* 
 
 ftn_status_t ftn_gen_fill(const ftn_desc_t* dst, uint64_t seed, uint64_t array_id, int32_t mode,
                           ftn_stream_t stream) {
+  return ftn_gen_fill_at(dst, seed, array_id, mode, 0, stream);
+}
+
+ftn_status_t ftn_gen_fill_at(const ftn_desc_t* dst, uint64_t seed, uint64_t array_id, int32_t mode, uint64_t t0,
+                             ftn_stream_t stream) {
   FTN_CHECK(check_desc(dst, "ftn_gen_fill(dst)", 1, FTN_MAX_RANK));
   if (mode < FTN_GEN_U01 || mode > FTN_GEN_RAW) return fail(FTN_ERR_UNSUPPORTED, "ftn_gen_fill: mode");
   const bool is_real = dst->type == FTN_F32 || dst->type == FTN_F64;
@@ -389,7 +397,7 @@ ftn_status_t ftn_gen_fill(const ftn_desc_t* dst, uint64_t seed, uint64_t array_i
     return fail(FTN_ERR_TYPE, "ftn_gen_fill: U01/U11 are for real types");
   FTN_CHECK(require_sm100());
   const ftn_desc_t* ops[1] = {nullptr};
-  return run(OP_GEN, false, dst, ops, 0, nullptr, nullptr, seed ^ (array_id << 56), mode, (cudaStream_t)stream);
+  return run(OP_GEN, false, dst, ops, 0, nullptr, nullptr, seed ^ (array_id << 56), mode, (cudaStream_t)stream, t0);
 }
 
 }  // extern "C"

@@ -49,15 +49,11 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 }
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
-bool jacobi2d_resident_fits(const ftn_desc_t* u);
-int64_t jacobi_resident_min();
-ftn_status_t jacobi2d_resident_run(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
-                                   cudaStream_t s);
 ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s);
 ftn_status_t jacobi3d_fused2_planes(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t plane_lo,
                                     int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
-                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
+                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s, double* res);
 
 bool stencil_tma_able(const ftn_desc_t* d) {
   if (d->type != FTN_F64 || d->dim[0].sm != 8 || ((uintptr_t)d->base_addr % 16) != 0) return false;
@@ -530,20 +526,30 @@ static int64_t jacobi_pad_min() {
   return v > 0 ? v : INT64_MAX;
 }
 
-static bool padded_pair(const ftn_desc_t* u, const ftn_desc_t* unew, cudaStream_t s, StreamTemp& tu, StreamTemp& tw,
-                        ftn_desc_t* du, ftn_desc_t* dw) {
+// Bytes of the two padded packed copies (each 256-byte aligned); 0 when an extent is unsuitable.
+static size_t padded_bytes(const ftn_desc_t* u) {
   for (int d = 0; d < u->rank; ++d)
-    if (u->dim[d].extent < 3 || u->dim[d].extent >= (1ll << 31)) return false;
+    if (u->dim[d].extent < 3 || u->dim[d].extent >= (1ll << 31)) return 0;
   const int64_t n1 = u->dim[0].extent, ld = n1 + (n1 & 1);  // even leading dimension: 16-byte rows
   size_t elems = (size_t)ld;
   for (int d = 1; d < u->rank; ++d) elems *= (size_t)u->dim[d].extent;
-  if (tu.alloc(elems * 8, s) != FTN_OK || tw.alloc(elems * 8, s) != FTN_OK) {
-    cudaGetLastError();  // allocation failed: the caller takes the generic path
-    return false;
-  }
+  return 2 * ((elems * 8 + 255) / 256 * 256);
+}
+
+// The padded path applies: arrays the TMA kernels cannot address, enough sweeps.
+static bool padded_wanted(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps) {
+  return !(stencil_tma_able(u) && stencil_tma_able(unew)) && sweeps >= jacobi_pad_min() && padded_bytes(u) > 0;
+}
+
+// Padded packed copies du / dw of u / unew in the caller's workspace ws (padded_bytes(u)
+// bytes, 256-byte aligned); copies both in.
+static ftn_status_t padded_pair(const ftn_desc_t* u, const ftn_desc_t* unew, cudaStream_t s, char* ws,
+                                ftn_desc_t* du, ftn_desc_t* dw) {
+  const int64_t n1 = u->dim[0].extent, ld = n1 + (n1 & 1);
+  const size_t half = padded_bytes(u) / 2;
   for (ftn_desc_t* d : {du, dw}) {
     memset(d, 0, sizeof(*d));
-    d->base_addr = d == du ? tu.ptr : tw.ptr;
+    d->base_addr = d == du ? ws : ws + half;
     d->elem_len = 8;
     d->rank = u->rank;
     d->type = FTN_F64;
@@ -555,7 +561,20 @@ static bool padded_pair(const ftn_desc_t* u, const ftn_desc_t* unew, cudaStream_
       sm *= k == 0 ? ld : u->dim[k].extent;
     }
   }
-  return launch_copy(du, u, s) == FTN_OK && launch_copy(dw, unew, s) == FTN_OK;
+  FTN_CHECK(launch_copy(du, u, s));
+  return launch_copy(dw, unew, s);
+}
+
+// Interior section (lb+1 : ub-1 in every dimension) of a Jacobi array: the points a sweep
+// updates; false when it is empty.
+static bool interior_section(const ftn_desc_t* u, ftn_desc_t* out) {
+  int64_t lo[3], hi[3], st[3] = {1, 1, 1};
+  for (int d = 0; d < u->rank; ++d) {
+    if (u->dim[d].extent < 3) return false;
+    lo[d] = u->dim[d].lower_bound + 1;
+    hi[d] = u->dim[d].lower_bound + u->dim[d].extent - 2;
+  }
+  return ftn_desc_section(out, u, lo, hi, st) == FTN_OK;
 }
 
 extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
@@ -591,11 +610,25 @@ extern "C" int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, in
   return n;
 }
 
+extern "C" ftn_status_t ftn_jacobi_workspace_size(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps,
+                                                  size_t* bytes) {
+  FTN_CHECK(jacobi_check(u, unew));
+  if (!bytes) return fail(FTN_ERR_NULL, "ftn_jacobi_workspace_size: bytes NULL");
+  *bytes = padded_wanted(u, unew, sweeps) ? padded_bytes(u) : 0;
+  return FTN_OK;
+}
+
 extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
                                    int32_t* result_in_unew, ftn_stream_t stream) {
+  return ftn_jacobi_ws(u, unew, sweeps, coeff, nullptr, 0, result_in_unew, stream);
+}
+
+extern "C" ftn_status_t ftn_jacobi_ws(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t sweeps, double coeff,
+                                      void* ws, size_t ws_bytes, int32_t* result_in_unew, ftn_stream_t stream) {
   NvtxRange nvtx_("ftn_jacobi");
   FTN_CHECK(jacobi_check(u, unew));
   if (sweeps < 0) return fail(FTN_ERR_SHAPE, "ftn_jacobi: negative sweep count");
+  if (ws && ((uintptr_t)ws % 256)) return fail(FTN_ERR_WORKSPACE, "ftn_jacobi_ws: workspace must be 256-byte aligned");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
@@ -606,32 +639,21 @@ extern "C" ftn_status_t ftn_jacobi(const ftn_desc_t* u, const ftn_desc_t* unew, 
     FTN_CHECK(make_stencil_map(&mw, unew));
   }
   const int64_t nlast = u->dim[u->rank - 1].extent;
-  // Opt-in (ftn_jacobi_set_resident): grids that fit the aggregate shared memory (e.g. the
-  // paper's 1024^2), all sweeps in one cooperative launch with neighbour-only synchronisation
-  // (stencil_res.cu); same results, same result array, the other array holds iterate
-  // sweeps-1 as after the swapped DO nest.
-  const int64_t res_min = jacobi_resident_min();
-  if (u->rank == 2 && res_min > 0 && sweeps >= res_min && jacobi2d_resident_fits(u)) {
-    FTN_CHECK(jacobi2d_resident_run(u, unew, sweeps, coeff, s));
-    if (result_in_unew) *result_in_unew = (int32_t)(sweeps & 1);
-    return FTN_OK;
-  }
   // Arrays the TMA kernels cannot address (odd leading dimension, sections with a non-unit
-  // first stride or unaligned strides): for enough sweeps, run the temporally blocked kernels
-  // on padded packed copies (copy both arrays in, the sweeps, copy both back: 4 extra passes
+  // first stride or unaligned strides): for enough sweeps and a caller workspace of
+  // ftn_jacobi_workspace_size bytes, run the temporally blocked kernels on padded packed
+  // copies in the workspace (copy both arrays in, the sweeps, copy both back: 4 extra passes
   // instead of `sweeps` passes of the generic one-point-per-thread kernel).  Same results,
-  // same result array; falls back to the generic kernel if the temporaries do not fit.
-  if (!tma && sweeps >= jacobi_pad_min()) {
-    StreamTemp tu, tw;
+  // same result array; without the workspace the generic kernel runs.  Nothing is allocated.
+  if (padded_wanted(u, unew, sweeps) && ws && ws_bytes >= padded_bytes(u)) {
     ftn_desc_t du, dw;
-    if (padded_pair(u, unew, s, tu, tw, &du, &dw)) {
-      int32_t in_new = 0;
-      FTN_CHECK(ftn_jacobi(&du, &dw, sweeps, coeff, &in_new, stream));
-      FTN_CHECK(launch_copy(u, &du, s));
-      FTN_CHECK(launch_copy(unew, &dw, s));
-      if (result_in_unew) *result_in_unew = in_new;
-      return FTN_OK;
-    }
+    FTN_CHECK(padded_pair(u, unew, s, (char*)ws, &du, &dw));
+    int32_t in_new = 0;
+    FTN_CHECK(ftn_jacobi_ws(&du, &dw, sweeps, coeff, nullptr, 0, &in_new, stream));
+    FTN_CHECK(launch_copy(u, &du, s));
+    FTN_CHECK(launch_copy(unew, &dw, s));
+    if (result_in_unew) *result_in_unew = in_new;
+    return FTN_OK;
   }
   // Temporal blocking: launches of up to T fused sweeps (ftn_jacobi_plan).
   // Every launch swaps u/unew; the plan's launch count has the parity of `sweeps`, so the
@@ -685,13 +707,14 @@ extern "C" ftn_status_t ftn_jacobi_host(const double* host_u, double* host_resul
 namespace ftn {
 ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
                               int32_t halo, int32_t first, int32_t last, int64_t out_lo, int64_t out_hi,
-                              cudaStream_t s) {
+                              cudaStream_t s, double* res) {
   const int r = src->rank;
   const int64_t nl = src->dim[r - 1].extent;
   const bool tma = stencil_tma_able(src) && stencil_tma_able(dst);
   const int64_t lo = halo, hi = nl - halo - 1;
   if (out_lo > out_hi) return FTN_OK;
-  if (sweeps == 1) {
+  if (res && !(tma && r == 2)) return fail(FTN_ERR_UNSUPPORTED, "fused residual: rank-2 TMA-able slabs only");
+  if (sweeps == 1 && !res) {
     CUtensorMap m;
     const CUtensorMap* mp = nullptr;
     if (tma) {
@@ -707,7 +730,7 @@ ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int3
     const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
     return jacobi3d_fused2_planes(src, dst, coeff, out_lo, out_hi, flo, fhi, s);
   }
-  return jacobi2d_fused_rows(src, dst, sweeps, coeff, out_lo, out_hi, fix_lo, fix_hi, s);
+  return jacobi2d_fused_rows(src, dst, sweeps, coeff, out_lo, out_hi, fix_lo, fix_hi, s, res);
 }
 }  // namespace ftn
 
@@ -728,14 +751,75 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
                 "ftn_jacobi_slab: several sweeps per step need a TMA-able slab (rank 2: up to 6, rank 3: 2)");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
-  return jacobi_slab_part(src, dst, sweeps, coeff, halo, first, last, halo, nl - halo - 1, (cudaStream_t)stream);
+  return jacobi_slab_part(src, dst, sweeps, coeff, halo, first, last, halo, nl - halo - 1, (cudaStream_t)stream,
+                          nullptr);
 }
 
 // Jacobi iteration to convergence (R#25): blocks of check_every
-// sweeps, the last sweep of each block a single sweep so that the two arrays hold
-// consecutive iterates, then res = MAXVAL(ABS(u_s - u_{s-1})) (exact: a max of exactly
-// rounded differences); stop when res <= tol or after max_sweeps.  Synchronises the stream
-// once per block to read res.
+// sweeps, then res = MAXVAL(ABS(u_s - u_{s-1})) over the interior points (exact: a max of
+// exactly rounded differences); stop when res <= tol or after max_sweeps.  Rank-2 TMA-able
+// arrays: the block runs the plan of ftn_jacobi and its LAST launch (jacobi2d_wq) folds the
+// residual of its last two levels into an fmax slot as it stores them -- no extra pass over
+// the arrays.  Otherwise the block's last sweep is a single sweep (the two arrays then hold
+// consecutive iterates) followed by a MAXVAL(ABS(x - y)) pass over the interior sections.
+// Synchronises the stream once per block to read res.
+namespace ftn {
+// Workspace layout of the solve: [0, 16) the residual slot, [16, 16 + rws) the reduction
+// workspace, then (optionally, 256-byte aligned) the padded copies of ftn_jacobi_ws.
+static size_t solve_head(const ftn_desc_t* u) {
+  size_t rws = 0;
+  ftn_reduce_workspace_size(u, &rws);
+  return (16 + rws + 255) / 256 * 256;
+}
+
+// One block of k sweeps of the solve on the caller's stream; *cur flips per launch; the
+// block's residual is left in the device slot res_dev (NaN when the interior is empty).
+static ftn_status_t solve_block(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t k, int T, double coeff,
+                                double* res_dev, void* rw, size_t rw_bytes, int* cur, cudaStream_t s) {
+  const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
+  const int64_t nlast = u->dim[u->rank - 1].extent;
+  const bool fused_res = tma && u->rank == 2;
+  FTN_CUDA(cudaMemsetAsync(res_dev, 0xff, sizeof(double), s));  // NaN: the empty fmax slot
+  const int64_t np = ftn_jacobi_plan(fused_res ? k : k - 1, T, nullptr, 0);
+  std::vector<int32_t> plan((size_t)np);
+  ftn_jacobi_plan(fused_res ? k : k - 1, T, plan.data(), np);
+  if (!fused_res) plan.push_back(1);  // the last sweep alone: consecutive iterates in u / unew
+  for (size_t q = 0; q < plan.size(); ++q) {
+    const ftn_desc_t* src = *cur ? unew : u;
+    const ftn_desc_t* dst = *cur ? u : unew;
+    const int32_t kk = plan[q];
+    if (fused_res && q + 1 == plan.size()) {
+      FTN_CHECK(jacobi2d_fused_rows(src, dst, kk, coeff, 1, nlast - 2, 0, nlast - 1, s, res_dev));
+    } else if (kk >= 2) {
+      FTN_CHECK(jacobi_fused(src, dst, kk, coeff, s));
+    } else {
+      CUtensorMap m;
+      const CUtensorMap* mp = nullptr;
+      if (tma) {
+        FTN_CHECK(make_stencil_map(&m, src));
+        mp = &m;
+      }
+      FTN_CHECK(sweep(src, dst, mp, coeff, 1, nlast - 2, s));
+    }
+    *cur ^= 1;
+  }
+  if (!fused_res) {
+    ftn_desc_t iu, iw;
+    if (interior_section(u, &iu) && interior_section(unew, &iw))
+      FTN_CHECK(ftn_maxval_absdiff(&iu, &iw, res_dev, rw, rw_bytes, (ftn_stream_t)s));
+  }
+  return FTN_OK;
+}
+}  // namespace ftn
+
+extern "C" ftn_status_t ftn_jacobi_solve_workspace_size(const ftn_desc_t* u, const ftn_desc_t* unew,
+                                                        int64_t max_sweeps, int64_t check_every, size_t* bytes) {
+  FTN_CHECK(jacobi_check(u, unew));
+  if (!bytes) return fail(FTN_ERR_NULL, "ftn_jacobi_solve_workspace_size: bytes NULL");
+  *bytes = solve_head(u) + (padded_wanted(u, unew, max_sweeps) && check_every >= 3 ? padded_bytes(u) : 0);
+  return FTN_OK;
+}
+
 extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t max_sweeps,
                                          int64_t check_every, double tol, double coeff, void* ws, size_t ws_bytes,
                                          int64_t* sweeps_done, double* residual, int32_t* result_in_unew,
@@ -745,22 +829,22 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   if (max_sweeps < 0 || check_every < 1) return fail(FTN_ERR_SHAPE, "ftn_jacobi_solve: need max_sweeps >= 0, check_every >= 1");
   size_t rws = 0;
   FTN_CHECK(ftn_reduce_workspace_size(u, &rws));
-  if (!ws || ws_bytes < rws + 16 || ((uintptr_t)ws % 8))
-    return fail(FTN_ERR_WORKSPACE, "ftn_jacobi_solve: workspace must hold ftn_reduce_workspace_size(u) + 16 bytes");
+  if (!ws || ws_bytes < rws + 16 || ((uintptr_t)ws % 256))
+    return fail(FTN_ERR_WORKSPACE,
+                "ftn_jacobi_solve: workspace must hold ftn_reduce_workspace_size(u) + 16 bytes, 256-byte aligned");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tma = stencil_tma_able(u) && stencil_tma_able(unew);
-  if (!tma && max_sweeps >= jacobi_pad_min() && check_every >= 3) {  // as in ftn_jacobi
-    StreamTemp tu, tw;
+  // arrays the TMA kernels cannot address: padded copies in the workspace when it has room
+  const size_t head = solve_head(u);
+  if (padded_wanted(u, unew, max_sweeps) && check_every >= 3 && ws_bytes >= head + padded_bytes(u)) {
     ftn_desc_t du, dw;
-    if (padded_pair(u, unew, s, tu, tw, &du, &dw)) {
-      FTN_CHECK(ftn_jacobi_solve(&du, &dw, max_sweeps, check_every, tol, coeff, ws, ws_bytes, sweeps_done, residual,
-                                 result_in_unew, stream));
-      FTN_CHECK(launch_copy(u, &du, s));
-      FTN_CHECK(launch_copy(unew, &dw, s));
-      return FTN_OK;
-    }
+    FTN_CHECK(padded_pair(u, unew, s, (char*)ws + head, &du, &dw));
+    FTN_CHECK(ftn_jacobi_solve(&du, &dw, max_sweeps, check_every, tol, coeff, ws, head, sweeps_done, residual,
+                               result_in_unew, stream));
+    FTN_CHECK(launch_copy(u, &du, s));
+    FTN_CHECK(launch_copy(unew, &dw, s));
+    return FTN_OK;
   }
   const int T = jacobi_fuse_for(u, unew);
   double* res_dev = reinterpret_cast<double*>(ws);
@@ -768,39 +852,13 @@ extern "C" ftn_status_t ftn_jacobi_solve(const ftn_desc_t* u, const ftn_desc_t* 
   int cur = 0;  // 0: u holds the newest iterate
   int64_t done = 0;
   double res = INFINITY;
-  const int64_t nlast = u->dim[u->rank - 1].extent;
   while (done < max_sweeps) {
     const int64_t k = check_every < max_sweeps - done ? check_every : max_sweeps - done;
-    // the first k-1 sweeps by the plan of ftn_jacobi (launch count of their parity), then
-    // one single sweep, so the two arrays end up holding consecutive iterates
-    const int64_t np = ftn_jacobi_plan(k - 1, T, nullptr, 0);
-    std::vector<int32_t> plan((size_t)np);
-    ftn_jacobi_plan(k - 1, T, plan.data(), np);
-    int64_t left = 1;
-    for (int32_t kk : plan) {
-      if (kk >= 2) {
-        FTN_CHECK(jacobi_fused(cur ? unew : u, cur ? u : unew, kk, coeff, s));
-        cur ^= 1;
-      } else {
-        left += 1;
-      }
-    }
-    for (; left > 0; --left) {
-      const ftn_desc_t* src = cur ? unew : u;
-      const ftn_desc_t* dst = cur ? u : unew;
-      CUtensorMap m;
-      const CUtensorMap* mp = nullptr;
-      if (tma) {
-        FTN_CHECK(make_stencil_map(&m, src));
-        mp = &m;
-      }
-      FTN_CHECK(sweep(src, dst, mp, coeff, 1, nlast - 2, s));
-      cur ^= 1;
-    }
+    FTN_CHECK(solve_block(u, unew, k, T, coeff, res_dev, rw, ws_bytes - 16, &cur, s));
     done += k;
-    FTN_CHECK(ftn_maxval_absdiff(u, unew, res_dev, rw, ws_bytes - 16, stream));
     FTN_CUDA(cudaMemcpyAsync(&res, res_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
     FTN_CUDA(cudaStreamSynchronize(s));
+    if (res != res) res = -INFINITY;  // empty interior (R#10); NaN data are outside the parity inputs (R#11)
     if (res <= tol) break;
   }
   if (sweeps_done) *sweeps_done = done;

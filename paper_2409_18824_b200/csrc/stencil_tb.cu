@@ -395,10 +395,15 @@ ftn_status_t launch_wf(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
 // Input rows [row_lo - T, row_hi + T] are read.
 ftn_status_t jacobi2d_wq_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                               int64_t row_hi, int64_t fix_lo, int64_t fix_hi, double* res, cudaStream_t s);
+// res != nullptr: also fold MAXVAL(ABS(iterate T - iterate T-1)) over the stored points into
+// the fmax slot *res (jacobi2d_wq's fused residual).
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
-                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s) {
-  static const bool old = getenv("FTN_WF_OLD") && atoi(getenv("FTN_WF_OLD")) != 0;
-  if (!old || T > 6) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, nullptr, s);
+                                 int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s, double* res) {
+  if (res) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, res, s);
+  // jacobi2d_wq (stencil_wq.cu) for T = 7, 8, or for every T with FTN_WF_WQ=1: at T = 5 it
+  // measured 1215 vs 1602 GLUPS for jacobi2d_wf<5>, so wf is the default
+  static const bool wq = getenv("FTN_WF_WQ") && atoi(getenv("FTN_WF_WQ")) != 0;
+  if (wq || T > 6) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, nullptr, s);
   // FTN_WF_CFG selects a tuning variant for every T that has one; other T use the default
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
   int key = cfg < 0 ? T * 10 + 9 : T * 10 + cfg;
@@ -415,6 +420,8 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     // 4 CTAs x 4 warps per SM: 1570 GLUPS vs 1500 with a producer warp (3 CTAs x 5 warps)
     case 59: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 4, 1>>(WF_ARGS);
     case 69: return launch_wf<6, WFCfg<6, 4, 6, 4, 1>>(WF_ARGS);
+#ifdef FTN_WF_TUNING
+    // tuning variants (FTN_WF_CFG), compiled only into tuning builds (-DFTN_WF_TUNING)
     case 58: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3>>(WF_ARGS);   // producer warp, 3 CTAs/SM
     case 52: return launch_wf<5, WFCfg<5, 4, 6, 4, 1, 3, 1>>(WF_ARGS);  // no producer, 3 CTAs/SM (168 regs)
     case 53: return launch_wf<5, WFCfg<5, 4, 12, 3, 1, 3, 1>>(WF_ARGS); // 12-row boxes, 3 CTAs/SM
@@ -431,7 +438,6 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 55: return launch_wf<5, WFCfg<5, 4, 3, 8, 1, 3>>(WF_ARGS);
     case 67: return launch_wf<6, WFCfg<6, 4, 3, 8, 1, 3>>(WF_ARGS);
     case 66: return launch_wf<6, WFCfg<6, 3, 6, 4, 1, 4>>(WF_ARGS);
-    // tuning variants (FTN_WF_CFG)
     case 38: return launch_wf<3, WFCfg<3, 4, 12, 3, 2>>(WF_ARGS);   // lag 2: levels independent
     case 48: return launch_wf<4, WFCfg<4, 4, 12, 3, 2>>(WF_ARGS);
     case 37: return launch_wf<3, WFCfg<3, 4, 6, 6, 1>>(WF_ARGS);
@@ -448,6 +454,7 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
     case 43: return launch_wf<4, WFCfg<4, 4, 18, 3, 1>>(WF_ARGS);
     case 34: return launch_wf<3, WFCfg<3, 2, 12, 3, 1>>(WF_ARGS);
     case 44: return launch_wf<4, WFCfg<4, 2, 12, 3, 1>>(WF_ARGS);
+#endif
   }
 #undef WF_ARGS
   }
@@ -457,7 +464,7 @@ ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, i
 // The whole interior of a single array: rows 1 .. n2-2, boundary rows 0 and n2-1.
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s) {
   const int64_t n2 = src->dim[1].extent;
-  return jacobi2d_fused_rows(src, dst, T, coeff, 1, n2 - 2, 0, n2 - 1, s);
+  return jacobi2d_fused_rows(src, dst, T, coeff, 1, n2 - 2, 0, n2 - 1, s, nullptr);
 }
 
 }  // namespace ftn

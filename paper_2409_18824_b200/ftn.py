@@ -89,6 +89,13 @@ def _load():
         "ftn_matmul_ex_workspace_size": [P, P, P, ctypes.c_uint32, szp],
         "ftn_matmul_ex": [P, P, P, ctypes.c_uint32, vp, ctypes.c_size_t, vp],
         "ftn_jacobi": [P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
+        "ftn_jacobi_workspace_size": [P, P, ctypes.c_int64, szp],
+        "ftn_jacobi_ws": [P, P, ctypes.c_int64, ctypes.c_double, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int32),
+                          vp],
+        "ftn_jacobi_solve_workspace_size": [P, P, ctypes.c_int64, ctypes.c_int64, szp],
+        "ftn_jacobi_solve_dist": [vp, P, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                  ctypes.c_double, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
         "ftn_comm_init": [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8),
                           ctypes.c_int32],
@@ -106,8 +113,8 @@ def _load():
         "ftn_matmul_colsharded": [vp, P, P, P, vp, ctypes.c_size_t, vp],
         "ftn_bcast": [vp, P, ctypes.c_int32, vp],
         "ftn_gen_fill": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, vp],
+        "ftn_gen_fill_at": [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint64, vp],
         "ftn_jacobi_set_fusion": [ctypes.c_int32],
-        "ftn_jacobi_set_resident": [ctypes.c_int64, ctypes.c_int32],
         "ftn_jacobi_host": [vp, vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_pw_advection": [P, P, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_double, vp],
     }
@@ -416,7 +423,14 @@ def jacobi(u: FArray, unew: FArray, sweeps: int, coeff: float | None = None, str
     if coeff is None:
         coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
     r = ctypes.c_int32()
-    _call("ftn_jacobi", u.ref(), unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
+    n = ctypes.c_size_t()
+    _call("ftn_jacobi_workspace_size", u.ref(), unew.ref(), sweeps, ctypes.byref(n))
+    if n.value:   # arrays the TMA kernels cannot address: padded copies in a caller workspace
+        ws = workspace(n.value, u.tensor.device, "jacobi", stream)
+        _call("ftn_jacobi_ws", u.ref(), unew.ref(), sweeps, coeff, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+              ctypes.byref(r), _stream(stream))
+    else:
+        _call("ftn_jacobi", u.ref(), unew.ref(), sweeps, coeff, ctypes.byref(r), _stream(stream))
     return bool(r.value)
 
 
@@ -448,12 +462,6 @@ def jacobi_set_fusion(sweeps_per_launch: int):
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
 
 
-def jacobi_set_resident(min_sweeps: int, halo_depth: int = 0):
-    """SMEM-resident Jacobi for small rank-2 grids (one cooperative launch for all sweeps) when
-    sweeps >= min_sweeps (0 disables); halo_depth K = sweeps per neighbour exchange (0: auto)."""
-    _call("ftn_jacobi_set_resident", ctypes.c_int64(min_sweeps), halo_depth)
-
-
 def maxval_absdiff(x: FArray, y: FArray, out=None, stream=None) -> torch.Tensor:
     """MAXVAL(ABS(x - y)) without forming x - y."""
     res = out if out is not None else torch.empty((), dtype=x.dtype, device=x.tensor.device)
@@ -468,7 +476,9 @@ def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol
     """Jacobi to convergence (R#25): (sweeps done, last residual, result in unew)."""
     if coeff is None:
         coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
-    ws = workspace(reduce_workspace_size(u) + 64, u.tensor.device, "solve", stream)
+    n = ctypes.c_size_t()
+    _call("ftn_jacobi_solve_workspace_size", u.ref(), unew.ref(), max_sweeps, check_every, ctypes.byref(n))
+    ws = workspace(n.value, u.tensor.device, "solve", stream)
     done, res, new = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
     _call("ftn_jacobi_solve", u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff,
           ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(done), ctypes.byref(res), ctypes.byref(new),
@@ -497,8 +507,9 @@ def jacobi_plan(sweeps: int, T: int | None = None) -> list[int]:
     return list(buf[:n])
 
 
-def gen_fill(dst: FArray, seed: int, array_id: int, mode: int, stream=None):
-    _call("ftn_gen_fill", dst.ref(), seed & 0xFFFFFFFFFFFFFFFF, array_id, mode, _stream(stream))
+def gen_fill(dst: FArray, seed: int, array_id: int, mode: int, stream=None, t0: int = 0):
+    """Seeded synthetic values; t0: index of dst's first element in the sequence."""
+    _call("ftn_gen_fill_at", dst.ref(), seed & 0xFFFFFFFFFFFFFFFF, array_id, mode, t0, _stream(stream))
 
 
 def launch_count() -> int:
@@ -591,6 +602,19 @@ class Comm:
         _call("ftn_jacobi_dist", self.handle, u.ref(), unew.ref(), sweeps, coeff, halo, ctypes.byref(r),
               _stream(stream))
         return bool(r.value)
+
+    def jacobi_solve(self, u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol: float, coeff=None,
+                     halo: int = 1, stream=None) -> tuple[int, float, bool]:
+        """Distributed Jacobi to convergence (ftn_jacobi_solve_dist): (sweeps done, global residual,
+        result in unew), identical on every rank."""
+        if coeff is None:
+            coeff = JACOBI_C2 if u.rank == 2 else JACOBI_C3
+        ws = workspace(8 * (self.nranks + 2) + reduce_workspace_size(u), u.tensor.device, "solve_dist", stream)
+        done, res, new = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
+        _call("ftn_jacobi_solve_dist", self.handle, u.ref(), unew.ref(), halo, max_sweeps, check_every, tol, coeff,
+              ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(done), ctypes.byref(res), ctypes.byref(new),
+              _stream(stream))
+        return done.value, res.value, bool(new.value)
 
     def matmul(self, c_local: FArray, a_full: FArray, b_local: FArray, stream=None):
         ws = workspace(matmul_workspace_size(c_local, a_full, b_local), c_local.tensor.device, "matmul", stream)

@@ -45,6 +45,12 @@ def test_generator_matches_synth(ftn, mode):
     big = ftn.FArray.empty((1 << 20,))
     ftn.gen_fill(big, 7, 3, mode)
     np.testing.assert_array_equal(big.to_numpy(), synth.values(1 << 20, seed=7, array_id=3, mode=mode))
+    # a slab of a larger array generated where it lives (ftn_gen_fill_at): sequence offset t0
+    sl = ftn.FArray.empty((37, 41, 5))
+    t0 = 37 * 41 * 11
+    ftn.gen_fill(sl, synth.SEED, 5, mode, t0=t0)
+    np.testing.assert_array_equal(sl.to_numpy(), synth.values(37 * 41 * 5, array_id=5, mode=mode, start=t0)
+                                  .reshape((37, 41, 5), order="F"))
 
 
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])

@@ -21,11 +21,8 @@ def ftn():
 
 @pytest.fixture
 def streaming(ftn):
-    """The streaming (temporally blocked) kernels only: the SMEM-resident path for small grids
-    (tests/test_gpu_jacobi_resident.py) is switched off for the test."""
-    ftn.jacobi_set_resident(0)
+    """The streaming (temporally blocked) kernels (the only Jacobi path since round 2)."""
     yield
-    ftn.jacobi_set_resident(0)
 
 
 def _run_both(ftn, u0, sweeps, coeff, lbs=None):

@@ -30,7 +30,7 @@ def test_maxval_absdiff(ftn):
     assert got == np.max(np.abs(a[88::-2, ::3] - b[0:89:2, ::-3]))
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("shape,check,tol", [((130, 97), 5, 1e-3), ((130, 97), 7, -1.0), ((300, 200), 10, 1e-4),
                                              ((60, 50, 40), 4, 1e-3)])
 def test_jacobi_solve(ftn, T, shape, check, tol):
@@ -63,3 +63,49 @@ def test_jacobi_solve_non_tma_arrays(ftn, shape, sec):
     d2, r2, n2 = oracle.jacobi_solve(OA(ou).section(*osec), OA(ow).section(*osec), 40, 7, 1e-3, coeff)
     assert (done, res, new) == (d2, r2, n2)
     np.testing.assert_array_equal((sw if new else su).to_numpy(), (OA(ow) if n2 else OA(ou)).section(*osec).to_numpy())
+
+
+@pytest.mark.parametrize("T", [2, 5])
+@pytest.mark.parametrize("shape", [(2, 40), (40, 2), (3, 2, 9), (3, 3)])
+def test_jacobi_solve_degenerate_interiors(ftn, T, shape):
+    """R#25 / R#10: no interior point (or a single one): every block runs, the residual of an
+    empty interior is -inf (never <= tol = -1, so all max_sweeps run), equal to the oracle."""
+    ftn.jacobi_set_fusion(T)
+    try:
+        u0 = synth.jacobi_init(shape)
+        coeff = 0.25 if len(shape) == 2 else 1.0 / 6.0
+        U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+        got = ftn.jacobi_solve(U, W, 9, 4, -1.0, coeff)
+        a, b = u0.copy(order="F"), u0.copy(order="F")
+        ref = oracle.jacobi_solve(OA(a), OA(b), 9, 4, -1.0, coeff)
+        assert got == ref
+        np.testing.assert_array_equal(U.to_numpy(), a)
+        np.testing.assert_array_equal(W.to_numpy(), b)
+    finally:
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
+
+
+def test_jacobi_ws_allocates_nothing_without_workspace(ftn):
+    """ftn_jacobi on arrays the TMA kernels cannot address runs the generic kernel (no
+    temporaries); ftn_jacobi_ws with ftn_jacobi_workspace_size bytes runs the padded path;
+    both equal the oracle."""
+    import ctypes
+    u0 = synth.jacobi_init((131, 97))
+    coeff = 0.25
+    a, b = u0.copy(order="F"), u0.copy(order="F")
+    new_o = oracle.jacobi(OA(a), OA(b), 12, coeff)
+    ref = b if new_o else a
+    for use_ws in (False, True):
+        U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+        n = ctypes.c_size_t()
+        ftn._call("ftn_jacobi_workspace_size", U.ref(), W.ref(), 12, ctypes.byref(n))
+        assert n.value > 0
+        r = ctypes.c_int32()
+        if use_ws:
+            ws = ftn.workspace(n.value, slot="test_ws")
+            ftn._call("ftn_jacobi_ws", U.ref(), W.ref(), 12, coeff, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                      ctypes.byref(r), None)
+        else:
+            ftn._call("ftn_jacobi", U.ref(), W.ref(), 12, coeff, ctypes.byref(r), None)
+        assert bool(r.value) == new_o
+        np.testing.assert_array_equal((W if r.value else U).to_numpy(), ref)

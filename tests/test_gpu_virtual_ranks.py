@@ -265,3 +265,42 @@ def test_virtual_rank_errors(ftn):
         for c in comms:
             c.destroy()
     assert all(e is not None and e.name == "FTN_ERR_NCCL" for e in errs)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("shape,halo,check,tol", [
+    ((300, 203), 5, 10, 1e-3), ((130, 301), 3, 7, -1.0), ((200, 150), 1, 4, 2e-3), ((200, 160), 8, 9, 1e-4),
+    ((70, 40, 61), 2, 5, 1e-3), ((64, 33, 50), 1, 3, -1.0)])
+@pytest.mark.parametrize("overlap", [0, 2])
+def test_jacobi_solve_dist_virtual_vs_oracle(ftn, p, shape, halo, check, tol, overlap):
+    """ftn_jacobi_solve_dist at p virtual ranks == the oracle's solve on the undivided array:
+    sweeps done, the global residual (max over the ranks' owned interiors; fused into the last
+    launch of each block for 2-D slabs) and every owned plane bit for bit, the same on every
+    rank."""
+    coeff = C2 if len(shape) == 2 else C3
+    if shape[-1] - 2 < p:
+        pytest.skip("fewer interior planes than ranks")
+    u0 = synth.jacobi_init(shape, array_id=7 * p + len(shape))
+    a, b = u0.copy(order="F"), u0.copy(order="F")
+    d_o, r_o, n_o = oracle.jacobi_solve(OA(a), OA(b), 40, check, tol, coeff)
+    ref = b if n_o else a
+    slabs = slab_arrays(ftn, u0, p, halo)
+    comms = ftn.Comm.virtual(p)
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    out = [None] * p
+    try:
+        for c in comms:
+            c.set_overlap(overlap)
+
+        def rank(r):
+            (_, U), (_, W) = slabs[r][3]
+            out[r] = comms[r].jacobi_solve(U, W, 40, check, tol, coeff, halo=halo, stream=streams[r])
+            streams[r].synchronize()
+        run_ranks(p, rank)
+    finally:
+        for c in comms:
+            c.destroy()
+    assert all(o == (d_o, r_o, n_o) for o in out), (out, (d_o, r_o, n_o))
+    for (g0, nl, owned, pair) in slabs:
+        got = pair[1 if n_o else 0][1].to_numpy()
+        np.testing.assert_array_equal(got[..., halo:halo + owned], ref[..., g0 + halo:g0 + halo + owned])

@@ -175,3 +175,49 @@ def test_section_equals_packed():
     outs_p = _run(*packed, z)
     for s, p in zip(outs_sec, outs_p):
         np.testing.assert_array_equal(s.to_numpy()[1:-1, 1:-1, 1:-1], p[1:-1, 1:-1, 1:-1])
+
+
+def _order_case(field):
+    """Fields for which the Fortran statement order of R#26 decides the rounded result of one
+    output point (k0, j0, i0) of `field`; returns (fields, coefficients, tcx, tcy, expected).
+
+    Each tendency is x term, then y term, then the parenthesised vertical term
+    (tz1*flux_in - tz2*flux_out).  The cases put 2^53 into the vertical fluxes, where adding 1
+    is a round-half-even tie:
+      su, sv: x term = 1, y term = 0, both vertical fluxes = 2^53  ->  1 + (2^53 - 2^53) = 1
+              ((1 + 2^53) - 2^53 would give 0);
+      sw:     x term = 1, y term = 1, vertical term = 2^53 - 0     ->  (1 + 1) + 2^53 = 2^53 + 2
+              (2^53 first, then + 1 + 1, would give 2^53)."""
+    shape = (7, 7, 7)
+    nz = shape[0]
+    u, v, w = _field(shape), _field(shape), _field(shape)
+    tz = [np.zeros(nz), np.zeros(nz), np.zeros(nz), np.zeros(nz)]
+    i0 = j0 = k0 = 3
+    if field == "su":
+        # x: tcx*(u(i-1)*(u(i)+u(i-1)) - u(i+1)*(u(i)+u(i+1))) = 0.5*(1*2 - 0) = 1
+        u[:, :, i0 - 1] = 1.0
+        u[:, :, i0] = 1.0
+        w[:] = 1.0                          # y: v = 0 -> 0
+        tz[0][:] = tz[1][:] = 2.0 ** 52     # z: 2^52*u(k-1)*(1+1) = 2^52*u(k+1)*(1+1) = 2^53
+        return (u, v, w), tz, 0.5, 0.5, 1.0
+    if field == "sv":
+        # x: tcx*(v(i-1)*(u(i-1)+u(j+1,i-1)) - v(i+1)*(u(i)+u(j+1,i))) = 0.5*(1*2 - 1*0) = 1
+        u[:, :, i0 - 1] = 1.0
+        v[:] = 1.0                          # y: tcy*(1*(1+1) - 1*(1+1)) = 0
+        w[:] = 1.0
+        tz[0][:] = tz[1][:] = 2.0 ** 52     # z: 2^52*1*2 - 2^52*1*2
+        return (u, v, w), tz, 0.5, 0.5, 1.0
+    # sw
+    w[:] = 1.0
+    u[:, :, i0 - 1] = 1.0                   # x: 0.5*(1*(1+1) - 1*(0+0)) = 1
+    v[:, j0 - 1, :] = 1.0                   # y: 0.5*(1*(1+1) - 1*(0+0)) = 1
+    tz[2][:] = 2.0 ** 52                    # z: 2^52*1*(1+1) - 0 = 2^53
+    return (u, v, w), tz, 0.5, 0.5, 2.0 ** 53 + 2.0
+
+
+@pytest.mark.parametrize("field", ["su", "sv", "sw"])
+def test_statement_order_and_vertical_parenthesis(field):
+    (u, v, w), tz, tcx, tcy, expected = _order_case(field)
+    outs = _run(u, v, w, tz, tcx=tcx, tcy=tcy)
+    got = outs["su sv sw".split().index(field)][3, 3, 3]
+    assert got == expected, (field, got, expected)

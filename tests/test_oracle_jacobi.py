@@ -166,7 +166,7 @@ def test_solve_equals_fixed_sweeps_when_not_converging(orc):
     c, d = u.copy(order="F"), u.copy(order="F")
     orc.jacobi(FArray(c), FArray(d), 13, C2)
     np.testing.assert_array_equal(b, d)
-    assert res == np.max(np.abs(b - a))                 # last two iterates
+    assert res == np.max(np.abs(b[1:-1, 1:-1] - a[1:-1, 1:-1]))   # last two iterates, interior (R#25)
 
 
 def test_solve_harmonic_stops_at_first_check(orc):
@@ -186,3 +186,22 @@ def test_solve_residual_monotone_on_dyadic_data(orc):
         _, r, _ = orc.jacobi_solve(FArray(a), FArray(b), s, s, -1.0, C2)
         res.append(r)
     assert all(x >= y for x, y in zip(res, res[1:]))
+
+
+def test_solve_residual_is_over_the_interior(orc):
+    """R#25: the residual compares the last two iterates on the points a sweep updates.  With
+    different boundary rings in u and unew (each array keeps its own ring under the swap) the
+    ring differences do not enter; the iterates themselves come from the plain DO nest."""
+    u = synth.jacobi_init((23, 19))
+    w = u.copy(order="F")
+    w[0, :] += 100.0          # unew's ring differs from u's by 100 on one face
+    for s in (1, 2, 5, 6):
+        a, b = u.copy(order="F"), w.copy(order="F")
+        done, res, new = orc.jacobi_solve(FArray(a), FArray(b), s, s, -1.0, C2)
+        assert done == s and new == (s % 2 == 1)
+        c, d = u.copy(order="F"), w.copy(order="F")          # iterates s-1 and s by the DO nest
+        orc.jacobi(FArray(c), FArray(d), s, C2)
+        assert res == np.max(np.abs(d[1:-1, 1:-1] - c[1:-1, 1:-1])) < 100.0
+    e = np.zeros((2, 9), order="F")                           # no interior: -inf (R#10)
+    _, res, _ = orc.jacobi_solve(FArray(e.copy(order="F")), FArray(e.copy(order="F")), 3, 3, -1.0, C2)
+    assert res == -np.inf

@@ -30,16 +30,6 @@ def main(which):
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi2d_tma)
         ftn.jacobi_set_fusion(DEFAULT_FUSION)
         del U, W
-    if "resident" in which:
-        n = 1024
-        U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
-        ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
-        ftn.assign(W, U)
-        ftn.jacobi_set_resident(1, 0)
-        ftn.jacobi(U, W, 300)    # jacobi2d_resident: one cooperative launch for 300 sweeps
-        ftn.jacobi(U, W, 300)
-        ftn.jacobi_set_resident(0, 0)
-        del U, W
     if "jacobi3d" in which:
         n = 512
         U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))

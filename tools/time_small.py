@@ -17,22 +17,6 @@ def main():
     ftn.gen_fill(U, 18824, 0, ftn.GEN_U01)
     ftn.assign(W, U)
     lups = (n - 2) ** 2 * sweeps
-    # SMEM-resident path (one launch for all sweeps) per halo depth K, then the streaming kernels
-    for K in (1, 2, 3, 4):
-        ftn.jacobi_set_resident(1, K)
-        ftn.jacobi(U, W, sweeps)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n0 = ftn.launch_count()
-        a.record()
-        for _ in range(5):
-            ftn.jacobi(U, W, sweeps)
-        b.record()
-        torch.cuda.synchronize()
-        t = a.elapsed_time(b) / 5 / 1e3
-        print(f"n={n} resident K={K} launches={(ftn.launch_count() - n0) // 5} {lups / t / 1e9:.1f} GLUPS "
-              f"({t / sweeps * 1e6:.2f} us/sweep)", flush=True)
-    ftn.jacobi_set_resident(0, 0)
     for T in (1, 2, 3, 4, 5, 6):
         ftn.jacobi_set_fusion(T)
         for _ in range(2):
@@ -64,7 +48,6 @@ def main():
         print(f"n={n} T={T} launches={nl} stream {lups / t_stream / 1e9:.1f} GLUPS ({t_stream / nl * 1e6:.2f} us/launch)"
               f"  graph {lups / t_graph / 1e9:.1f} GLUPS ({t_graph / nl * 1e6:.2f} us/launch)", flush=True)
     ftn.jacobi_set_fusion(5)
-    ftn.jacobi_set_resident(0, 0)
 
 
 if __name__ == "__main__":
