@@ -638,31 +638,39 @@ def cpu_oracle_jacobi(budget_s=12.0, max_sweeps=100):
 
 
 def run_reference(args):
-    """--impl reference: the oracle timed on the host cores (no reference code base exists)."""
+    """--impl reference: the oracle (oracle/ftn_oracle.c, OpenMP over independent rows) timed on
+    the host cores on the SAME workload and config as the headline: each step is the full 100
+    sweeps of the 8192^2 grid (N = 1) or of the weak-scaled global grid 8192 x (8192 N + 2) that
+    the N GPUs advance together (N > 1).  Rank 0 alone runs it; no reference code base exists."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import numpy as np
     import oracle
     import synth
-    n = 8192
-    u = synth.jacobi_init((n, n))
+    N = max(1, args.gpus)
+    n, sweeps = 8192, 100
+    n2 = n if N == 1 else n * N + 2
+    u = synth.jacobi_init((n, n2))
     w = u.copy(order="F")
     U, Wd = oracle.FArray(u), oracle.FArray(w)
     for _ in range(args.warmup):
-        oracle.jacobi(U, Wd, 1, 0.25)
+        oracle.jacobi(U, Wd, 1, 0.25)        # warm-up: one sweep each (page-in, thread start)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.jacobi(U, Wd, 1, 0.25)      # each step: a bounded sample = 1 of the 100 sweeps
+        oracle.jacobi(U, Wd, sweeps, 0.25)   # one step = the full 100 sweeps
     t = time.perf_counter() - t0
-    glups = (n - 2) ** 2 * args.steps / t / 1e9
+    interior = (n - 2) * (n2 - 2)
+    glups = interior * sweeps * args.steps / t / 1e9
     cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     cpu = {"value": glups, "unit": "GLUPS", "cores": cores, "kind": "oracle",
-           "sample": "1 sweep of the 8192^2 grid per step (the workload is 100 sweeps)"}
+           "sample": f"the whole workload: {args.steps} steps of 100 sweeps of the {n}x{n2} grid, OpenMP over rows"}
     line = {"impl": "reference", "metric": METRIC, "value": glups, "unit": "GLUPS", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": CONFIG, "cpu_baseline": cpu,
+            "config": dict(CONFIG, parallelism=f"slab{N}" if N > 1 else "1 GPU",
+                           global_grid=f"{n}x{n2}"),
+            "cpu_baseline": cpu,
             "e2e": {"value": glups, "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     del np
     print(json.dumps(line), flush=True)

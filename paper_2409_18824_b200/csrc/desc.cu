@@ -214,20 +214,30 @@ StreamTemp::~StreamTemp() {
 
 ftn_status_t StreamTemp::alloc(size_t bytes, cudaStream_t s) {
   stream = s;
-  // Keep freed temporaries in the device's default stream-ordered pool instead of returning
-  // them to the driver at every synchronisation (the default release threshold is 0, which
-  // makes a large temporary cost a fresh mapping on every call).
-  static std::atomic<bool> pool_set[64] = {};
+  // Fortran-semantics temporaries (R#5: an overlapping assignment, TRANSPOSE or MATMUL result)
+  // come from a memory pool owned by this library, one per device: the device's default pool
+  // and the caller's allocator are left alone.  The pool keeps up to 256 MiB of freed blocks
+  // for reuse (small temporaries of repeated calls cost no new mapping) and returns anything
+  // above that to the driver at the next synchronisation.
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!pool_set[dev & 63].exchange(true)) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev & 63]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      FTN_CUDA(cudaMemPoolCreate(&pools[dev & 63], &props));
+      uint64_t keep = uint64_t(256) << 20;
+      FTN_CUDA(cudaMemPoolSetAttribute(pools[dev & 63], cudaMemPoolAttrReleaseThreshold, &keep));
     }
+    pool = pools[dev & 63];
   }
-  FTN_CUDA(cudaMallocAsync(&ptr, bytes > 0 ? bytes : 16, s));
+  FTN_CUDA(cudaMallocFromPoolAsync(&ptr, bytes > 0 ? bytes : 16, pool, s));
   return FTN_OK;
 }
 

@@ -295,10 +295,15 @@ def workspace(nbytes: int, device=None, slot: str = "main", stream=None) -> torc
     return buf
 
 
-def _as_operand(x, like: FArray):
+def _as_operand(x, like: FArray, stream=None):
+    """A Python scalar becomes a rank-0 device operand whose host-to-device copy and lifetime
+    are ordered on the stream the kernel runs on (the caching allocator then reuses its block
+    only after that stream's later work), not on whatever stream is current."""
     if isinstance(x, FArray):
         return x
-    return FArray.scalar(x, dtype=like.dtype, device=like.tensor.device)
+    st = stream if stream is not None else torch.cuda.current_stream(like.tensor.device)
+    with torch.cuda.stream(st):
+        return FArray.scalar(x, dtype=like.dtype, device=like.tensor.device)
 
 
 # ------------------------------------------------------------------------------ a3
@@ -316,8 +321,8 @@ def fill(dst: FArray, value, stream=None):
 
 def elemental(op: int, dst: FArray, a, b, c=None, contract: bool = False, stream=None):
     """dst = a op b, or dst = a*b + c for op == MULADD (scalars allowed as operands)."""
-    a, b = _as_operand(a, dst), _as_operand(b, dst)
-    c = _as_operand(c, dst) if c is not None else a
+    a, b = _as_operand(a, dst, stream), _as_operand(b, dst, stream)
+    c = _as_operand(c, dst, stream) if c is not None else a
     _call("ftn_elemental", op, dst.ref(), a.ref(), b.ref(), c.ref(), CONTRACT if contract else 0, _stream(stream))
 
 

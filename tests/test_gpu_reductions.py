@@ -50,7 +50,10 @@ def test_every_small_n(ftn):
     for n in range(0, 2101, 7):
         G = big.section((1, n)) if n > 0 else ftn.FArray.empty((0,))
         O = OA(v[:n].copy())
-        assert ftn.sum(G).item() == oracle.reduce_orderR(O, oracle.SUM), n
+        got = ftn.sum(G).item()
+        assert got == oracle.reduce_orderR(O, oracle.SUM), n
+        # and within the R#8 bound of the exactly rounded sum (independent of the R emulation)
+        assert abs(got - oracle.sum_exact(O)) <= 4 * max(n, 1) * U * oracle.sum_abs(O), n
         assert ftn.maxval(G).item() == oracle.maxval(O), n
 
 
@@ -183,7 +186,9 @@ def test_c4_full_size_order_r_bit_exact(ftn):
     ftn.gen_fill(x, synth.SEED, 10, ftn.GEN_U01)
     host = x.to_numpy()
     O = OA(host, [-511, 0, 1])
-    assert ftn.sum(x).item() == oracle.reduce_orderR(O, oracle.SUM)
+    got = ftn.sum(x).item()
+    assert got == oracle.reduce_orderR(O, oracle.SUM)
+    assert abs(got - oracle.sum_exact(O)) <= 4 * (1 << 30) * U * oracle.sum_abs(O)   # R#8, exact sum
     assert ftn.maxval(x).item() == oracle.maxval(O)
     assert ftn.minval(x).item() == oracle.minval(O)
     del x, host, O
