@@ -682,6 +682,16 @@ CONFIG = {"workload": "BASELINE configs[1]: 2-D 5-point Jacobi stencil, real(8) 
           "l2": "working set 2 x 512 MiB > 126 MB L2 (no flush needed)", "seed": SEED}
 
 
+def fused_kernel_name(sizes):
+    """The 2-D kernels of a launch plan ({sweeps per launch: count}): jacobi2d_wq<k> for k >= 7
+    (and any k under FTN_WF_WQ=1), jacobi2d_wf<k> for 2 <= k <= 6, jacobi2d_tma for k = 1."""
+    wq_all = os.environ.get("FTN_WF_WQ", "0") not in ("", "0")
+    names = []
+    for k in sorted((int(x) for x in sizes), reverse=True):
+        names.append("jacobi2d_tma" if k == 1 else (f"jacobi2d_wq<{k}>" if k >= 7 or wq_all else f"jacobi2d_wf<{k}>"))
+    return " + ".join(names)
+
+
 def traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "jacobi2d_traffic.json")
     try:
@@ -754,8 +764,7 @@ def main():
             "e2e": head.get("e2e"),
             "gpu_launches": head["launches"],
             "roofline": {"bound": "hbm",
-                         "kernel": (f"jacobi2d_wf<{head['plan']['max_sweeps_per_launch']}>"
-                                    if head["plan"]["max_sweeps_per_launch"] > 1 else "jacobi2d_tma"),
+                         "kernel": fused_kernel_name(head["plan"]["sweeps_per_launch"]),
                          "achieved": head["achieved_gbs"],
                          "peak": hbm_peak, "unit": "GB/s", "frac": frac, "peak_source": peak_src,
                          "traffic": traffic_from_profiles(),

@@ -466,10 +466,8 @@ ftn_status_t jacobi_check(const ftn_desc_t* u, const ftn_desc_t* unew) {
 
 static std::atomic<bool> g_attr_done[64] = {};  // per device (idempotent)
 
-// Sweeps fused per launch for 2-D arrays (1 = off, 2..6): ftn_jacobi_set_fusion, else the
-// FTN_JACOBI_FUSE environment variable, else 5 (measured on B200 at 8192^2 x 100 with the
-// register-ring kernel: T=2 ~640, T=3 955-975, T=4 1230-1254, T=5 1484-1501, T=6 1190-1330
-// GLUPS).
+// Sweeps fused per launch for 2-D arrays (1 = off, 2..12): ftn_jacobi_set_fusion, else the
+// FTN_JACOBI_FUSE environment variable, else a size-dependent default (jacobi_fuse_for).
 static std::atomic<int> g_fuse{0};
 static std::atomic<bool> g_fuse_explicit{false};  // set by ftn_jacobi_set_fusion or FTN_JACOBI_FUSE
 int jacobi_fuse_T() {
@@ -477,24 +475,27 @@ int jacobi_fuse_T() {
   if (t == 0) {
     const char* e = getenv("FTN_JACOBI_FUSE");
     if (e) g_fuse_explicit.store(true);
-    t = e ? atoi(e) : 5;
-    t = t < 1 ? 1 : (t > 8 ? 8 : t);
+    t = e ? atoi(e) : 8;
+    t = t < 1 ? 1 : (t > 12 ? 12 : t);
     g_fuse.store(t);
   }
   return t;
 }
 
 // Sweeps per launch for this array: T for TMA-able rank-2 arrays, 2 for TMA-able rank-3 arrays
-// (jacobi3d_tb2, when T >= 2), 1 otherwise.  Unless T was set explicitly, small rank-2 grids
-// (<= 2^21 points, e.g. the paper's 1024^2) use 6: a launch there is bound by the ~10-12 us of
-// per-launch latency, not by its work, so fewer launches win (1024^2: T=5 364, T=6 506 GLUPS;
-// 2048^2: equal).
+// (jacobi3d_tb2, when T >= 2), 1 otherwise.  Unless T was set explicitly, the rank-2 default
+// depends on the grid (measured on B200, DESIGN.md §4.3 / §4.6): > 2^23 points 8 (jacobi2d_wq:
+// 8192^2 x 100 1981 GLUPS vs 1600 at T = 5), <= 2^23 points 5 (2048^2: 929 vs 792 at 8),
+// <= 2^21 points 6 (1024^2: 548 vs 422 at 5; launches there are latency bound).
 int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
   int T = jacobi_fuse_T();
   if (T < 2 || !stencil_tma_able(u) || !stencil_tma_able(unew)) return 1;
   for (int d = 0; d < u->rank; ++d)
     if (u->dim[d].extent < 3) return 1;
-  if (u->rank == 2 && !g_fuse_explicit.load() && u->dim[0].extent * u->dim[1].extent <= (int64_t(1) << 21)) T = 6;
+  if (u->rank == 2 && !g_fuse_explicit.load()) {
+    const int64_t pts = u->dim[0].extent * u->dim[1].extent;
+    T = pts <= (int64_t(1) << 21) ? 6 : pts <= (int64_t(1) << 23) ? 5 : 8;
+  }
   return u->rank == 2 ? T : 2;
 }
 
@@ -578,8 +579,15 @@ static bool interior_section(const ftn_desc_t* u, ftn_desc_t* out) {
 }
 
 extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
-  if (sweeps_per_launch < 1 || sweeps_per_launch > 8)
-    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..8 sweeps per launch");
+  if (sweeps_per_launch == 0) {  // back to the default (FTN_JACOBI_FUSE, else size-dependent)
+    const char* e = getenv("FTN_JACOBI_FUSE");
+    int t = e ? atoi(e) : 8;
+    g_fuse.store(t < 1 ? 1 : (t > 12 ? 12 : t));
+    g_fuse_explicit.store(e != nullptr);
+    return FTN_OK;
+  }
+  if (sweeps_per_launch < 1 || sweeps_per_launch > 12)
+    return fail(FTN_ERR_UNSUPPORTED, "ftn_jacobi_set_fusion: 1..12 sweeps per launch");
   g_fuse.store(sweeps_per_launch);
   g_fuse_explicit.store(true);
   return FTN_OK;
@@ -587,26 +595,18 @@ extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
 
 extern "C" int32_t ftn_jacobi_get_fusion(void) { return jacobi_fuse_T(); }
 
-// Launch plan for S sweeps with at most T per launch: floor(S/T) launches of
-// T and one of S mod T; every launch swaps u/unew, so when the launch count does not have the
-// parity of S one T-launch is split into T-1 and 1 (or, for S < T, the single launch into
-// S-1 and 1).  Each entry is the number of sweeps of one launch.
+// Launch plan for S sweeps with at most T per launch: the fewest launches n
+// >= ceil(S/T) whose count has the parity of S (every launch swaps u/unew, so the result then
+// lands in unew iff S is odd), with the sweeps spread as evenly as possible over them (sizes
+// ceil(S/n) first, then floor(S/n)): no short launch that pays a whole HBM pass for one or two
+// sweeps.  Each entry is the number of sweeps of one launch.
 extern "C" int64_t ftn_jacobi_plan(int64_t sweeps, int32_t T, int32_t* sizes, int64_t cap) {
-  std::vector<int32_t> v;
   if (T < 1) T = 1;
-  for (int64_t i = 0; i < sweeps / T; ++i) v.push_back(T);
-  if (sweeps % T) v.push_back((int32_t)(sweeps % T));
-  if ((int64_t)(v.size() % 2) != sweeps % 2) {
-    // split the first launch with >= 2 sweeps: k -> (k - 1) + 1
-    for (size_t i = 0; i < v.size(); ++i)
-      if (v[i] >= 2) {
-        v[i] -= 1;
-        v.insert(v.begin() + i + 1, 1);
-        break;
-      }
-  }
-  const int64_t n = (int64_t)v.size();
-  for (int64_t i = 0; i < n && i < cap; ++i) sizes[i] = v[i];
+  if (sweeps <= 0) return 0;
+  int64_t n = (sweeps + T - 1) / T;
+  if ((n & 1) != (sweeps & 1)) ++n;  // n <= sweeps: when n = ceil(S/T) <= S has the wrong parity, n + 1 <= S
+  const int64_t q = sweeps / n, r = sweeps % n;  // r launches of q + 1, n - r of q
+  for (int64_t i = 0; i < n && i < cap; ++i) sizes[i] = (int32_t)(i < r ? q + 1 : q);
   return n;
 }
 

@@ -69,7 +69,7 @@ struct WQCfg {
   static constexpr int BOX = 128 * R * 8;      // bytes per box
   static constexpr int SMEM = NW * NS * BOX + NW * NS * 8 + 128;
   static constexpr int THREADS = NW * 32;
-  static_assert(T >= 1 && T <= 8, "1..8 sweeps per launch");
+  static_assert(T >= 1 && T <= 12, "1..12 sweeps per launch");
 };
 
 struct WQParams {
@@ -81,31 +81,81 @@ struct WQParams {
   int64_t nrows;    // output rows row_lo .. row_lo + nrows - 1
   int64_t fix_lo;   // rows <= fix_lo and >= fix_hi keep their value at every level
   int64_t fix_hi;
-  int64_t seg;      // output rows per unit
-  int64_t units;
+  // Flattened, weighted work split (no units of fixed size): the strips' rows are laid end to
+  // end, strip by strip, each row weighing w_edge (first / last strip: their windows touch the
+  // global boundary columns and run the select path) or w_in (every other strip); warp gw of
+  // the grid takes the rows whose weighted start lies in [gw*W/GW, (gw+1)*W/GW).  Every warp
+  // then carries the same weighted work -- one or two pieces (a row range of one strip) instead
+  // of a whole number of equal units, so neither wave quantisation nor the slower edge strips
+  // leave a straggler.
+  int64_t w_edge, w_in;   // row weights
+  int64_t W;              // total weight
+  int64_t GW;             // warps of the grid
   double coeff;
   double* res;      // RES: fmax slot of MAXVAL(ABS(L_T - L_{T-1})) over the stored points
 };
 
-// The box sequence of one warp: unit u (strip fastest), chunk q of the unit.
+__device__ __forceinline__ int64_t wq_ceil_div(int64_t a, int64_t b) { return a <= 0 ? 0 : (a + b - 1) / b; }
+
+// First weighted position of strip s (s in [0, strips]).
+__device__ __forceinline__ int64_t wq_strip_start(const WQParams& p, int64_t s) {
+  if (s <= 0) return 0;
+  if (s >= p.strips) return p.W;
+  return p.w_edge * p.nrows + (s - 1) * p.w_in * p.nrows;
+}
+
+// Strip holding weighted position x in [0, W).
+__device__ __forceinline__ int64_t wq_strip_of(const WQParams& p, int64_t x) {
+  const int64_t e = p.w_edge * p.nrows;
+  if (x < e) return 0;
+  const int64_t s = 1 + (x - e) / (p.w_in * p.nrows);
+  return s < p.strips - 1 ? s : p.strips - 1;
+}
+
+// Piece k of warp gw: strip c, output rows [ja, jb) (absolute positions in dim 2).  false:
+// no piece k; an empty piece (ja == jb) is possible and carries no rows.
+__device__ __forceinline__ bool wq_piece(const WQParams& p, int64_t gw, int64_t k, int64_t& c, int64_t& ja,
+                                         int64_t& jb) {
+  const int64_t A = gw * p.W / p.GW, B = (gw + 1) * p.W / p.GW;
+  if (A >= B) return false;
+  const int64_t s = wq_strip_of(p, A) + k;
+  if (s > wq_strip_of(p, B - 1)) return false;
+  const int64_t P0 = wq_strip_start(p, s), P1 = wq_strip_start(p, s + 1);
+  const int64_t w = (s == 0 || s == p.strips - 1) ? p.w_edge : p.w_in;
+  int64_t lo = wq_ceil_div(A - P0, w), hi = wq_ceil_div((B < P1 ? B : P1) - P0, w);
+  if (hi > p.nrows) hi = p.nrows;
+  if (lo > hi) lo = hi;
+  c = s;
+  ja = p.row_lo + lo;
+  jb = p.row_lo + hi;
+  return true;
+}
+
+// The box sequence of one warp: piece k of the warp, chunk q of the piece (pieces without
+// rows are skipped).
 template <class C>
 struct WQCursor {
-  int64_t u, q, nch, c, ja;
-  __device__ __forceinline__ void unit(const WQParams& p) {
-    c = u % p.strips;
-    ja = p.row_lo + (u / p.strips) * p.seg;
-    const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
-    nch = (jb - ja + 2 * C::T + C::R - 1) / C::R;
+  int64_t gw, k, q, nch, c, ja;
+  bool live;
+  __device__ __forceinline__ void find(const WQParams& p) {
+    int64_t jb;
+    for (;;) {
+      live = wq_piece(p, gw, k, c, ja, jb);
+      if (!live || jb > ja) break;
+      ++k;
+    }
+    if (live) nch = (jb - ja + 2 * C::T + C::R - 1) / C::R;
     q = 0;
   }
-  __device__ __forceinline__ void start(const WQParams& p, int64_t gw) {
-    u = gw;
-    if (u < p.units) unit(p);
+  __device__ __forceinline__ void start(const WQParams& p, int64_t gw_) {
+    gw = gw_;
+    k = 0;
+    find(p);
   }
-  __device__ __forceinline__ void advance(const WQParams& p, int64_t GW) {
-    if (u < p.units && ++q == nch) {
-      u += GW;
-      if (u < p.units) unit(p);
+  __device__ __forceinline__ void advance(const WQParams& p) {
+    if (live && ++q == nch) {
+      ++k;
+      find(p);
     }
   }
   __device__ __forceinline__ void issue(const CUtensorMap* map, uint8_t* ring, uint64_t* full, int s) const {
@@ -137,23 +187,21 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wq(const __grid_
   // nothing of this grid touches global memory before the previous grid has completed
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int64_t GW = (int64_t)gridDim.x * C::NW;
   const int64_t gw = (int64_t)blockIdx.x * C::NW + warp;
   WQCursor<C> icur;  // NS boxes ahead of the consumed one
   icur.start(p, gw);
   if (lane == 0) dev::prefetch_tma(&src_map);
   for (int s = 0; s < NS; ++s) {
-    if (lane == 0 && icur.u < p.units) icur.issue(&src_map, ring, full, s);
-    icur.advance(p, GW);
+    if (lane == 0 && icur.live) icur.issue(&src_map, ring, full, s);
+    icur.advance(p);
   }
   const uint32_t ring_off = (uint32_t)(ring - smem_raw);
   const double coeff = p.coeff;
   double rmax = __longlong_as_double(0x7ff8000000000000ll);  // RES: fmax over this lane's stored points
   int64_t k = 0;  // boxes consumed by this warp
-  for (int64_t u = gw; u < p.units; u += GW) {
-    const int64_t c = u % p.strips;
-    const int64_t ja = p.row_lo + (u / p.strips) * p.seg;
-    const int64_t jb = min(ja + p.seg, p.row_lo + p.nrows);
+  int64_t c, ja, jb;
+  for (int64_t pk = 0; wq_piece(p, gw, pk, c, ja, jb); ++pk) {
+    if (jb <= ja) continue;
     const int nr = (int)(jb - ja) + 2 * T;       // input rows, relative 0 .. nr-1 (global ja - T + r)
     const int64_t gcol0 = c * C::WO - C::H;       // global column of window column 0
     const int64_t g0 = gcol0 + 4 * lane;          // global column of this lane's first column
@@ -252,11 +300,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) jacobi2d_wq(const __grid_
       else
         chunk(st, s0, false);
       __syncwarp();
-      if (lane == 0 && icur.u < p.units) {
+      if (lane == 0 && icur.live) {
         dev::fence_proxy_async();  // this warp's reads of the slot precede the TMA overwrite
         icur.issue(&src_map, ring, full, sl);
       }
-      icur.advance(p, GW);
+      icur.advance(p);
     }
   }
   if (RES) {
@@ -326,21 +374,18 @@ ftn_status_t launch_wq(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     if (occ < 1) occ = 1;
     occ_cache[dev & 63].store(occ);
   }
-  const int64_t warps = (int64_t)num_sms() * occ * C::NW;
-  struct PlanEntry {
-    int64_t strips = -1, nrows, warps, seg, units;
-  };
-  thread_local PlanEntry pc;
-  if (pc.strips == p.strips && pc.nrows == p.nrows && pc.warps == warps) {
-    p.seg = pc.seg;
-    p.units = pc.units;
-  } else {
-    plan_units_halo(p.strips, p.nrows, warps, 2 * C::T, &p.seg, &p.units);
-    pc = {p.strips, p.nrows, warps, p.seg, p.units};
-  }
+  // one persistent wave: every resident warp takes an equal share of the weighted rows
   int64_t grid = (int64_t)num_sms() * occ;
-  const int64_t need = (p.units + C::NW - 1) / C::NW;
-  if (grid > need) grid = need;
+  const int64_t need = (p.strips * p.nrows + 63) / 64;  // at least ~64 rows per CTA's warps
+  if (grid > need) grid = need < 1 ? 1 : need;
+  p.GW = grid * C::NW;
+  // row weights: edge strips run the select path (FTN_WQ_EDGE_W = its cost in 1/8 of an
+  // interior row; measured at 8192^2, T = 8: 8 -> 1521, 12 -> 1852, 16 -> 1924-1930,
+  // 20 -> 1908, 24 -> 1878 GLUPS)
+  static const int64_t w_edge = getenv("FTN_WQ_EDGE_W") ? atoll(getenv("FTN_WQ_EDGE_W")) : 16;
+  p.w_in = 8;
+  p.w_edge = w_edge > 0 ? w_edge : 8;
+  p.W = (p.strips == 1 ? p.w_edge : 2 * p.w_edge + (p.strips - 2) * p.w_in) * p.nrows;
   static const bool pdl = !getenv("FTN_WF_PDL") || atoi(getenv("FTN_WF_PDL")) != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -377,10 +422,16 @@ ftn_status_t jacobi2d_wq_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int 
     WQ_CASE(6, FTN_WQ_MINB_MID)
     WQ_CASE(7, FTN_WQ_MINB_HI)
     WQ_CASE(8, FTN_WQ_MINB_HI)
+#ifdef FTN_WQ_BIG_T
+    WQ_CASE(9, FTN_WQ_MINB_HI)
+    WQ_CASE(10, FTN_WQ_MINB_HI)
+    WQ_CASE(11, FTN_WQ_MINB_HI)
+    WQ_CASE(12, FTN_WQ_MINB_HI)
+#endif
   }
 #undef WQ_CASE
 #undef WQ_ARGS
-  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_wq: T must be 1..8");
+  return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_wq: T must be 1..8 (1..12 in -DFTN_WQ_BIG_T builds)");
 }
 
 }  // namespace ftn

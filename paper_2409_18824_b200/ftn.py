@@ -463,7 +463,8 @@ def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FA
 
 
 def jacobi_set_fusion(sweeps_per_launch: int):
-    """Temporal-blocking factor of the Jacobi kernels (1..6, default 5; 3-D uses min(T, 2)); results are identical."""
+    """Temporal-blocking factor of the Jacobi kernels (1..12, 0 = the size-dependent default; 3-D uses
+    min(T, 2)); results are identical."""
     _call("ftn_jacobi_set_fusion", sweeps_per_launch)
 
 

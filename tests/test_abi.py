@@ -101,15 +101,17 @@ def test_compute_calls_validate_before_device(ftn):
 
 
 def test_jacobi_launch_plan(ftn):
-    """ftn_jacobi_plan (host logic): sweep counts sum to S, each in 1..T, and the launch count
-    has the parity of S (the result lands in unew iff S is odd)."""
+    """ftn_jacobi_plan (host logic): sweep counts sum to S, each in 1..T, the launch count has
+    the parity of S (the result lands in unew iff S is odd) and is the smallest such count
+    >= ceil(S/T), and the sweeps are spread evenly (sizes differ by at most one)."""
     for S in range(0, 120):
-        for T in (1, 2, 3, 4, 5, 6):
+        for T in range(1, 13):
             p = ftn.jacobi_plan(S, T)
             assert sum(p) == S and len(p) % 2 == S % 2 and all(1 <= k <= T for k in p), (S, T, p)
-            # at most three launches shorter than T (the remainder and the parity split k ->
-            # (k-1) + 1; e.g. S = 3, T = 2 needs [1, 1, 1])
-            assert sum(1 for k in p if k < T) <= 3, (S, T, p)
-    assert ftn.jacobi_plan(100, 4).count(4) == 24 and len(ftn.jacobi_plan(100, 4)) == 26
-    assert ftn.jacobi_plan(100, 5) == [5] * 20          # the bench's plan: no short launch
+            n = -(-S // T)
+            assert len(p) == (n if n % 2 == S % 2 else n + 1), (S, T, p)
+            assert not p or max(p) - min(p) <= 1, (S, T, p)
+    assert ftn.jacobi_plan(100, 4) == [4] * 22 + [3] * 4
+    assert ftn.jacobi_plan(100, 8) == [8] * 2 + [7] * 12   # 14 launches, none short
+    assert ftn.jacobi_plan(100, 5) == [5] * 20          # no short launch
     assert ftn.jacobi_plan(100, 2) == [2] * 50          # C5's plan

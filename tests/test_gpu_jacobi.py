@@ -7,7 +7,7 @@ import torch
 import oracle
 import synth
 from oracle import FArray as OA
-DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
+DEFAULT_FUSION = 0   # ftn_jacobi_set_fusion(0): back to the default (size-dependent)
 
 pytestmark = pytest.mark.gpu
 C2, C3 = 0.25, 1.0 / 6.0
@@ -277,8 +277,8 @@ def test_error_paths_launch_nothing(ftn):
                            ftn.FArray.empty((20, 16), dtype=torch.float32), 1),  # real(4)
         lambda: ftn.jacobi_slab(U, W, 2, 1, True, True),                       # sweeps > halo
         lambda: ftn.jacobi_slab(U, W, 1, 8, True, True),                       # no owned plane
-        lambda: ftn.jacobi_set_fusion(9),
-        lambda: ftn.jacobi_set_fusion(0),
+        lambda: ftn.jacobi_set_fusion(13),
+        lambda: ftn.jacobi_set_fusion(-1),
     ]
     for f in cases:
         with pytest.raises(ftn.FtnError):

@@ -6,7 +6,7 @@ import pytest
 import oracle
 import synth
 from oracle import FArray as OA
-DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
+DEFAULT_FUSION = 0   # ftn_jacobi_set_fusion(0): back to the default (size-dependent)
 
 pytestmark = pytest.mark.gpu
 
