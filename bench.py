@@ -594,6 +594,57 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                 "roofline": {"bound": "hbm", "bytes_per_cell": 48, "frac": gbs / N / hbm_peak}}
             del F, O, Z
             torch.cuda.empty_cache()
+    # SURVEY §8(e) strong scaling, predicted on one GPU: each rank's share at p = 8 run alone
+    # (no exchange), against the same kernel on the whole 1-GPU problem: the compute side of
+    # the 1 -> 8 efficiency (wave quantisation, halo recompute, shorter streams)
+    if "shares" in args.rows and N == 1:
+        P8 = 8
+        shares = {}
+        # C3: c(:, J_r) = MATMUL(a, b(:, J_r)), 8192 x 8192 x 1024 (512 tiles of 128 x 128)
+        n = 8192
+        A, B, C = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n // P8)), ftn.FArray.empty((n, n // P8))
+        ftn.gen_fill(A, SEED, 1, ftn.GEN_U11)
+        ftn.gen_fill(B, SEED, 2, ftn.GEN_U11)
+        t = timed(torch, lambda: ftn.matmul(C, A, B), steps, warm, None, None)
+        tf = 2.0 * n * n * (n // P8) * steps / t / 1e12
+        shares["c3_matmul_share_8192x8192x1024"] = {"value": tf, "unit": "TFLOP/s", "ms": t / steps * 1e3,
+                                                    "frac_of_fp64_peak": tf / FP64_PEAK_TFLOPS}
+        if "c3_matmul_8192" in rows:
+            shares["c3_matmul_share_8192x8192x1024"]["vs_full_problem"] = tf / rows["c3_matmul_8192"]["value"]
+        del A, B, C
+        torch.cuda.empty_cache()
+        # C5: a rank's slab 2048 x 2048 x (2046/8 owned + 2 x 2 halo) planes, 100 sweeps
+        n, sw = 2048, 100
+        nl = (n - 2) // P8 + 4
+        U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
+        ftn.gen_fill(U, SEED, 7, ftn.GEN_U01)
+        ftn.assign(W, U)
+        t = timed(torch, lambda: ftn.jacobi(U, W, sw), 2, 1, None, None)
+        gl = (n - 2) ** 2 * (nl - 2) * sw * 2 / t / 1e9
+        shares["c5_jacobi3d_slab_2048x2048x260"] = {"value": gl, "unit": "GLUPS", "ms": t / 2 * 1e3}
+        if "c5_jacobi3d_2048" in rows:
+            shares["c5_jacobi3d_slab_2048x2048x260"]["vs_full_problem"] = gl / rows["c5_jacobi3d_2048"]["value"]
+        del U, W
+        torch.cuda.empty_cache()
+        # C4: a rank's slab 1024 x 1024 x 128 (SUM and b*c+d)
+        arrs = [ftn.FArray.empty((1024, 1024, 1024 // P8)) for _ in range(4)]
+        for k, a in enumerate(arrs):
+            ftn.gen_fill(a, SEED, 10 + k, ftn.GEN_U01)
+        b, c, d, r = arrs
+        n_el = 1024 * 1024 * (1024 // P8)
+        out = torch.empty((), dtype=torch.float64, device="cuda")
+        for name, nb, fn, full in (("c4_sum_share_1024x1024x128", 8 * n_el, lambda: ftn.sum(b, out), "c4_sum"),
+                                   ("c4_muladd_share_1024x1024x128", 32 * n_el, lambda: ftn.muladd(r, b, c, d),
+                                    "c4_muladd_r=b*c+d")):
+            t = timed(torch, fn, steps, warm, None, None)
+            g = nb * steps / t / 1e9
+            shares[name] = {"value": g, "unit": "GB/s", "ms": t / steps * 1e3, "frac": g / hbm_peak}
+            if full in rows:
+                shares[name]["vs_full_problem"] = g / rows[full]["value"]
+        del arrs, b, c, d, r
+        torch.cuda.empty_cache()
+        rows["p8_shares_on_one_gpu"] = shares
+
     return rows
 
 
@@ -707,7 +758,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
-    ap.add_argument("--rows", default="c1,c4,c3,paper,c5,f4", help="comma list of extra rows, or 'none'")
+    ap.add_argument("--rows", default="c1,c4,c3,paper,c5,f4,shares", help="comma list of extra rows, or 'none'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")
