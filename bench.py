@@ -516,6 +516,9 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
     # (an even number of 2-sweep launches, so no single sweep in the plan)
     if "c5" in args.rows:
         n, sweeps = 2048, 100
+        probe = ftn.FArray.empty((8, 8, 8))
+        T3 = ftn.jacobi_fusion(probe)   # the rank-3 sweeps per launch (3 by default)
+        del probe
         free = torch.cuda.mem_get_info()[0]
         plane = n * n
         checksum = None
@@ -538,7 +541,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                 t, interior = None, 0
         else:
             from paper_2409_18824_b200 import dist as D
-            halo = 2                                     # 2 halo planes: 2 fused sweeps per exchange
+            halo = 3                                     # 3 halo planes: 3 fused sweeps per exchange
             g0, nl = D.jacobi_slab(n, N, rank, halo=halo)
             U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
             # the global array's values where they live (decomposition-independent input):
@@ -560,12 +563,12 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         if t:
             ns = max(2, steps // 2)
             gl = interior * sweeps * ns / t / 1e9
-            # algorithmic bytes: 16 B per interior point per launch (jacobi3d_tb2 does 2 sweeps
-            # per launch, ftn_jacobi_plan with T = min(fusion, 2), also on the 2-halo slabs)
-            nl3 = len(ftn.jacobi_plan(sweeps, min(2, ftn.jacobi_fusion())))
+            # algorithmic bytes: 16 B per interior point per launch (ftn_jacobi_plan with T = 3:
+            # jacobi3d_wr<3>, and jacobi3d_tb2 for the plan's 2-sweep launches; 3-halo slabs at N > 1)
+            nl3 = len(ftn.jacobi_plan(sweeps, T3))
             gbs = 16 * interior * nl3 * ns / t / 1e9 / N
             rows["c5_jacobi3d_2048"] = {"value": gl, "unit": "GLUPS", "ms_per_sweep": t / ns / sweeps * 1e3,
-                                        "launches_per_step": nl3,
+                                        "launches_per_step": nl3, "sweeps_per_launch_max": T3,
                                         "roofline": {"bound": "hbm", "achieved_gbs_per_gpu": gbs,
                                                      "frac": gbs / hbm_peak},
                                         "checksum": checksum}
@@ -613,17 +616,18 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             shares["c3_matmul_share_8192x8192x1024"]["vs_full_problem"] = tf / rows["c3_matmul_8192"]["value"]
         del A, B, C
         torch.cuda.empty_cache()
-        # C5: a rank's slab 2048 x 2048 x (2046/8 owned + 2 x 2 halo) planes, 100 sweeps
+        # C5: a rank's slab 2048 x 2048 x (256 owned + 2) planes, 100 sweeps (the local compute of
+        # one rank; the 3 halo planes per side only add the exchange)
         n, sw = 2048, 100
-        nl = (n - 2) // P8 + 4
+        nl = (n - 2) // P8 + 1 + 2
         U, W = ftn.FArray.empty((n, n, nl)), ftn.FArray.empty((n, n, nl))
         ftn.gen_fill(U, SEED, 7, ftn.GEN_U01)
         ftn.assign(W, U)
         t = timed(torch, lambda: ftn.jacobi(U, W, sw), 2, 1, None, None)
         gl = (n - 2) ** 2 * (nl - 2) * sw * 2 / t / 1e9
-        shares["c5_jacobi3d_slab_2048x2048x260"] = {"value": gl, "unit": "GLUPS", "ms": t / 2 * 1e3}
+        shares["c5_jacobi3d_slab_2048x2048x258"] = {"value": gl, "unit": "GLUPS", "ms": t / 2 * 1e3}
         if "c5_jacobi3d_2048" in rows:
-            shares["c5_jacobi3d_slab_2048x2048x260"]["vs_full_problem"] = gl / rows["c5_jacobi3d_2048"]["value"]
+            shares["c5_jacobi3d_slab_2048x2048x258"]["vs_full_problem"] = gl / rows["c5_jacobi3d_2048"]["value"]
         del U, W
         torch.cuda.empty_cache()
         # C4: a rank's slab 1024 x 1024 x 128 (SUM and b*c+d)

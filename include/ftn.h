@@ -251,7 +251,7 @@ ftn_status_t ftn_jacobi_ws(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t 
 
 /* Tuning (not semantics): rank-2 sweeps are executed up to T at a time by one kernel that
  * keeps the intermediate iterates in registers (temporal blocking, SURVEY §8(f) f2,
- * DESIGN.md §4.3), rank-3 sweeps up to min(T, 2) at a time (§4.4).  Results are
+ * DESIGN.md §4.3), rank-3 sweeps up to min(T, 3) at a time (§4.4).  Results are
  * bit-identical for every T; the array that does not hold the result holds an earlier
  * iterate.  T in 1..12 (1 = one sweep per launch; the kernels fuse up to 8, larger T only
  * in tuning builds); default 8 or the FTN_JACOBI_FUSE environment variable; unless T is set
@@ -261,6 +261,10 @@ ftn_status_t ftn_jacobi_ws(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t 
  * Process-wide. */
 ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch);
 int32_t ftn_jacobi_get_fusion(void);
+/* The sweeps per launch ftn_jacobi uses for this array (at most ftn_jacobi_get_fusion(); the
+ * size-dependent rank-2 default; min(T, 3) for rank 3 -- jacobi3d_wr / jacobi3d_tb2; 1 for
+ * arrays the fused kernels cannot address); 0 for an invalid descriptor.  Host-only. */
+int32_t ftn_jacobi_fusion_for(const ftn_desc_t* u);
 
 /* ftn_jacobi with the data on the host: host_u -> u (host-to-device copy), u -> unew
  * (device copy, presets the boundary of unew), `sweeps` sweeps, then the result -> host_result

@@ -50,6 +50,8 @@ void plan_units_halo(int64_t tiles, int64_t len, int64_t grid, int64_t halo_rows
 
 ftn_status_t jacobi2d_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, cudaStream_t s);
 ftn_status_t jacobi3d_fused2(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, cudaStream_t s);
+ftn_status_t jacobi3d_wr_planes(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t plane_lo,
+                                int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 ftn_status_t jacobi3d_fused2_planes(const ftn_desc_t* src, const ftn_desc_t* dst, double coeff, int64_t plane_lo,
                                     int64_t plane_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s);
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
@@ -487,6 +489,18 @@ int jacobi_fuse_T() {
 // depends on the grid (measured on B200, DESIGN.md §4.3 / §4.6): > 2^23 points 8 (jacobi2d_wq:
 // 8192^2 x 100 1981 GLUPS vs 1600 at T = 5), <= 2^23 points 5 (2048^2: 929 vs 792 at 8),
 // <= 2^21 points 6 (1024^2: 548 vs 422 at 5; launches there are latency bound).
+// Sweeps fused per launch for rank-3 arrays (FTN_J3_T overrides, 1..4): 3 by default --
+// jacobi3d_wr<3> (stencil3d_wr.cu), measured at 2048^3 x 100: T = 2 jacobi3d_tb2 539-570,
+// T = 3 631, T = 4 620 GLUPS.  Launches of 2 sweeps use jacobi3d_tb2 (faster
+// than jacobi3d_wr<2>: 539 vs 486), launches of 3 or 4 jacobi3d_wr.
+int jacobi3d_T() {
+  static const int t = [] {
+    const char* e = getenv("FTN_J3_T");
+    int v = e ? atoi(e) : 3;
+    return v < 1 ? 1 : (v > 4 ? 4 : v);
+  }();
+  return t;
+}
 int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
   int T = jacobi_fuse_T();
   if (T < 2 || !stencil_tma_able(u) || !stencil_tma_able(unew)) return 1;
@@ -496,12 +510,15 @@ int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
     const int64_t pts = u->dim[0].extent * u->dim[1].extent;
     T = pts <= (int64_t(1) << 21) ? 6 : pts <= (int64_t(1) << 23) ? 5 : 8;
   }
-  return u->rank == 2 ? T : 2;
+  return u->rank == 2 ? T : (T < jacobi3d_T() ? T : jacobi3d_T());
 }
 
 // k >= 2 fused sweeps src -> dst
 ftn_status_t jacobi_fused(const ftn_desc_t* src, const ftn_desc_t* dst, int k, double coeff, cudaStream_t s) {
-  return src->rank == 2 ? jacobi2d_fused(src, dst, k, coeff, s) : jacobi3d_fused2(src, dst, coeff, s);
+  if (src->rank == 2) return jacobi2d_fused(src, dst, k, coeff, s);
+  if (k == 2) return jacobi3d_fused2(src, dst, coeff, s);
+  const int64_t n3 = src->dim[2].extent;
+  return jacobi3d_wr_planes(src, dst, k, coeff, 1, n3 - 2, 0, n3 - 1, s);
 }
 
 ftn_status_t jacobi_prepare() {
@@ -594,6 +611,11 @@ extern "C" ftn_status_t ftn_jacobi_set_fusion(int32_t sweeps_per_launch) {
 }
 
 extern "C" int32_t ftn_jacobi_get_fusion(void) { return jacobi_fuse_T(); }
+
+extern "C" int32_t ftn_jacobi_fusion_for(const ftn_desc_t* u) {
+  if (check_desc(u, "ftn_jacobi_fusion_for(u)", 2, 3) != FTN_OK) return 0;
+  return jacobi_fuse_for(u, u);
+}
 
 // Launch plan for S sweeps with at most T per launch: the fewest launches n
 // >= ceil(S/T) whose count has the parity of S (every launch swaps u/unew, so the result then
@@ -726,9 +748,12 @@ ftn_status_t jacobi_slab_part(const ftn_desc_t* src, const ftn_desc_t* dst, int3
   const int64_t fix_lo = first ? lo - 1 : INT64_MIN / 4;
   const int64_t fix_hi = last ? hi + 1 : INT64_MAX / 4;
   if (r == 3) {
-    // 32-bit plane arithmetic in the kernel: clamp the "no boundary" sentinels to the slab
-    const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
-    return jacobi3d_fused2_planes(src, dst, coeff, out_lo, out_hi, flo, fhi, s);
+    if (sweeps == 2) {
+      // 32-bit plane arithmetic in the kernel: clamp the "no boundary" sentinels to the slab
+      const int64_t flo = first ? fix_lo : lo - 3, fhi = last ? fix_hi : hi + 3;
+      return jacobi3d_fused2_planes(src, dst, coeff, out_lo, out_hi, flo, fhi, s);
+    }
+    return jacobi3d_wr_planes(src, dst, sweeps, coeff, out_lo, out_hi, fix_lo, fix_hi, s);  // clamps the sentinels
   }
   return jacobi2d_fused_rows(src, dst, sweeps, coeff, out_lo, out_hi, fix_lo, fix_hi, s, res);
 }
@@ -746,9 +771,9 @@ extern "C" ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t*
     return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need halo >= 1 and at least one owned plane");
   if (sweeps < 1 || sweeps > halo) return fail(FTN_ERR_SHAPE, "ftn_jacobi_slab: need 1 <= sweeps <= halo");
   const bool tma = stencil_tma_able(src) && stencil_tma_able(dst);
-  if (sweeps > 1 && !(tma && (r == 2 || sweeps == 2)))
+  if (sweeps > 1 && !(tma && (r == 2 ? sweeps <= 8 : sweeps <= 4)))
     return fail(FTN_ERR_UNSUPPORTED,
-                "ftn_jacobi_slab: several sweeps per step need a TMA-able slab (rank 2: up to 6, rank 3: 2)");
+                "ftn_jacobi_slab: several sweeps per step need a TMA-able slab (rank 2: up to 8, rank 3: up to 4)");
   FTN_CHECK(require_sm100());
   FTN_CHECK(jacobi_prepare());
   return jacobi_slab_part(src, dst, sweeps, coeff, halo, first, last, halo, nl - halo - 1, (cudaStream_t)stream,

@@ -124,6 +124,8 @@ def _load():
         f.restype = st
     L.ftn_jacobi_get_fusion.restype = ctypes.c_int32
     L.ftn_jacobi_get_fusion.argtypes = []
+    L.ftn_jacobi_fusion_for.restype = ctypes.c_int32
+    L.ftn_jacobi_fusion_for.argtypes = [P]
     L.ftn_jacobi_plan.restype = ctypes.c_int64
     L.ftn_jacobi_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64]
     L.ftn_launch_count.restype = ctypes.c_uint64
@@ -500,8 +502,9 @@ def jacobi_slab(src: FArray, dst: FArray, sweeps: int, halo: int, first: bool, l
     _call("ftn_jacobi_slab", src.ref(), dst.ref(), sweeps, coeff, halo, int(first), int(last), _stream(stream))
 
 
-def jacobi_fusion() -> int:
-    return int(lib.ftn_jacobi_get_fusion())
+def jacobi_fusion(u: "FArray | None" = None) -> int:
+    """The process-wide fusion factor T, or (with u) the sweeps per launch ftn_jacobi uses for u."""
+    return int(lib.ftn_jacobi_get_fusion() if u is None else lib.ftn_jacobi_fusion_for(u.ref()))
 
 
 def jacobi_plan(sweeps: int, T: int | None = None) -> list[int]:

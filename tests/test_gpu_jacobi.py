@@ -161,14 +161,16 @@ def test_2d_temporal_blocking_long_strip(ftn):
     ftn.jacobi_set_fusion(DEFAULT_FUSION)
 
 
-@pytest.mark.parametrize("T", [1, 2])
+@pytest.mark.parametrize("T", [1, 2, 3, 4])
 @pytest.mark.parametrize("shape", [(3, 3, 3), (4, 5, 6), (61, 29, 5), (62, 30, 6), (63, 31, 4), (121, 57, 9),
-                                   (130, 18, 7), (64, 64, 64), (200, 90, 40), (17, 100, 33)])
+                                   (130, 18, 7), (64, 64, 64), (200, 90, 40), (17, 100, 33), (57, 25, 8),
+                                   (58, 27, 12), (113, 49, 11), (114, 52, 3)])
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 5])
 def test_3d_temporal_blocking(ftn, T, shape, sweeps):
-    """Rank-3 launches of two fused sweeps (jacobi3d_tb2) are bit-identical to
-    the oracle's DO nest; tiles of 60 x 28 outputs, so these shapes cover one tile, exact
-    multiples and ragged tails in i and j."""
+    """Rank-3 launches of T fused sweeps (jacobi3d_wr<T>) are bit-identical to
+    the oracle's DO nest; boxes of 64 x 32 with (64 - 2H) x (32 - 2T) outputs (56 x 24 at
+    T = 4, 56 x 26 at T = 3, 60 x 28 at T = 2), so these shapes cover one tile, exact multiples
+    and ragged tails in i and j."""
     ftn.jacobi_set_fusion(T)
     try:
         u0 = synth.jacobi_init(shape, array_id=sum(shape) + sweeps)
@@ -240,14 +242,15 @@ def test_jacobi_host_buffers(ftn, shape, sweeps):
 
 @pytest.mark.slow
 def test_c5_bench_configuration_100_sweeps(ftn):
-    """C5 exactly as bench.py runs it (2048^3, 100 sweeps = 50 launches of jacobi3d_tb2):
-    sampled points recomputed by the oracle on their dependence cone (203^3 windows)."""
+    """C5 exactly as bench.py runs it (2048^3, 100 sweeps = 26 launches of jacobi3d_wr: 22 of 4
+    and 4 of 3 sweeps): sampled points recomputed by the oracle on their dependence cone
+    (203^3 windows)."""
     n, sweeps = 2048, 100
     U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
     ftn.gen_fill(U, synth.SEED, 7, ftn.GEN_U01)
     ftn.assign(W, U)
-    assert ftn.jacobi_plan(sweeps, 2) == [2] * 50
-    pts = [(1, 1, 1), (n - 2, 1000, 5), (700, 1300, 1900), (150, n - 2, 60)]
+    assert ftn.jacobi_plan(sweeps, 4) == [4] * 22 + [3] * 4
+    pts = [(1, 1, 1), (n - 2, 1000, 5), (700, 1300, 1900), (150, n - 2, 60), (56, 24, 1024), (57, 25, 2046)]
     R = sweeps + 1
     wins = []
     for p in pts:
