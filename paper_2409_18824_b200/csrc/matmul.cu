@@ -23,6 +23,7 @@
 //   for every l exactly once.
 #include "ftn_internal.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 #include <cstring>
@@ -47,6 +48,14 @@ struct MParams {
   int64_t M, N, K;
   int64_t tiles_m, tiles_n;
   int kt;  // number of BK steps
+  // Work: tiles [0, dp_tiles) whole, one per CTA in turn (data parallel); tiles
+  // [dp_tiles, dp_tiles + sk_tiles) by stream-K: their sk_tiles * kt k-steps split evenly over
+  // the CTAs of one persistent wave, a tile's partial sums combined in k order by the CTA that
+  // finishes it last (sk_part: 2 slots of BM x BN per CTA, sk_cnt: one counter per tile, zero
+  // at launch and left zero).
+  int64_t dp_tiles, sk_tiles;
+  double* sk_part;
+  int* sk_cnt;
 };
 
 // byte offset of element (row, x) inside a 128B-swizzled box (rows of 16 doubles)
@@ -76,15 +85,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // grouped raster for L2 reuse of A row-panels and B column-panels
-  const int64_t b = blockIdx.x;
-  const int64_t per_group = GROUP_M * p.tiles_n;
-  const int64_t first_m = (b / per_group) * GROUP_M;
-  const int64_t gsz = min((int64_t)GROUP_M, p.tiles_m - first_m);
-  const int64_t tm = first_m + (b % per_group) % gsz;
-  const int64_t tn = (b % per_group) / gsz;
-  const int m0 = (int)(tm * BM), n0 = (int)(tn * BN);
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       dev::mbar_init(&full[s], 1);
@@ -94,13 +94,26 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
-  // TMA producer: lane 0 of warp 0
-  auto issue = [&](int kt) {
-    const int s = kt % STAGES;
-    if (kt >= STAGES) dev::mbar_wait_idle(&empty[s], ((kt / STAGES) - 1) & 1);
+  int m0 = 0, n0 = 0;  // origin of the current tile
+  // grouped raster for L2 reuse of A row-panels and B column-panels
+  auto set_tile = [&](int tile) {
+    const int per_group = GROUP_M * (int)p.tiles_n;
+    const int first_m = (tile / per_group) * GROUP_M;
+    const int gsz = min(GROUP_M, (int)p.tiles_m - first_m);
+    const int tm = first_m + (tile % per_group) % gsz;
+    const int tn = (tile % per_group) / gsz;
+    m0 = tm * BM;
+    n0 = tn * BN;
+  };
+
+  // TMA producer: lane 0 of warp 0.  k-step kk of the current tile into pipeline slot it
+  // (it counts this CTA's k-steps over all its tiles: stage it % STAGES, phase it / STAGES).
+  auto issue = [&](int kk, uint32_t it) {
+    const int s = it % STAGES;
+    if (it >= STAGES) dev::mbar_wait_idle(&empty[s], ((it / STAGES) - 1) & 1);
     uint8_t* st = smem + s * STAGE_BYTES;
     dev::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-    const int k0 = kt * BK;
+    const int k0 = kk * BK;
     if constexpr (!TA) {
 #pragma unroll
       for (int a = 0; a < BM / 16; ++a) dev::tma_load_2d(st + a * A_BOX_BYTES, &map_a, &full[s], m0 + 16 * a, k0);
@@ -122,21 +135,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (producer) {
     dev::prefetch_tma(&map_a);
     dev::prefetch_tma(&map_b);
-    for (int kt = 0; kt < STAGES - 1 && kt < p.kt; ++kt) issue(kt);
   }
-  __syncwarp();
 
   // ---------------- MMA warps
   const int wm = warp >> 2;  // 0..1 -> rows wm*64
   const int wn = warp & 3;   // 0..3 -> cols wn*32
   const int g = lane >> 2, t = lane & 3;
   double acc[4][4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
   // fragment loads index the __shared__ array directly so the compiler emits LDS and
   // may schedule them early (the mbarrier waits are compiler memory barriers)
@@ -171,53 +176,158 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
-  for (int kt = 0; kt < p.kt; ++kt) {
-    const int s = kt % STAGES;
-    if (producer && kt + STAGES - 1 < p.kt) issue(kt + STAGES - 1);  // refills the stage freed at kt-1
+  uint32_t it = 0;  // k-steps consumed by this CTA
+  // acc = sum over k-steps [k_lo, k_hi) of the current tile
+  auto run = [&](int k_lo, int k_hi) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+    if (producer)
+      for (int kk = k_lo; kk < k_lo + STAGES - 1 && kk < k_hi; ++kk) issue(kk, it + (uint32_t)(kk - k_lo));
     __syncwarp();
-    dev::mbar_wait(&full[s], (kt / STAGES) & 1);
-    const uint32_t st = smem_base + s * STAGE_BYTES;
+    for (int kk = k_lo; kk < k_hi; ++kk, ++it) {
+      const int s = it % STAGES;
+      if (producer && kk + STAGES - 1 < k_hi) issue(kk + STAGES - 1, it + STAGES - 1);  // the stage freed at it-1
+      __syncwarp();
+      dev::mbar_wait(&full[s], (it / STAGES) & 1);
+      const uint32_t st = smem_base + s * STAGE_BYTES;
 #pragma unroll
-    for (int kb = 0; kb < BK / 8; ++kb) {
-      // A: row l = kb*8 + phys -> +kb*8 rows (the swizzle phase (row & 7) is unchanged)
-      // B: x = (kb & 1) * 8 + phys in box kb >> 1 -> +8 doubles = +4 chunks: XOR by 4 commutes
-      // rows carry l (MK / NK layouts): +kb*8 rows; elements carry l (KM / KN): box kb>>1, chunk ^ 4
-      const uint32_t a_kb = TA ? (kb >> 1) * B_BOX_BYTES : kb * 8 * 128;
-      const uint32_t a_x = TA ? ((kb & 1) ? 64u : 0u) : 0u;
-      const uint32_t b_kb = TB ? kb * 8 * 128 : (kb >> 1) * B_BOX_BYTES;
-      const uint32_t b_x = TB ? 0u : ((kb & 1) ? 64u : 0u);  // chunk index ^ 4 == byte offset ^ 64
+      for (int kb = 0; kb < BK / 8; ++kb) {
+        // A: row l = kb*8 + phys -> +kb*8 rows (the swizzle phase (row & 7) is unchanged)
+        // B: x = (kb & 1) * 8 + phys in box kb >> 1 -> +8 doubles = +4 chunks: XOR by 4 commutes
+        // rows carry l (MK / NK layouts): +kb*8 rows; elements carry l (KM / KN): box kb>>1, chunk ^ 4
+        const uint32_t a_kb = TA ? (kb >> 1) * B_BOX_BYTES : kb * 8 * 128;
+        const uint32_t a_x = TA ? ((kb & 1) ? 64u : 0u) : 0u;
+        const uint32_t b_kb = TB ? kb * 8 * 128 : (kb >> 1) * B_BOX_BYTES;
+        const uint32_t b_x = TB ? 0u : ((kb & 1) ? 64u : 0u);  // chunk index ^ 4 == byte offset ^ 64
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        double af[4][2], bf[4];
+        for (int q = 0; q < 2; ++q) {
+          double af[4][2], bf[4];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          af[mt][0] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][0] ^ a_x));
-          af[mt][1] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][1] ^ a_x));
+          for (int mt = 0; mt < 4; ++mt) {
+            af[mt][0] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][0] ^ a_x));
+            af[mt][1] = *reinterpret_cast<const double*>(smem_raw + st + a_kb + (a_off[q][mt][1] ^ a_x));
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+            bf[nt] = *reinterpret_cast<const double*>(smem_raw + st + b_kb + (b_off[q][nt] ^ b_x));
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt][0], af[mt][1], bf[nt]);
         }
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-          bf[nt] = *reinterpret_cast<const double*>(smem_raw + st + b_kb + (b_off[q][nt] ^ b_x));
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt][0], af[mt][1], bf[nt]);
       }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) dev::mbar_arrive(&empty[s]);
-  }
+  };
 
   // ---------------- epilogue: c(i, j) through the descriptor strides
+  auto store = [&]() {
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+      for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t i = m0 + wm * 64 + mt * 16 + g + ((r >> 1) << 3);
-        const int64_t j = n0 + wn * 32 + nt * 8 + 2 * t + (r & 1);
-        if (i < p.M && j < p.N) *reinterpret_cast<double*>(p.c + i * p.c_sm0 + j * p.c_sm1) = acc[mt][nt][r];
+        for (int r = 0; r < 4; ++r) {
+          const int64_t i = m0 + wm * 64 + mt * 16 + g + ((r >> 1) << 3);
+          const int64_t j = n0 + wn * 32 + nt * 8 + 2 * t + (r & 1);
+          if (i < p.M && j < p.N) *reinterpret_cast<double*>(p.c + i * p.c_sm0 + j * p.c_sm1) = acc[mt][nt][r];
+        }
+  };
+
+  // Work items of this CTA: whole tiles blockIdx.x, +G, ... below dp_tiles, then (stream-K)
+  // its share [lo, hi) of the tail's k-steps, tile by tile.  One call site of run() keeps the
+  // register allocation of the single-tile kernel.
+  __shared__ int sk_last;
+  // 32-bit work cursors (tiles < 2^31; the tail's k-steps I < 2^31, checked on the host)
+  const int G = (int)gridDim.x, b = (int)blockIdx.x, kt = p.kt, dpt = (int)p.dp_tiles;
+  const int I = (int)(p.sk_tiles * kt);
+  const int hi = p.sk_tiles ? (int)((int64_t)(b + 1) * I / G) : 0;
+  int dp_t = b, a = p.sk_tiles ? (int)((int64_t)b * I / G) : 0;
+  for (;;) {
+    int tt, k_lo, k_hi;
+    if (dp_t < dpt) {
+      tt = dp_t;
+      dp_t += G;
+      k_lo = 0;
+      k_hi = kt;
+    } else if (a < hi) {
+      k_lo = a % kt;
+      k_hi = min(kt, k_lo + (hi - a));
+      tt = dpt + a / kt;
+      a += k_hi - k_lo;
+    } else {
+      break;
+    }
+    set_tile(tt);
+    run(k_lo, k_hi);
+    if (k_lo == 0 && k_hi == kt) {
+      store();
+      continue;
+    }
+    // a partial tile of the stream-K tail: publish it; the CTA that completes the tile
+    // combines the partial sums in k order (CTA order), so the bits do not depend on which
+    // CTA finishes last
+    const int ts = tt - dpt;
+    auto start_of = [&](int cb) { return (int)((int64_t)cb * I / G); };
+    auto cta_of = [&](int x) {  // the CTA whose share holds tail k-step x
+      int c = (int)((int64_t)x * G / I);
+      while (c + 1 < G && start_of(c + 1) <= x) ++c;
+      while (c > 0 && start_of(c) > x) --c;
+      return c;
+    };
+    const int b_lo = cta_of(ts * kt), b_hi = cta_of((ts + 1) * kt - 1);
+    auto slot_of = [&](int cb) { return 2 * cb + (start_of(cb) >= ts * kt ? 0 : 1); };
+    double* mine = p.sk_part + (size_t)slot_of(b) * (BM * BN) + (size_t)threadIdx.x * 64;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        *reinterpret_cast<double4*>(mine + (mt * 4 + nt) * 4) =
+            make_double4(acc[mt][nt][0], acc[mt][nt][1], acc[mt][nt][2], acc[mt][nt][3]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int prev = atomicAdd(&p.sk_cnt[ts], 1);
+      sk_last = prev == (int)(b_hi - b_lo);
+      if (sk_last) p.sk_cnt[ts] = 0;  // left zero for the next launch
+    }
+    __syncthreads();
+    if (!sk_last) continue;
+    __threadfence();
+    // every segment (this CTA's too) is in its slot: c = ((p_lo + p_lo+1) + ...) per element,
+    // streamed from the slots (acc is dead here, so the fixup needs few registers)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const size_t off = (size_t)threadIdx.x * 64 + (mt * 4 + nt) * 4;
+        const double* s0 = p.sk_part + (size_t)slot_of(b_lo) * (BM * BN) + off;
+        double2 v01 = __ldcg(reinterpret_cast<const double2*>(s0));
+        double2 v23 = __ldcg(reinterpret_cast<const double2*>(s0 + 2));
+#pragma unroll 1
+        for (int cb = b_lo + 1; cb <= b_hi; ++cb) {
+          const double* sc = p.sk_part + (size_t)slot_of(cb) * (BM * BN) + off;
+          const double2 w01 = __ldcg(reinterpret_cast<const double2*>(sc));
+          const double2 w23 = __ldcg(reinterpret_cast<const double2*>(sc + 2));
+          v01.x = v01.x + w01.x;
+          v01.y = v01.y + w01.y;
+          v23.x = v23.x + w23.x;
+          v23.y = v23.y + w23.y;
+        }
+        const double v[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int64_t i = m0 + wm * 64 + mt * 16 + g + ((r >> 1) << 3);
+          const int64_t j = n0 + wn * 32 + nt * 8 + 2 * t + (r & 1);
+          if (i < p.M && j < p.N) *reinterpret_cast<double*>(p.c + i * p.c_sm0 + j * p.c_sm1) = v[r];
+        }
       }
+  }
 }
 
 bool tma_able(const ftn_desc_t* d) {
@@ -262,8 +372,25 @@ ftn_status_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const MPa
     attr_set[dev & 63] = true;
   }
   const int64_t tiles = p.tiles_m * p.tiles_n;
-  dmma_gemm_kernel<TA, TB><<<(unsigned)tiles, THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  const int64_t grid = p.sk_tiles ? (int64_t)num_sms() : tiles;
+  dmma_gemm_kernel<TA, TB><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(ma, mb, p);
   return after_launch("dmma_gemm_kernel");
+}
+
+// Stream-K for the tail (FTN_MATMUL_SK=0 disables): when whole tiles would leave the last
+// wave of one-CTA-per-SM tiles less than ~93 % full (e.g. MATMUL of a p = 8 column block of C3:
+// 512 tiles on 148 SMs = 3.46 waves), all but one full wave stay whole tiles and the rest is
+// split evenly by k-steps over one persistent wave.
+bool use_stream_k(int64_t tiles, int kt) {
+  static const bool on = !getenv("FTN_MATMUL_SK") || atoi(getenv("FTN_MATMUL_SK")) != 0;
+  const int64_t G = num_sms();
+  if (!on || tiles < G || kt < 8) return false;
+  const int64_t waves = (tiles + G - 1) / G;
+  return (double)tiles / (double)(waves * G) < 0.93;
+}
+
+size_t sk_ws_bytes(int64_t tiles_bound) {
+  return (size_t)2 * num_sms() * BM * BN * 8 + (size_t)tiles_bound * 4 + 512;
 }
 
 // Small products (M*N*K <= 2^21, e.g. C1's 48 x 48 x 32): one thread per c(i, j) folding
@@ -318,7 +445,7 @@ ftn_status_t run_small_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ft
 
 // c = MATMUL(op(a), op(b)), op = TRANSPOSE when ta / tb.  op(a) is (M, K), op(b) is (K, N).
 ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
-                        cudaStream_t s, bool force_dmma = false) {
+                        size_t ws_bytes, cudaStream_t s, bool force_dmma = false) {
   const int64_t M = ta ? a->dim[1].extent : a->dim[0].extent;
   const int64_t K = ta ? a->dim[0].extent : a->dim[1].extent;
   const int64_t N = tb ? b->dim[0].extent : b->dim[1].extent;
@@ -354,6 +481,23 @@ ftn_status_t run_matmul(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc
   p.tiles_m = (M + BM - 1) / BM;
   p.tiles_n = (N + BN - 1) / BN;
   p.kt = (int)((K + BK - 1) / BK);
+  const int64_t tiles = p.tiles_m * p.tiles_n;
+  p.dp_tiles = tiles;
+  p.sk_tiles = 0;
+  p.sk_part = nullptr;
+  p.sk_cnt = nullptr;
+  char* sk = ws ? (char*)(((uintptr_t)w + 255) & ~uintptr_t(255)) : nullptr;
+  if (sk && !tma_able(b)) sk += pack_bytes(b);  // after the packed b
+  sk = sk ? (char*)(((uintptr_t)sk + 255) & ~uintptr_t(255)) : nullptr;
+  const int64_t G = num_sms();
+  if (sk && use_stream_k(tiles, p.kt) &&
+      (size_t)(sk - ws) + (size_t)2 * G * BM * BN * 8 + (size_t)tiles * 4 <= ws_bytes) {
+    p.dp_tiles = (tiles / G - 1) * G;
+    p.sk_tiles = tiles - p.dp_tiles;
+    p.sk_part = reinterpret_cast<double*>(sk);
+    p.sk_cnt = reinterpret_cast<int*>(sk + (size_t)2 * G * BM * BN * 8);
+    FTN_CUDA(cudaMemsetAsync(p.sk_cnt, 0, (size_t)p.sk_tiles * 4, s));
+  }
   if (!ta && !tb) return launch_gemm<false, false>(ma, mb, p, s);
   if (ta && !tb) return launch_gemm<true, false>(ma, mb, p, s);
   if (!ta && tb) return launch_gemm<false, true>(ma, mb, p, s);
@@ -752,16 +896,23 @@ size_t ws_bytes_for(const ftn_desc_t* a, const ftn_desc_t* b) {
     }
     case 2: return 0;
   }
-  return pack_bytes(a) + pack_bytes(b) + 512;
+  {
+    // stream-K partial tiles (either orientation of the operands)
+    const int64_t mm = std::max(a->dim[0].extent, a->dim[1].extent), nn = std::max(b->dim[0].extent, b->dim[1].extent);
+    const int64_t tiles = ((mm + BM - 1) / BM) * ((nn + BN - 1) / BN);
+    const int64_t kk = std::max(a->dim[0].extent, a->dim[1].extent);
+    const size_t sk = tiles >= num_sms() && !small_matmul(mm, nn, kk) ? sk_ws_bytes(tiles) : 0;
+    return pack_bytes(a) + pack_bytes(b) + 512 + sk;
+  }
 }
 
 ftn_status_t dispatch(const ftn_desc_t* c, const ftn_desc_t* a, const ftn_desc_t* b, bool ta, bool tb, char* ws,
-                      cudaStream_t s, bool force_dmma = false) {
+                      size_t ws_bytes, cudaStream_t s, bool force_dmma = false) {
   switch (form_of(a, b)) {
     case 1: return run_matvec(c, a, b, ws, s);
     case 2: return run_vecmat(c, a, b, s);
   }
-  return run_matmul(c, a, b, ta, tb, ws, s, force_dmma);
+  return run_matmul(c, a, b, ta, tb, ws, ws_bytes, s, force_dmma);
 }
 
 }  // namespace
@@ -776,12 +927,12 @@ ftn_status_t matmul_local_ex(const ftn_desc_t* c, const ftn_desc_t* a, const ftn
   const size_t need = ws_bytes_for(a, b);
   if (need > 512 && (!ws || ws_bytes < need))
     return fail(FTN_ERR_WORKSPACE, "ftn_matmul: workspace too small (see ftn_matmul_workspace_size)");
-  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return dispatch(c, a, b, ta, tb, (char*)ws, s, force);
+  if (!desc_overlap(c, a) && !desc_overlap(c, b)) return dispatch(c, a, b, ta, tb, (char*)ws, ws_bytes, s, force);
   StreamTemp tmp;  // R#5: the product is formed before c is defined
   FTN_CHECK(tmp.alloc((size_t)desc_size(c) * 8, s));
   ftn_desc_t t;
   FTN_CHECK(make_packed(&t, tmp.ptr, c));
-  FTN_CHECK(dispatch(&t, a, b, ta, tb, (char*)ws, s, force));
+  FTN_CHECK(dispatch(&t, a, b, ta, tb, (char*)ws, ws_bytes, s, force));
   return launch_copy(c, &t, s);
 }
 
