@@ -280,7 +280,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         gbs = nbytes * N * steps / t / 1e9
         rows[name] = {"value": gbs, "unit": "GB/s", "ms": t / steps * 1e3, "ms_min": LAST_STEP_MS[0],
                       "ms_median": LAST_STEP_MS[1],
-                      "roofline": {"bound": "hbm", "frac": gbs / N / hbm_peak}}
+                      "roofline": {"bound": "hbm", "frac": gbs / N / hbm_peak,
+                                   "frac_of_8TBps_spec": gbs / N / HBM_SPEC_GBS}}
 
     # C1: real(8) a(0:63,1:48) = its 0-based offset, s = a(::2,:); latency of each call (median of
     # 1000, CUDA events around the call: host launch overhead included) and the closed forms of
@@ -388,6 +389,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         b, c, d, r = arrs
         n_el = 1024 * 1024 * nk
         gbs_row("c4_muladd_r=b*c+d", 32 * n_el, lambda: ftn.muladd(r, b, c, d))
+        gbs_row("hbm_copy_r=b", 16 * n_el, lambda: ftn.assign(r, b))      # the in-run copy ceiling
         out = torch.empty((), dtype=torch.float64, device="cuda")
         if not distmode:
             gbs_row("c4_sum", 8 * n_el, lambda: ftn.sum(b, out))
@@ -737,6 +739,18 @@ CONFIG = {"workload": "BASELINE configs[1]: 2-D 5-point Jacobi stencil, real(8) 
           "l2": "working set 2 x 512 MiB > 126 MB L2 (no flush needed)", "seed": SEED}
 
 
+HBM_SPEC_GBS = 8000.0   # B200 datasheet HBM3e bandwidth (BASELINE's ~8 TB/s)
+
+
+def in_run_ceilings(rows, hbm_peak):
+    """the HBM ceilings measured in this run beside the denominators --
+    read-only (C4 SUM, 8 B/elem), copy (r = b, 16 B/elem), triad (b*c+d, 32 B/elem), the
+    MEASURED_PEAKS copy figure and the 8 TB/s spec."""
+    get = lambda k: rows.get(k, {}).get("value") if isinstance(rows.get(k), dict) else None  # noqa: E731
+    return {"read_gbs": get("c4_sum"), "copy_gbs": get("hbm_copy_r=b"), "triad_gbs": get("c4_muladd_r=b*c+d"),
+            "measured_peaks_copy_gbs": hbm_peak, "spec_gbs": HBM_SPEC_GBS, "unit": "GB/s"}
+
+
 def fused_kernel_name(sizes):
     """The 2-D kernels of a launch plan ({sweeps per launch: count}): jacobi2d_wq<k> for k >= 7
     (and any k under FTN_WF_WQ=1), jacobi2d_wf<k> for 2 <= k <= 6, jacobi2d_tma for k = 1."""
@@ -830,6 +844,7 @@ def main():
                                   "single-sweep roofline 6556/16 = 410 GLUPS; time = all launches of the timed region")},
             "cpu_baseline": cpu,
             "clocks": clk,
+            "hbm_ceilings_in_run": in_run_ceilings(rows, hbm_peak),
             "rows": rows,
         }
         print(json.dumps(line), flush=True)

@@ -37,8 +37,14 @@
 namespace ftn {
 namespace {
 
-constexpr int W3_NW = 8;                  // warps per CTA (bands of 4 rows)
-constexpr int W3_R = 4;                   // rows per lane
+#ifndef FTN_W3_NW
+#define FTN_W3_NW 8
+#endif
+#ifndef FTN_W3_R
+#define FTN_W3_R 4
+#endif
+constexpr int W3_NW = FTN_W3_NW;          // warps per CTA (bands of W3_R rows)
+constexpr int W3_R = FTN_W3_R;            // rows per lane
 constexpr int W3_BX = 64, W3_BY = W3_NW * W3_R;  // box 64 x 32
 constexpr int W3_PLANE = W3_BX * W3_BY * 8;      // 16 KB
 constexpr int W3_THREADS = W3_NW * 32;

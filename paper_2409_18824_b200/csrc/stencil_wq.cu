@@ -38,7 +38,7 @@
 #define FTN_WQ_R 4
 #endif
 #ifndef FTN_WQ_NS
-#define FTN_WQ_NS 3
+#define FTN_WQ_NS 2  // ring stages per warp: 8192^2, T = 8: 2 -> 2022, 3 -> 1971, 4 -> 1919 GLUPS
 #endif
 #ifndef FTN_WQ_UNROLL
 #define FTN_WQ_UNROLL 2
