@@ -12,7 +12,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2409_18824_b200 import ftn  # noqa: E402
-DEFAULT_FUSION = 5   # ftn_jacobi_get_fusion() default (FTN_JACOBI_FUSE unset)
+DEFAULT_FUSION = 0   # ftn_jacobi_set_fusion(0): back to the size-dependent default
 
 SEED = 18824
 
@@ -24,8 +24,10 @@ def main(which):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
-        ftn.jacobi(U, W, 10)     # two fused launches (5 sweeps each, jacobi2d_wf<5>), the default
-        ftn.jacobi(U, W, 10)
+        ftn.jacobi(U, W, 16)     # two fused launches (8 sweeps each, jacobi2d_wq<8>), the default
+        ftn.jacobi(U, W, 14)     # two launches of jacobi2d_wq<7>
+        ftn.jacobi_set_fusion(5)
+        ftn.jacobi(U, W, 10)     # two launches of jacobi2d_wf<5> (grids <= 2^23 points use it)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi2d_tma)
         ftn.jacobi_set_fusion(DEFAULT_FUSION)
@@ -35,6 +37,7 @@ def main(which):
         U, W = ftn.FArray.empty((n, n, n)), ftn.FArray.empty((n, n, n))
         ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
         ftn.assign(W, U)
+        ftn.jacobi(U, W, 6)      # two launches of jacobi3d_wr<3> (the default)
         ftn.jacobi(U, W, 4)      # two launches of jacobi3d_tb2 (2 sweeps each)
         ftn.jacobi_set_fusion(1)
         ftn.jacobi(U, W, 1)      # the single-sweep kernel (jacobi3d_tma)
