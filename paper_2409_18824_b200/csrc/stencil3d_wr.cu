@@ -31,8 +31,11 @@
 // plane range) per CTA, equal weighted work, no wave quantisation.
 #include "ftn_internal.cuh"
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 namespace ftn {
 namespace {
@@ -69,29 +72,45 @@ struct W3Params {
   int32_t tiles_i, tiles_j;
   int32_t plane_lo, nplanes;   // output planes [plane_lo, plane_lo + nplanes)
   int32_t fix_lo, fix_hi;      // planes <= fix_lo and >= fix_hi keep their value at every level
-  int64_t w_edge, w_in, W;     // weighted flattened split (see the header comment)
+  int64_t w_iedge, w_jedge, w_in, W;  // weighted flattened split (see the header comment)
   int64_t G;                   // CTAs
   double coeff;
 };
 
+#ifndef FTN_W3_TRACE
+#define FTN_W3_TRACE 0
+#endif
+#if FTN_W3_TRACE
+__device__ long long* w3_trace;  // per CTA: start, end (globaltimer ns), edge / interior tile-planes
+#endif
+
 __device__ __forceinline__ int64_t w3_cdiv(int64_t a, int64_t b) { return a <= 0 ? 0 : (a + b - 1) / b; }
 
-__device__ __forceinline__ bool w3_edge_tile(const W3Params& p, int64_t t) {
+// Tile weights: the tiles of the first / last tile column (their boxes start or end outside
+// the array in the contiguous dimension and run the select path) weigh w_iedge, the other
+// tiles of the first / last tile row w_jedge, every other tile w_in (per plane).
+__device__ __forceinline__ int64_t w3_weight(const W3Params& p, int64_t t) {
   const int64_t ti = t % p.tiles_i, tj = t / p.tiles_i;
-  return ti == 0 || ti == p.tiles_i - 1 || tj == 0 || tj == p.tiles_j - 1;
+  if (ti == 0 || ti == p.tiles_i - 1) return p.w_iedge;
+  return (tj == 0 || tj == p.tiles_j - 1) ? p.w_jedge : p.w_in;
+}
+__device__ __forceinline__ bool w3_edge_tile(const W3Params& p, int64_t t) { return w3_weight(p, t) != p.w_in; }
+
+// Per-plane weight of tiles [0, ti) of a row whose middle tiles weigh wm.
+__device__ __forceinline__ int64_t w3_row_prefix(const W3Params& p, int64_t ti, int64_t wm) {
+  if (ti <= 0) return 0;
+  if (ti >= p.tiles_i) return p.tiles_i == 1 ? p.w_iedge : 2 * p.w_iedge + (p.tiles_i - 2) * wm;
+  return p.w_iedge + (ti - 1) * wm;
 }
 
-// Weighted start of tile t: tiles of row tj = 0 and tj = tiles_j - 1 are all edge tiles; the
-// other rows have an edge tile at each end.
+// Weighted start of tile t (tiles i fastest; rows tj = 0 and tj = tiles_j - 1 are j-edge rows).
 __device__ __forceinline__ int64_t w3_tile_start(const W3Params& p, int64_t t) {
-  const int64_t ti = t % p.tiles_i, tj = t / p.tiles_i, TI = p.tiles_i, N = p.nplanes;
-  const int64_t row_edge = TI * p.w_edge * N;                                     // an all-edge row
-  const int64_t row_mid = (TI <= 2 ? TI * p.w_edge : 2 * p.w_edge + (TI - 2) * p.w_in) * N;
+  const int64_t ti = t % p.tiles_i, tj = t / p.tiles_i, N = p.nplanes;
+  const int64_t row_j = w3_row_prefix(p, p.tiles_i, p.w_jedge), row_m = w3_row_prefix(p, p.tiles_i, p.w_in);
   int64_t s = 0;
-  if (tj > 0) s += row_edge + (tj - 1) * row_mid;   // rows 0 .. tj-1 (row 0 all edge)
-  const bool all_edge = tj == 0 || tj == p.tiles_j - 1;
-  if (all_edge) return s + ti * p.w_edge * N;
-  return s + (ti == 0 ? 0 : p.w_edge * N + (ti - 1) * p.w_in * N);
+  if (tj > 0) s += (row_j + (tj - 1) * row_m) * N;   // row 0 (a j-edge row) and the middle rows before tj
+  const bool jrow = tj == 0 || tj == p.tiles_j - 1;
+  return s + w3_row_prefix(p, ti, jrow ? p.w_jedge : p.w_in) * N;
 }
 
 // Tile holding weighted position x (binary search over the monotone tile starts).
@@ -113,7 +132,7 @@ __device__ __forceinline__ bool w3_piece(const W3Params& p, int64_t b, int64_t k
   if (A >= B || t > t1) return false;
   const int64_t P0 = w3_tile_start(p, t);
   const int64_t P1 = t + 1 < (int64_t)p.tiles_i * p.tiles_j ? w3_tile_start(p, t + 1) : p.W;
-  const int64_t w = w3_edge_tile(p, t) ? p.w_edge : p.w_in;
+  const int64_t w = w3_weight(p, t);
   int64_t lo = w3_cdiv(A - P0, w), hi = w3_cdiv((B < P1 ? B : P1) - P0, w);
   if (hi > p.nplanes) hi = p.nplanes;
   if (lo > hi) lo = hi;
@@ -217,8 +236,17 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
   uint32_t g = 0;  // level-0 planes consumed by this CTA
   int64_t t;
   int32_t ka, kb;
+#if FTN_W3_TRACE
+  uint64_t tr0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+  int64_t tr_edge = 0, tr_in = 0;
+#endif
   for (int64_t pk = 0; w3_piece(p, b, pk, t0, t1, t, ka, kb); ++pk) {
     if (kb <= ka) continue;
+#if FTN_W3_TRACE
+    if (w3_edge_tile(p, t)) tr_edge += kb - ka;
+    else tr_in += kb - ka;
+#endif
     const int32_t i0 = (int32_t)(t % p.tiles_i) * C::OX - C::H, j0 = (int32_t)(t / p.tiles_i) * C::OY - T;
     const int nq = (kb - ka) + 2 * T;  // level-0 planes ka-T .. kb+T-1 (steps q)
     const int32_t gi0 = i0 + x0;
@@ -348,6 +376,16 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
       else step(q, false);
     }
   }
+#if FTN_W3_TRACE
+  if (threadIdx.x == 0 && w3_trace) {
+    uint64_t tr1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+    w3_trace[4 * b + 0] = (long long)tr0;
+    w3_trace[4 * b + 1] = (long long)tr1;
+    w3_trace[4 * b + 2] = tr_edge;
+    w3_trace[4 * b + 3] = tr_in;
+  }
+#endif
 }
 
 template <int T>
@@ -410,18 +448,51 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     e.sm3 = src->dim[2].sm;
     mp = &e.map;
   }
-  // one persistent wave, equal weighted work per CTA (edge tiles run the select path:
-  // FTN_W3_EDGE_W = their cost in 1/8 of an interior tile's)
-  static const int64_t w_edge = getenv("FTN_W3_EDGE_W") ? atoll(getenv("FTN_W3_EDGE_W")) : 12;  // 8: 507, 12: 616, 16: 614, 24: 592 GLUPS (2048^3, T = 3)
+  // one persistent wave, equal weighted work per CTA.  Weights in eighths of an interior tile
+  // (FTN_W3_EDGE_W = "i,j"); per-CTA durations at 2048^3 (FTN_W3_TRACE builds): a tile of the first /
+  // last tile column costs ~1.75x an interior one, another tile of the first / last tile row
+  // ~1.4x (their boxes overhang the array in the contiguous dimension resp. by whole rows).
+  static int64_t wi_e = 16, wj_e = 11;  // 2048^3 / 512^3 GLUPS: (12,12) 611 / 405, (14,11) 616 / 455, (16,11) 618 / 497
+  static const bool parsed = [] {
+    if (const char* e = getenv("FTN_W3_EDGE_W")) {
+      long long a = 0, b = 0;
+      const int n = sscanf(e, "%lld,%lld", &a, &b);
+      if (n >= 1 && a > 0) wi_e = a;
+      wj_e = n == 2 && b > 0 ? b : wi_e;
+    }
+    return true;
+  }();
+  (void)parsed;
   p.w_in = 8;
-  p.w_edge = w_edge > 0 ? w_edge : 8;
+  p.w_iedge = wi_e;
+  p.w_jedge = wj_e;
   const int64_t TI = p.tiles_i, TJ = p.tiles_j;
-  const int64_t row_edge = TI * p.w_edge, row_mid = TI <= 2 ? TI * p.w_edge : 2 * p.w_edge + (TI - 2) * p.w_in;
-  p.W = (TJ <= 2 ? TJ * row_edge : 2 * row_edge + (TJ - 2) * row_mid) * nk;
+  auto row_total = [&](int64_t wm) { return TI == 1 ? p.w_iedge : 2 * p.w_iedge + (TI - 2) * wm; };
+  p.W = (TJ == 1 ? row_total(p.w_jedge) : 2 * row_total(p.w_jedge) + (TJ - 2) * row_total(p.w_in)) * nk;
   int64_t grid = num_sms();
   const int64_t need = (TI * TJ * nk + 15) / 16;  // at least ~16 planes of a tile per CTA
   if (grid > need) grid = need < 1 ? 1 : need;
   p.G = grid;
+#if FTN_W3_TRACE
+  {
+    static long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 4 * 8 * 1024);
+    cudaMemcpyToSymbolAsync(w3_trace, &buf, sizeof(buf), 0, cudaMemcpyHostToDevice, s);
+    static int calls = 0;
+    if (getenv("FTN_W3_TRACE_DUMP") && ++calls == atoi(getenv("FTN_W3_TRACE_DUMP"))) {
+      jacobi3d_wr<T><<<(unsigned)grid, W3_THREADS, C::SMEM, s>>>(*mp, p);
+      std::vector<long long> h(4 * grid);
+      cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      long long t0 = h[0];
+      for (int64_t i = 0; i < grid; ++i) t0 = std::min(t0, h[4 * i]);
+      for (int64_t i = 0; i < grid; ++i)
+        fprintf(stderr, "W3TRACE %lld %lld %lld %lld %lld\n", (long long)i, h[4 * i] - t0, h[4 * i + 1] - t0,
+                h[4 * i + 2], h[4 * i + 3]);
+      return after_launch("jacobi3d_wr");
+    }
+  }
+#endif
   jacobi3d_wr<T><<<(unsigned)grid, W3_THREADS, C::SMEM, s>>>(*mp, p);
   return after_launch("jacobi3d_wr");
 }
