@@ -110,6 +110,7 @@ def lib():
             "orc_pw_advection_f64": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_void_p, ctypes.c_void_p,
                                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                                     ctypes.c_double]),
+            "orc_tra_adv_f64": (ctypes.c_int, [P, P, P, P, P, P, P, P, P, P, P, ctypes.c_void_p, ctypes.c_int64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -374,6 +375,19 @@ def jacobi_solve(u: FArray, unew: FArray, max_sweeps: int, check_every: int, tol
     _check(lib().orc_jacobi_solve_f64(u.ref(), unew.ref(), max_sweeps, check_every, tol, coeff, ctypes.byref(d),
                                       ctypes.byref(r), ctypes.byref(n)), "jacobi_solve")
     return d.value, r.value, bool(n.value)
+
+
+def tra_adv(md: FArray, tsn: FArray, pun: FArray, pvn: FArray, pwn: FArray, umask: FArray, vmask: FArray,
+            tmask: FArray, ztfreez: FArray, rnfmsk: FArray, upsmsk: FArray, rnfmsk_z, iters: int) -> None:
+    """The tra-adv DO nests (R#28): 3-D fields indexed (ji, jj, jk), the
+    2-D fields (ji, jj), rnfmsk_z a float64 vector of length jpk; md is updated in place."""
+    nk = md.shape[2]
+    z = np.ascontiguousarray(np.asarray(rnfmsk_z, dtype=np.float64))
+    if z.shape != (nk,):
+        raise ValueError("tra_adv: rnfmsk_z must have length jpk")
+    _check(lib().orc_tra_adv_f64(md.ref(), tsn.ref(), pun.ref(), pvn.ref(), pwn.ref(), umask.ref(), vmask.ref(),
+                                 tmask.ref(), ztfreez.ref(), rnfmsk.ref(), upsmsk.ref(), ctypes.c_void_p(z.ctypes.data),
+                                 iters), "tra_adv")
 
 
 def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FArray, tzc1, tzc2, tzd1, tzd2,

@@ -946,6 +946,200 @@ int orc_pw_advection_f64(const orc_array* su, const orc_array* sv, const orc_arr
   return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* tra-adv (R#28): the NEMO tracer-advection benchmark the paper   */
+/* runs ("tra-adv": "a tracer advection scheme from the NEMO ocean model benchmarking  */
+/* suite ... six fields on a three dimensional grid of size 1024 by 512 by 512, running over */
+/* 20 iterations").  Its body is NOT in the paper; this is the PSyclone NEMO benchmark's     */
+/* tra_adv loop nest as recalled in DESIGN.md R#28 (not checked against the source), written */
+/* as the Fortran DO nests in their order, fields indexed (ji, jj, jk), ji contiguous.        */
+/* Temporaries zind, zwx, zwy, zslpx, zslpy are zero at the start of the call (R#28) and keep */
+/* their values from one iteration to the next; zdt = zbtr = 1.                              */
+/*   do jt = 1, iters                                                                        */
+/*    (1) zind = 1 - MAX(rnfmsk*rnfmsk_z, upsmsk, zice) * tmask, zice = tsn <= ztfreez+0.1    */
+/*    (2) zwx(:,:,jpk) = 0; zwy(:,:,jpk) = 0                                                 */
+/*        jk<jpk, jj<jpj, ji<jpi: zwx = umask*(md(ji+1)-md); zwy = vmask*(md(jj+1)-md)        */
+/*    (3) zslpx(:,:,jpk) = 0; zslpy(:,:,jpk) = 0                                              */
+/*        jk<jpk, jj>=2, ji>=2: zslpx = (zwx + zwx(ji-1)) * (0.25 + SIGN(0.25, zwx*zwx(ji-1))) */
+/*                              zslpy = (zwy + zwy(jj-1)) * (0.25 + SIGN(0.25, zwy*zwy(jj-1))) */
+/*    (4) same range: zslpx = SIGN(1, zslpx) * MIN(ABS(zslpx), 2*ABS(zwx(ji-1)), 2*ABS(zwx))  */
+/*                    zslpy = SIGN(1, zslpy) * MIN(ABS(zslpy), 2*ABS(zwy(jj-1)), 2*ABS(zwy))  */
+/*    (5) jk<jpk, 2<=jj<jpj, 2<=ji<jpi:                                                       */
+/*          z0u = SIGN(0.5, pun); zalpha = 0.5 - z0u; zu = z0u - 0.5*pun*zdt                  */
+/*          zzwx = md(ji+1) + zind*(zu*zslpx(ji+1)); zzwy = md + zind*(zu*zslpx)              */
+/*          zwx = pun*(zalpha*zzwx + (1-zalpha)*zzwy)                                         */
+/*          z0v = SIGN(0.5, pvn); zalpha = 0.5 - z0v; zv = z0v - 0.5*pvn*zdt                  */
+/*          zzwx = md(jj+1) + zind*(zv*zslpy(jj+1)); zzwy = md + zind*(zv*zslpy)              */
+/*          zwy = pvn*(zalpha*zzwx + (1-zalpha)*zzwy)                                         */
+/*    (6) same range: md = md + (-zbtr*(zwx - zwx(ji-1) + zwy - zwy(jj-1)))                  */
+/*    (7) zwx(:,:,1) = 0; zwx(:,:,jpk) = 0; 2<=jk<jpk: zwx = tmask*(md(jk-1) - md)            */
+/*    (8) zslpx(:,:,1) = 0; 2<=jk<jpk, all ji, jj:                                            */
+/*          zslpx = (zwx + zwx(jk+1)) * (0.25 + SIGN(0.25, zwx*zwx(jk+1)))                    */
+/*    (9) same: zslpx = SIGN(1, zslpx) * MIN(ABS(zslpx), 2*ABS(zwx(jk+1)), 2*ABS(zwx))        */
+/*   (10) zwx(:,:,1) = pwn(:,:,1)*md(:,:,1)                                                   */
+/*   (11) jk<jpk, 2<=jj<jpj, 2<=ji<jpi:                                                       */
+/*          z0w = SIGN(0.5, pwn(jk+1)); zalpha = 0.5 + z0w; zw = z0w - 0.5*pwn(jk+1)*zdt*zbtr */
+/*          zzwx = md(jk+1) + zind*(zw*zslpx(jk+1)); zzwy = md + zind*(zw*zslpx)              */
+/*          zwx(jk+1) = pwn(jk+1)*(zalpha*zzwx + (1-zalpha)*zzwy)                             */
+/*   (12) same range: md = -zbtr*(zwx - zwx(jk+1))                                            */
+/* Fortran evaluation: left to right for * and -, parentheses as written; SIGN(a,b) = |a| with */
+/* the sign of b (a -0 b gives -|a|); MIN/MAX/ABS exact.  One rounding per operation.        */
+/* ------------------------------------------------------------------------ */
+#define TA(a, i, j, k) (*(double*)((a)->base + (i) * (a)->dim[0].sm + (j) * (a)->dim[1].sm + (k) * (a)->dim[2].sm))
+#define TA2(a, i, j) (*(const double*)((a)->base + (i) * (a)->dim[0].sm + (j) * (a)->dim[1].sm))
+static double f_sign(double a, double b) { return copysign(fabs(a), b); }
+
+int orc_tra_adv_f64(const orc_array* md, const orc_array* tsn, const orc_array* pun, const orc_array* pvn,
+                    const orc_array* pwn, const orc_array* umask, const orc_array* vmask, const orc_array* tmask,
+                    const orc_array* ztfreez, const orc_array* rnfmsk, const orc_array* upsmsk,
+                    const double* rnfmsk_z, int64_t iters) {
+  const orc_array* f3[8] = {md, tsn, pun, pvn, pwn, umask, vmask, tmask};
+  for (int q = 0; q < 8; ++q) {
+    if (f3[q]->rank != 3) return ORC_ERANK;
+    if (f3[q]->type != ORC_F64) return ORC_ETYPE;
+    for (int d = 0; d < 3; ++d) if (f3[q]->dim[d].ext != md->dim[d].ext) return ORC_ESHAPE;
+  }
+  const orc_array* f2[3] = {ztfreez, rnfmsk, upsmsk};
+  for (int q = 0; q < 3; ++q) {
+    if (f2[q]->rank != 2) return ORC_ERANK;
+    if (f2[q]->type != ORC_F64) return ORC_ETYPE;
+    for (int d = 0; d < 2; ++d) if (f2[q]->dim[d].ext != md->dim[d].ext) return ORC_ESHAPE;
+  }
+  if (iters < 0) return ORC_ESHAPE;
+  const int64_t ni = md->dim[0].ext, nj = md->dim[1].ext, nk = md->dim[2].ext, n = ni * nj * nk;
+  if (n == 0 || iters == 0) return ORC_OK;
+  /* temporaries: zero at the start of the call (R#28), packed (ji, jj, jk) */
+  double* buf = (double*)calloc((size_t)(5 * n), sizeof(double));
+  if (!buf) return ORC_ESHAPE;
+  orc_array tmp[5];
+  for (int q = 0; q < 5; ++q) {
+    tmp[q].base = (char*)(buf + q * n);
+    tmp[q].type = ORC_F64;
+    tmp[q].rank = 3;
+    tmp[q].dim[0] = (orc_dim){1, ni, 8};
+    tmp[q].dim[1] = (orc_dim){1, nj, 8 * ni};
+    tmp[q].dim[2] = (orc_dim){1, nk, 8 * ni * nj};
+  }
+  const orc_array *zind = &tmp[0], *zwx = &tmp[1], *zwy = &tmp[2], *zslpx = &tmp[3], *zslpy = &tmp[4];
+  const double zdt = 1.0, zbtr = 1.0;
+  for (int64_t jt = 0; jt < iters; ++jt) {
+    /* (1) */
+    for (int64_t k = 0; k < nk; ++k)
+      for (int64_t j = 0; j < nj; ++j)
+        for (int64_t i = 0; i < ni; ++i) {
+          const double zice = TA(tsn, i, j, k) <= TA2(ztfreez, i, j) + 0.1 ? 1.0 : 0.0;
+          double m = TA2(rnfmsk, i, j) * rnfmsk_z[k];
+          m = fmax(fmax(m, TA2(upsmsk, i, j)), zice);
+          TA(zind, i, j, k) = 1.0 - m * TA(tmask, i, j, k);
+        }
+    /* (2) */
+    for (int64_t j = 0; j < nj; ++j)
+      for (int64_t i = 0; i < ni; ++i) TA(zwx, i, j, nk - 1) = TA(zwy, i, j, nk - 1) = 0.0;
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 0; j < nj - 1; ++j)
+        for (int64_t i = 0; i < ni - 1; ++i) {
+          TA(zwx, i, j, k) = TA(umask, i, j, k) * (TA(md, i + 1, j, k) - TA(md, i, j, k));
+          TA(zwy, i, j, k) = TA(vmask, i, j, k) * (TA(md, i, j + 1, k) - TA(md, i, j, k));
+        }
+    /* (3) */
+    for (int64_t j = 0; j < nj; ++j)
+      for (int64_t i = 0; i < ni; ++i) TA(zslpx, i, j, nk - 1) = TA(zslpy, i, j, nk - 1) = 0.0;
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj; ++j)
+        for (int64_t i = 1; i < ni; ++i) {
+          const double ax = TA(zwx, i, j, k), bx = TA(zwx, i - 1, j, k);
+          TA(zslpx, i, j, k) = (ax + bx) * (0.25 + f_sign(0.25, ax * bx));
+          const double ay = TA(zwy, i, j, k), by = TA(zwy, i, j - 1, k);
+          TA(zslpy, i, j, k) = (ay + by) * (0.25 + f_sign(0.25, ay * by));
+        }
+    /* (4) */
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj; ++j)
+        for (int64_t i = 1; i < ni; ++i) {
+          const double sx = TA(zslpx, i, j, k);
+          TA(zslpx, i, j, k) = f_sign(1.0, sx) * fmin(fmin(fabs(sx), 2.0 * fabs(TA(zwx, i - 1, j, k))),
+                                                      2.0 * fabs(TA(zwx, i, j, k)));
+          const double sy = TA(zslpy, i, j, k);
+          TA(zslpy, i, j, k) = f_sign(1.0, sy) * fmin(fmin(fabs(sy), 2.0 * fabs(TA(zwy, i, j - 1, k))),
+                                                      2.0 * fabs(TA(zwy, i, j, k)));
+        }
+    /* (5) */
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj - 1; ++j)
+        for (int64_t i = 1; i < ni - 1; ++i) {
+          const double zi = TA(zind, i, j, k), u = TA(pun, i, j, k), v = TA(pvn, i, j, k);
+          const double z0u = f_sign(0.5, u);
+          double zalpha = 0.5 - z0u;
+          const double zu = z0u - (0.5 * u) * zdt;
+          double zzwx = TA(md, i + 1, j, k) + zi * (zu * TA(zslpx, i + 1, j, k));
+          double zzwy = TA(md, i, j, k) + zi * (zu * TA(zslpx, i, j, k));
+          TA(zwx, i, j, k) = u * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+          const double z0v = f_sign(0.5, v);
+          zalpha = 0.5 - z0v;
+          const double zv = z0v - (0.5 * v) * zdt;
+          zzwx = TA(md, i, j + 1, k) + zi * (zv * TA(zslpy, i, j + 1, k));
+          zzwy = TA(md, i, j, k) + zi * (zv * TA(zslpy, i, j, k));
+          TA(zwy, i, j, k) = v * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+        }
+    /* (6) */
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj - 1; ++j)
+        for (int64_t i = 1; i < ni - 1; ++i) {
+          const double ztra = -(zbtr * (((TA(zwx, i, j, k) - TA(zwx, i - 1, j, k)) + TA(zwy, i, j, k)) -
+                                        TA(zwy, i, j - 1, k)));
+          TA(md, i, j, k) = TA(md, i, j, k) + ztra;
+        }
+    /* (7) */
+    for (int64_t j = 0; j < nj; ++j)
+      for (int64_t i = 0; i < ni; ++i) TA(zwx, i, j, 0) = TA(zwx, i, j, nk - 1) = 0.0;
+    for (int64_t k = 1; k < nk - 1; ++k)
+      for (int64_t j = 0; j < nj; ++j)
+        for (int64_t i = 0; i < ni; ++i)
+          TA(zwx, i, j, k) = TA(tmask, i, j, k) * (TA(md, i, j, k - 1) - TA(md, i, j, k));
+    /* (8) */
+    for (int64_t j = 0; j < nj; ++j)
+      for (int64_t i = 0; i < ni; ++i) TA(zslpx, i, j, 0) = 0.0;
+    for (int64_t k = 1; k < nk - 1; ++k)
+      for (int64_t j = 0; j < nj; ++j)
+        for (int64_t i = 0; i < ni; ++i) {
+          const double a = TA(zwx, i, j, k), b = TA(zwx, i, j, k + 1);
+          TA(zslpx, i, j, k) = (a + b) * (0.25 + f_sign(0.25, a * b));
+        }
+    /* (9) */
+    for (int64_t k = 1; k < nk - 1; ++k)
+      for (int64_t j = 0; j < nj; ++j)
+        for (int64_t i = 0; i < ni; ++i) {
+          const double sx = TA(zslpx, i, j, k);
+          TA(zslpx, i, j, k) = f_sign(1.0, sx) * fmin(fmin(fabs(sx), 2.0 * fabs(TA(zwx, i, j, k + 1))),
+                                                      2.0 * fabs(TA(zwx, i, j, k)));
+        }
+    /* (10) */
+    for (int64_t j = 0; j < nj; ++j)
+      for (int64_t i = 0; i < ni; ++i) TA(zwx, i, j, 0) = TA(pwn, i, j, 0) * TA(md, i, j, 0);
+    /* (11) */
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj - 1; ++j)
+        for (int64_t i = 1; i < ni - 1; ++i) {
+          const double w1 = TA(pwn, i, j, k + 1), zi = TA(zind, i, j, k);
+          const double z0w = f_sign(0.5, w1);
+          const double zalpha = 0.5 + z0w;
+          const double zw = z0w - ((0.5 * w1) * zdt) * zbtr;
+          const double zzwx = TA(md, i, j, k + 1) + zi * (zw * TA(zslpx, i, j, k + 1));
+          const double zzwy = TA(md, i, j, k) + zi * (zw * TA(zslpx, i, j, k));
+          TA(zwx, i, j, k + 1) = w1 * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+        }
+    /* (12) */
+    for (int64_t k = 0; k < nk - 1; ++k)
+      for (int64_t j = 1; j < nj - 1; ++j)
+        for (int64_t i = 1; i < ni - 1; ++i)
+          TA(md, i, j, k) = -(zbtr * (TA(zwx, i, j, k) - TA(zwx, i, j, k + 1)));
+  }
+  free(buf);
+  return ORC_OK;
+}
+#undef TA
+#undef TA2
+
 /* Timing helper for bench.py's cpu_baseline (not part of any computed result): the number of
  * OpenMP threads the parallel loops above use; returns the previous setting (1 without OpenMP). */
 int orc_set_threads(int n) {
