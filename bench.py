@@ -599,6 +599,34 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                 "roofline": {"bound": "hbm", "bytes_per_cell": 48, "frac": gbs / N / hbm_peak}}
             del F, O, Z
             torch.cuda.empty_cache()
+        # tra-adv (R#28): the NEMO tracer advection, 1024 x 512 x 512, 20 iterations
+        # per step.  Algorithmic: 72 B per cell and iteration (md read and written, the seven
+        # other 3-D fields read once); the 8-pass implementation moves 288 B (its temporaries
+        # zind, zwx, zwy, zslpx, zslpy go through HBM), which the roofline line states
+        ni, nj, nk, iters = 1024, 512 // N if N > 1 else 512, 512, 20
+        if torch.cuda.mem_get_info()[0] > 14 * ni * nj * nk * 8 + (2 << 30):
+            D = [ftn.FArray.empty((ni, nj, nk)) for _ in range(8)]
+            for q, d in enumerate(D[:5]):
+                ftn.gen_fill(d, SEED, 70 + q + 10 * rank, ftn.GEN_U11)
+            for q, d in enumerate(D[5:]):
+                ftn.gen_fill(d, SEED, 80 + q, ftn.GEN_U01)
+            D2 = [ftn.FArray.empty((ni, nj)) for _ in range(3)]
+            for q, d in enumerate(D2):
+                ftn.gen_fill(d, SEED, 90 + q, ftn.GEN_U01)
+            RZ = ftn.FArray.empty((nk,))
+            ftn.gen_fill(RZ, SEED, 95, ftn.GEN_U01)
+            t = timed(torch, lambda: ftn.tra_adv(*D, *D2, RZ, iters), max(2, steps // 4), 1, None, dist)
+            ns = max(2, steps // 4)
+            cells = ni * nj * nk * N
+            gcs = cells * iters * ns / t / 1e9
+            gbs = 72 * cells * iters * ns / t / 1e9
+            rows["f4_tra_adv_1024x512x512_x20"] = {
+                "value": gcs, "unit": "Gcell-iterations/s", "ms_per_step": t / ns * 1e3, "achieved_gbs": gbs,
+                "roofline": {"bound": "hbm", "algorithmic_bytes_per_cell_iteration": 72,
+                             "implementation_bytes_per_cell_iteration": 288, "frac": gbs / N / hbm_peak,
+                             "frac_of_moved_bytes": 4 * gbs / N / hbm_peak}}
+            del D, D2, RZ
+            torch.cuda.empty_cache()
     # SURVEY §8(e) strong scaling, predicted on one GPU: each rank's share at p = 8 run alone
     # (no exchange), against the same kernel on the whole 1-GPU problem: the compute side of
     # the 1 -> 8 efficiency (wave quantisation, halo recompute, shorter streams)

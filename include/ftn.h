@@ -323,6 +323,22 @@ ftn_status_t ftn_pw_advection(const ftn_desc_t* su, const ftn_desc_t* sv, const 
                               const ftn_desc_t* tzc1, const ftn_desc_t* tzc2, const ftn_desc_t* tzd1,
                               const ftn_desc_t* tzd2, double tcx, double tcy, ftn_stream_t stream);
 
+/* tra-adv (the paper's NEMO tracer-advection benchmark, P:92 -- its body is
+ * not in the paper; R#28 gives the recalled loop nests this implements, identical
+ * to oracle/ftn_oracle.c's orc_tra_adv_f64): `iters` iterations updating the tracer md in
+ * place from the velocities pun, pvn, pwn, the masks umask, vmask, tmask, the temperature
+ * tsn (3-D, real(8), conformable, indexed (ji, jj, jk)), ztfreez, rnfmsk, upsmsk (2-D, extents
+ * (jpi, jpj)) and rnfmsk_z (1-D, extent jpk).  Any strides.  The temporaries zind, zwx, zwy,
+ * zslpx, zslpy live in the caller's workspace (ftn_tra_adv_workspace_size bytes, 256-byte
+ * aligned), are zeroed at the start of the call and carry over between iterations (R#28).
+ * md must not overlap an input (FTN_ERR_SHAPE); jpj, jpk <= 65535.  Bit-exact vs the oracle. */
+ftn_status_t ftn_tra_adv_workspace_size(const ftn_desc_t* md, size_t* bytes);
+ftn_status_t ftn_tra_adv(const ftn_desc_t* md, const ftn_desc_t* tsn, const ftn_desc_t* pun, const ftn_desc_t* pvn,
+                         const ftn_desc_t* pwn, const ftn_desc_t* umask, const ftn_desc_t* vmask,
+                         const ftn_desc_t* tmask, const ftn_desc_t* ztfreez, const ftn_desc_t* rnfmsk,
+                         const ftn_desc_t* upsmsk, const ftn_desc_t* rnfmsk_z, int64_t iters, void* ws,
+                         size_t ws_bytes, ftn_stream_t stream);
+
 /* ---------------------------------------------------------------- a8
  * Multi-GPU (one process per GPU, NCCL over NVLink).  The id travels between
  * processes through the caller's own channel (torch.distributed store). */

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "ftn")
 LIB = os.path.join(PKG, "libftn.so")
-SOURCES = ["desc", "elemental", "reduce", "reduce_dim", "transpose", "matmul", "stencil", "stencil_tb", "stencil_wq", "stencil3d_tb", "stencil3d_wr", "advection", "dist"]
+SOURCES = ["desc", "elemental", "reduce", "reduce_dim", "transpose", "matmul", "stencil", "stencil_tb", "stencil_wq", "stencil3d_tb", "stencil3d_wr", "advection", "tra_adv", "dist"]
 
 
 def nccl_root() -> str:

@@ -117,6 +117,8 @@ def _load():
         "ftn_jacobi_set_fusion": [ctypes.c_int32],
         "ftn_jacobi_host": [vp, vp, P, P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), vp],
         "ftn_pw_advection": [P, P, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_double, vp],
+        "ftn_tra_adv_workspace_size": [P, szp],
+        "ftn_tra_adv": [P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_int64, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -462,6 +464,19 @@ def pw_advection(su: FArray, sv: FArray, sw: FArray, u: FArray, v: FArray, w: FA
     """pw-advection (R#26): su, sv, sw at the interior points."""
     _call("ftn_pw_advection", su.ref(), sv.ref(), sw.ref(), u.ref(), v.ref(), w.ref(), tzc1.ref(), tzc2.ref(),
           tzd1.ref(), tzd2.ref(), tcx, tcy, _stream(stream))
+
+
+def tra_adv(md: FArray, tsn: FArray, pun: FArray, pvn: FArray, pwn: FArray, umask: FArray, vmask: FArray,
+            tmask: FArray, ztfreez: FArray, rnfmsk: FArray, upsmsk: FArray, rnfmsk_z: FArray, iters: int,
+            stream=None) -> None:
+    """tra-adv (R#28): `iters` iterations of the NEMO tracer-advection nests,
+    md updated in place (fields (ji, jj, jk); ztfreez, rnfmsk, upsmsk (ji, jj); rnfmsk_z (jk))."""
+    n = ctypes.c_size_t()
+    _call("ftn_tra_adv_workspace_size", md.ref(), ctypes.byref(n))
+    ws = workspace(n.value, md.tensor.device, "tra_adv", stream)
+    _call("ftn_tra_adv", md.ref(), tsn.ref(), pun.ref(), pvn.ref(), pwn.ref(), umask.ref(), vmask.ref(), tmask.ref(),
+          ztfreez.ref(), rnfmsk.ref(), upsmsk.ref(), rnfmsk_z.ref(), iters, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+          _stream(stream))
 
 
 def jacobi_set_fusion(sweeps_per_launch: int):
