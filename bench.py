@@ -601,8 +601,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             torch.cuda.empty_cache()
         # tra-adv (R#28): the NEMO tracer advection, 1024 x 512 x 512, 20 iterations
         # per step.  Algorithmic: 72 B per cell and iteration (md read and written, the seven
-        # other 3-D fields read once); the 8-pass implementation moves 288 B (its temporaries
-        # zind, zwx, zwy, zslpx, zslpy go through HBM), which the roofline line states
+        # other 3-D fields read once); the two fused passes move ~115 B (ncu: the horizontal
+        # pass writes md6 and zind, the vertical pass reads them back), which the line states
         ni, nj, nk, iters = 1024, 512 // N if N > 1 else 512, 512, 20
         if torch.cuda.mem_get_info()[0] > 14 * ni * nj * nk * 8 + (2 << 30):
             D = [ftn.FArray.empty((ni, nj, nk)) for _ in range(8)]
@@ -623,8 +623,8 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             rows["f4_tra_adv_1024x512x512_x20"] = {
                 "value": gcs, "unit": "Gcell-iterations/s", "ms_per_step": t / ns * 1e3, "achieved_gbs": gbs,
                 "roofline": {"bound": "hbm", "algorithmic_bytes_per_cell_iteration": 72,
-                             "implementation_bytes_per_cell_iteration": 288, "frac": gbs / N / hbm_peak,
-                             "frac_of_moved_bytes": 4 * gbs / N / hbm_peak}}
+                             "implementation_bytes_per_cell_iteration": 115, "frac": gbs / N / hbm_peak,
+                             "frac_of_moved_bytes": 115 / 72 * gbs / N / hbm_peak}}
             del D, D2, RZ
             torch.cuda.empty_cache()
     # SURVEY §8(e) strong scaling, predicted on one GPU: each rank's share at p = 8 run alone

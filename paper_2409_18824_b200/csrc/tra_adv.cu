@@ -1,11 +1,14 @@
 // tra-adv (R#28): the NEMO tracer-advection benchmark the paper
 // runs ("six fields on a three dimensional grid of size 1024 by 512 by 512, running over
-// 20 iterations"), its loop nests as recalled in R#28 -- the same statements, in the same
-// order, with the same Fortran evaluation order as oracle/ftn_oracle.c's orc_tra_adv_f64, so
-// results are bit-identical (-fmad=false; SIGN = copysign, MIN / MAX / ABS exact).
+// 20 iterations"), its loop nests as recalled in R#28 -- the same statements, with the same
+// Fortran evaluation order as oracle/ftn_oracle.c's orc_tra_adv_f64, so results are
+// bit-identical (-fmad=false; SIGN = copysign, MIN / MAX / ABS exact).  Fields are indexed
+// (ji, jj, jk), ji contiguous.
 //
-// Fields are indexed (ji, jj, jk), ji contiguous.  One iteration is eight passes, each a
-// kernel over its index range with one thread per ji (coalesced) and a block per (jj, jk) row:
+// Default: two fused passes per iteration (ta_h, ta_v below), ~115 B per cell moved against
+// the algorithmic 72 B.  FTN_TA_PASSES=8: the eight-pass version (K1..K8, one kernel per group
+// of loop nests, every temporary through HBM: 288 B per cell), kept as the plain reference
+// of the fusion:
 //   K1  steps 1-2   zind (all points); zwx, zwy (ji < jpi-1, jj < jpj-1, jk < jpk-1; 0 at jk = jpk-1)
 //   K2  steps 3-4   slopes zslpx, zslpy (ji >= 1, jj >= 1, jk < jpk-1; 0 at jk = jpk-1): step 4
 //                   at a point reads only step 3's value at that point, so the two fuse per point
@@ -15,10 +18,11 @@
 //   K6  steps 8-9   vertical slopes zslpx (all ji, jj, 1 <= jk < jpk-1; 0 at jk = 0)
 //   K7  steps 10-11 vertical fluxes: zwx(:,:,0) = pwn md, zwx(jk+1) (interior) -- reads no zwx
 //   K8  step 12     md = -(zwx - zwx(jk+1)) (interior)
-// Each pass is HBM-bound; the temporaries live in the caller's workspace (5 packed arrays),
-// zeroed at the start of the call (R#28).
+// The temporaries live in the caller's workspace (5 packed arrays), zeroed at the start of the
+// call (R#28).
 #include "ftn_internal.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace ftn {
@@ -176,6 +180,249 @@ __global__ void __launch_bounds__(256) ta_k8(const __grid_constant__ TAParams p,
   p.md(i, j, k) = -(1.0 * (p.zwx(i, j, k) - p.zwx(i, j, k + 1)));
 }
 
+// ---------------------------------------------------------------- fused: two passes per iteration
+// H: steps 1-6 for one (jk, 32 x 8 tile), every intermediate in shared memory (halo 2 in ji
+//    and jj); writes zind and md6 (the tracer after step 6) -- 72 B per cell instead of 192.
+// V: steps 7-12 for one (ji, jj) column, streaming jk with the vertical gradients, slopes and
+//    fluxes in registers; writes md and, for the column ji = jpi-1, the side buffer S(jj, jk)
+//    = its final zwx, which the next iteration's step 3 reads (R#28: the temporaries carry
+//    over) -- 40 B per cell instead of 96.
+#ifndef FTN_TA_TX
+#define FTN_TA_TX 32
+#endif
+#ifndef FTN_TA_TY
+#define FTN_TA_TY 32
+#endif
+constexpr int TH_X = FTN_TA_TX, TH_Y = FTN_TA_TY;  // output tile per CTA of 32 x 8 threads
+
+struct TAFused {
+  F3 md6;       // workspace: the tracer after step 6
+  double* side; // workspace: zwx(jpi-1, jj, jk), jj + jpj * jk
+};
+
+__device__ __forceinline__ double ta_limit(double a, double b) {  // steps 3-4 / 8-9: slope of (a, b)
+  const double s = (a + b) * (0.25 + fsign(0.25, a * b));
+  return fsign(1.0, s) * fmin(fmin(fabs(s), 2.0 * fabs(b)), 2.0 * fabs(a));
+}
+
+__device__ __forceinline__ double ta_zind(const TAParams& p, int64_t i, int64_t j, int64_t k) {
+  const double zice = p.tsn(i, j, k) <= p.ztfreez(i, j) + 0.1 ? 1.0 : 0.0;
+  double m = p.rnfmsk(i, j) * *reinterpret_cast<const double*>(p.rz + k * p.rz_s);
+  m = fmax(fmax(m, p.upsmsk(i, j)), zice);
+  return 1.0 - m * p.tmask(i, j, k);
+}
+
+// Shared-memory regions of one tile (origin i0, j0), each [rows][cols] with its own offsets:
+//   md  i0-2 .. i0+33, j0-2 .. j0+33    zi  i0-1 .. i0+31, j0-1 .. j0+31 (zind)
+//   wx  s = i0-2 .. i0+32, tile rows    wy  tile columns, t = j0-2 .. j0+32   (step 2)
+//   sx  s = i0-1 .. i0+32, tile rows    sy  tile columns, t = j0-1 .. j0+32   (steps 3-4)
+//   fx  f = i0-1 .. i0+31, tile rows    fy  tile columns, g = j0-1 .. j0+31   (step 5)
+// Loops walk rows with the 8 thread rows and columns with the 32 lanes (no divisions).
+struct TASmem {
+  double md[TH_Y + 4][TH_X + 4];
+  double zi[TH_Y + 1][TH_X + 1];
+  double wx[TH_Y][TH_X + 3];
+  double wy[TH_Y + 3][TH_X];
+  double sx[TH_Y][TH_X + 2];
+  double sy[TH_Y + 2][TH_X];
+};
+
+__global__ void __launch_bounds__(256) ta_h(const __grid_constant__ TAParams p, const __grid_constant__ TAFused q) {
+  extern __shared__ double ta_smem_raw[];
+  TASmem& S = *reinterpret_cast<TASmem*>(ta_smem_raw);
+  constexpr int MX = TH_X / 32, RY = TH_Y / 8;  // columns per lane, rows per thread row
+  const int64_t ni = p.ni, nj = p.nj, nk = p.nk;
+  const int64_t i0 = (int64_t)blockIdx.x * TH_X, j0 = (int64_t)blockIdx.y * TH_Y, k = blockIdx.z;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (k == nk - 1) {  // top plane: zind only, md6 = md
+    for (int ly = ty; ly < TH_Y; ly += 8)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int64_t i = i0 + tx + 32 * m, j = j0 + ly;
+        if (i < ni && j < nj) {
+          p.zind(i, j, k) = ta_zind(p, i, j, k);
+          q.md6(i, j, k) = p.md(i, j, k);
+        }
+      }
+    return;
+  }
+  // md over the halo-2 region
+  for (int ly = ty; ly < TH_Y + 4; ly += 8) {
+    const int64_t j = j0 - 2 + ly;
+    for (int lx = tx; lx < TH_X + 4; lx += 32) {
+      const int64_t i = i0 - 2 + lx;
+      S.md[ly][lx] = (i >= 0 && i < ni && j >= 0 && j < nj) ? p.md(i, j, k) : 0.0;
+    }
+  }
+  // zind over i0-1 .. i0+TH_X-1, j0-1 .. j0+TH_Y-1; the tile's own points go to global for pass V
+  for (int ly = ty; ly < TH_Y + 1; ly += 8) {
+    const int64_t j = j0 - 1 + ly;
+    for (int lx = tx; lx < TH_X + 1; lx += 32) {
+      const int64_t i = i0 - 1 + lx;
+      double z = 0.0;
+      if (i >= 0 && i < ni && j >= 0 && j < nj) {
+        z = ta_zind(p, i, j, k);
+        if (lx >= 1 && ly >= 1) p.zind(i, j, k) = z;
+      }
+      S.zi[ly][lx] = z;
+    }
+  }
+  __syncthreads();
+  // step 2 (and the carried-over zwx of the last column, R#28)
+  for (int ly = ty; ly < TH_Y; ly += 8) {
+    const int64_t j = j0 + ly;
+    for (int lx = tx; lx < TH_X + 3; lx += 32) {
+      const int64_t s = i0 - 2 + lx;
+      double v = 0.0;
+      if (j < nj - 1 && s >= 0 && s < ni - 1) v = p.umask(s, j, k) * (S.md[ly + 2][lx + 1] - S.md[ly + 2][lx]);
+      else if (j < nj && s == ni - 1) v = q.side[j + nj * k];
+      S.wx[ly][lx] = v;
+    }
+  }
+  for (int ly = ty; ly < TH_Y + 3; ly += 8) {
+    const int64_t t = j0 - 2 + ly;
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int c = tx + 32 * m;
+      const int64_t i = i0 + c;
+      double v = 0.0;
+      if (i < ni - 1 && t >= 0 && t < nj - 1) v = p.vmask(i, t, k) * (S.md[ly + 1][c + 2] - S.md[ly][c + 2]);
+      S.wy[ly][c] = v;
+    }
+  }
+  __syncthreads();
+  // steps 3-4
+  for (int ly = ty; ly < TH_Y; ly += 8)
+    for (int lx = tx; lx < TH_X + 2; lx += 32) S.sx[ly][lx] = ta_limit(S.wx[ly][lx + 1], S.wx[ly][lx]);
+  for (int ly = ty; ly < TH_Y + 2; ly += 8)
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int c = tx + 32 * m;
+      S.sy[ly][c] = ta_limit(S.wy[ly + 1][c], S.wy[ly][c]);
+    }
+  __syncthreads();
+  // step 5: x fluxes at f = i0-1 .. i0+TH_X-1 (zwx2(0) where step 5 leaves the boundary
+  // column), y fluxes at g = j0-1 .. j0+TH_Y-1, kept in registers; the y fluxes then replace wy
+  auto xflux = [&](int ly, int lx) {  // f = i0-1+lx, row j0+ly
+    const int64_t f = i0 - 1 + lx, j = j0 + ly;
+    if (f >= 1 && f <= ni - 2 && j >= 1 && j <= nj - 2) {
+      const double zi = S.zi[ly + 1][lx], u = p.pun(f, j, k);
+      const double z0u = fsign(0.5, u);
+      const double zalpha = 0.5 - z0u;
+      const double zu = z0u - (0.5 * u) * 1.0;
+      const double zzwx = S.md[ly + 2][lx + 2] + zi * (zu * S.sx[ly][lx + 1]);
+      const double zzwy = S.md[ly + 2][lx + 1] + zi * (zu * S.sx[ly][lx]);
+      return u * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+    }
+    return f == 0 ? S.wx[ly][lx + 1] : 0.0;
+  };
+  double fx[RY][MX][2], fy[RY + 1][MX];
+#pragma unroll
+  for (int r = 0; r < RY; ++r)
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int ly = ty + 8 * r, c = tx + 32 * m;
+      fx[r][m][0] = xflux(ly, c);       // f = i0 + c - 1
+      fx[r][m][1] = xflux(ly, c + 1);   // f = i0 + c
+    }
+#pragma unroll
+  for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int ly = ty + 8 * r, c = tx + 32 * m;  // g = j0-1+ly (ly < TH_Y + 1)
+      fy[r][m] = 0.0;
+      if (ly >= TH_Y + 1) continue;
+      const int64_t i = i0 + c, g = j0 - 1 + ly;
+      if (g >= 1 && g <= nj - 2 && i >= 1 && i <= ni - 2) {
+        const double zi = S.zi[ly][c + 1], w = p.pvn(i, g, k);
+        const double z0v = fsign(0.5, w);
+        const double zalpha = 0.5 - z0v;
+        const double zv = z0v - (0.5 * w) * 1.0;
+        const double zzwx = S.md[ly + 2][c + 2] + zi * (zv * S.sy[ly + 1][c]);
+        const double zzwy = S.md[ly + 1][c + 2] + zi * (zv * S.sy[ly][c]);
+        fy[r][m] = w * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+      } else if (g == 0) {
+        fy[r][m] = S.wy[ly + 1][c];
+      }
+    }
+  __syncthreads();  // every read of wy / sy is done: wy[ly][c] now holds the y flux at g = j0-1+ly
+#pragma unroll
+  for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int ly = ty + 8 * r, c = tx + 32 * m;
+      if (ly < TH_Y + 1) S.wy[ly][c] = fy[r][m];
+    }
+  __syncthreads();
+  // step 6
+#pragma unroll
+  for (int r = 0; r < RY; ++r)
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int ly = ty + 8 * r, c = tx + 32 * m;
+      const int64_t i = i0 + c, j = j0 + ly;
+      if (i >= ni || j >= nj) continue;
+      double v = S.md[ly + 2][c + 2];
+      if (i >= 1 && i <= ni - 2 && j >= 1 && j <= nj - 2) {
+        const double ztra = -(1.0 * (((fx[r][m][1] - fx[r][m][0]) + S.wy[ly + 1][c]) - S.wy[ly][c]));
+        v = v + ztra;
+      }
+      q.md6(i, j, k) = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) ta_v(const __grid_constant__ TAParams p, const __grid_constant__ TAFused q) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x, j = blockIdx.y;
+  const int64_t ni = p.ni, nj = p.nj, nk = p.nk;
+  if (i >= ni) return;
+  const bool inner = i >= 1 && i <= ni - 2 && j >= 1 && j <= nj - 2;
+  const bool last_col = i == ni - 1;
+  // step 7: zwx7(kk) = tmask (md6(kk-1) - md6(kk)) for 1 <= kk <= nk-2, 0 at kk = 0, nk-1
+  auto zwx7 = [&](int64_t kk, double m_lo, double m_hi) {
+    return (kk >= 1 && kk <= nk - 2) ? p.tmask(i, j, kk) * (m_lo - m_hi) : 0.0;
+  };
+  double m0 = q.md6(i, j, 0);
+  double m1 = nk > 1 ? q.md6(i, j, 1) : 0.0;
+  double z7_0 = 0.0;                                // zwx7(0)
+  double z7_1 = nk > 1 ? zwx7(1, m0, m1) : 0.0;     // zwx7(1)
+  // steps 8-9: zslpx(kk) = limit(zwx7(kk), zwx7(kk+1)) for 1 <= kk <= nk-2, 0 at kk = 0, nk-1
+  double s_prev = 0.0;                              // zslpx(0)
+  // step 10
+  double flux_prev = p.pwn(i, j, 0) * m0;           // zwx(0)
+  if (last_col) q.side[j + nj * 0] = flux_prev;
+  double zi_prev = p.zind(i, j, 0);
+  double m_prev = m0, m_cur = m1, z7_cur = z7_1;
+  (void)z7_0;
+  for (int64_t kk = 1; kk < nk; ++kk) {
+    // plane kk: md6(kk) = m_cur, zwx7(kk) = z7_cur; look ahead to kk+1
+    const double m_next = kk + 1 < nk ? q.md6(i, j, kk + 1) : 0.0;
+    const double z7_next = kk + 1 < nk ? zwx7(kk + 1, m_cur, m_next) : 0.0;
+    const double s_cur = (kk <= nk - 2) ? ta_limit(z7_cur, z7_next) : 0.0;
+    double flux;  // zwx(kk) after steps 7, 10, 11
+    if (inner) {
+      const double w1 = p.pwn(i, j, kk);
+      const double z0w = fsign(0.5, w1);
+      const double zalpha = 0.5 + z0w;
+      const double zw = z0w - ((0.5 * w1) * 1.0) * 1.0;
+      const double zzwx = m_cur + zi_prev * (zw * s_cur);
+      const double zzwy = m_prev + zi_prev * (zw * s_prev);
+      flux = w1 * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+      p.md(i, j, kk - 1) = -(1.0 * (flux_prev - flux));   // step 12 for plane kk-1
+    } else {
+      flux = z7_cur;
+      p.md(i, j, kk - 1) = m_prev;                        // boundary columns: md6 = md
+    }
+    if (last_col) q.side[j + nj * kk] = flux;
+    zi_prev = p.zind(i, j, kk);
+    flux_prev = flux;
+    s_prev = s_cur;
+    m_prev = m_cur;
+    m_cur = m_next;
+    z7_cur = z7_next;
+  }
+  p.md(i, j, nk - 1) = m_prev;  // the top plane: never updated (md6 = md there)
+}
+
 F3 f3_of(const ftn_desc_t* d) {
   F3 f;
   f.b = (char*)d->base_addr;
@@ -283,6 +530,29 @@ ftn_status_t ftn_tra_adv(const ftn_desc_t* md, const ftn_desc_t* tsn, const ftn_
   p.nj = nj;
   p.nk = nk;
   FTN_CUDA(cudaMemsetAsync(ws, 0, need, s));  // R#28: the temporaries start at zero
+  static const bool passes8 = getenv("FTN_TA_PASSES") && atoi(getenv("FTN_TA_PASSES")) == 8;
+  if (!passes8) {
+    if (nj > 65535 || nk > 65535) return fail(FTN_ERR_UNSUPPORTED, "ftn_tra_adv: jpj and jpk must be <= 65535");
+    static std::atomic<bool> attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+      FTN_CUDA(cudaFuncSetAttribute(ta_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TASmem)));
+      attr[dev & 63] = true;
+    }
+    TAFused q;
+    q.md6 = p.zwx;                                        // workspace array 1
+    q.side = reinterpret_cast<double*>(p.zwy.b);          // workspace array 2 (jpj x jpk used)
+    const dim3 gh((unsigned)((ni + TH_X - 1) / TH_X), (unsigned)((nj + TH_Y - 1) / TH_Y), (unsigned)nk);
+    const dim3 gv((unsigned)((ni + 255) / 256), (unsigned)nj);
+    for (int64_t it = 0; it < iters; ++it) {
+      ta_h<<<gh, 256, sizeof(TASmem), s>>>(p, q);
+      FTN_CHECK(after_launch("tra_adv_h"));
+      ta_v<<<gv, 256, 0, s>>>(p, q);
+      FTN_CHECK(after_launch("tra_adv_v"));
+    }
+    return FTN_OK;
+  }
   for (int64_t it = 0; it < iters; ++it) {
     FTN_CHECK(ta_launch(ta_k1, p, 0, ni, 0, nj, 0, nk, s));
     FTN_CHECK(ta_launch(ta_k2, p, 0, ni, 0, nj, 0, nk, s));
