@@ -13,7 +13,8 @@
 // every thread at 168 registers (spills); folding the producer in keeps 2 warps
 // per SMSP.
 //
-// Shared-memory layout (conflict-free fragment loads):
+// Shared-memory layout (fragment loads spread over the banks, DESIGN.md §4 kernel table; ncu still
+// counts ~200 M bank conflicts per 4096^3 product -- harmless, the DMMA pipe is at 97 %):
 //   A stage = 8 TMA boxes {16 (i), 32 (l)}, B stage = 2 boxes {16 (l), 128 (j)},
 //   all with the 128-byte swizzle.  Fortran A is i-fastest, but the m16n8k4 A
 //   fragment puts k across lanes; the MMA's k index t is therefore mapped to the
