@@ -74,3 +74,20 @@ def test_stream_k_transposed_operands(ftn):
     bt = np.asfortranarray(b_h.T)
     ftn.matmul(C, ftn.FArray.from_numpy(a_h), ftn.FArray.from_numpy(bt), transpose_b=True)
     assert np.all(np.abs(C.to_numpy() - co) <= 4 * k * 2.0 ** -53 * ab)
+
+
+def test_stream_k_with_packed_operands(ftn):
+    """Operands the TMA boxes cannot address (a leading dimension of 2049 doubles: rows not
+    16-byte aligned) are packed into the workspace first; the stream-K slots follow the packed
+    copies in the same workspace."""
+    m, n, k = 2048, 1280, 256
+    a_big = synth.farray((m + 1, k), array_id=41, mode=synth.U11)
+    b_big = synth.farray((k + 1, n), array_id=42, mode=synth.U11)
+    A = ftn.FArray.from_numpy(a_big).section((1, m), (1, k))
+    B = ftn.FArray.from_numpy(b_big).section((1, k), (1, n))
+    C = ftn.FArray.empty((m, n))
+    ftn.matmul(C, A, B)
+    a_h, b_h = np.asfortranarray(a_big[:m]), np.asfortranarray(b_big[:k])
+    co, ab = np.zeros((m, n), order="F"), np.zeros((m, n), order="F")
+    oracle.matmul(OA(co), OA(a_h), OA(b_h), OA(ab))
+    assert np.all(np.abs(C.to_numpy() - co) <= 4 * k * 2.0 ** -53 * ab)
