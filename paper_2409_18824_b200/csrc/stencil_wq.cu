@@ -386,6 +386,20 @@ ftn_status_t launch_wq(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   p.w_in = 8;
   p.w_edge = w_edge > 0 ? w_edge : 8;
   p.W = (p.strips == 1 ? p.w_edge : 2 * p.w_edge + (p.strips - 2) * p.w_in) * p.nrows;
+  // Strip-aligned shares (FTN_WQ_ALIGN, default on): with u = (row weight of all strips) /
+  // w_in warps' worth per row, GW = a multiple of u gives every interior strip the same whole
+  // number of warps and the same row cuts, so the warps of neighbouring strips sweep the same
+  // rows at the same time and their shared overlap columns meet in L2.  The left-over warps
+  // (< u) get no work: for gw >= GW the range [gw W / GW, ...) starts at or past W, so every
+  // piece wq_piece returns for them is empty.
+  static const bool align = !getenv("FTN_WQ_ALIGN") || atoi(getenv("FTN_WQ_ALIGN")) != 0;
+  if (align && p.strips > 2 && p.w_edge % p.w_in == 0) {
+    const int64_t u = 2 * (p.w_edge / p.w_in) + (p.strips - 2);
+    if (p.GW >= u) {
+      p.GW = p.GW / u * u;
+      grid = (p.GW + C::NW - 1) / C::NW;
+    }
+  }
   static const bool pdl = !getenv("FTN_WF_PDL") || atoi(getenv("FTN_WF_PDL")) != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
