@@ -166,3 +166,81 @@ def test_distributed_protocol_matches_undivided(world):
     for lo, blk in out["matmul"]:
         got[:, lo:lo + blk.shape[1]] = blk
     np.testing.assert_array_equal(got, c)      # every element's fold is local to one rank
+
+
+def _solve_worker(rank, world, port, q, shape, max_sweeps, check, tol):
+    """ftn_jacobi_solve_dist's protocol with the oracle as the local compute: halo-1 slabs, one
+    sweep per exchange, and after every block of `check` sweeps the residual over each rank's
+    owned interior, all-gathered; the maximum decides the stop (R#25)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coeff = 0.25 if len(shape) == 2 else 1.0 / 6.0
+        full = synth.jacobi_init(shape, array_id=5)
+        nlast = shape[-1]
+        sl = D.slab(nlast - 2, world, rank)
+        g0, nl = sl.lo, sl.owned + 2                  # halo 1: local plane 0 = global plane sl.lo
+        cur = np.asfortranarray(full[..., g0:g0 + nl].copy())
+        prev = cur.copy(order="F")
+        plane_sz = int(np.prod(shape[:-1]))
+        inner = (slice(1, -1),) * (len(shape) - 1)
+        done, res = 0, 0.0
+        while done < max_sweeps:
+            k = min(check, max_sweeps - done)
+            for _ in range(k):
+                reqs = []
+                lo_buf = torch.empty(plane_sz, dtype=torch.float64)
+                hi_buf = torch.empty(plane_sz, dtype=torch.float64)
+                if rank > 0:
+                    reqs.append(dist.isend(torch.from_numpy(cur[..., 1].ravel(order="F").copy()), rank - 1))
+                    reqs.append(dist.irecv(lo_buf, rank - 1))
+                if rank < world - 1:
+                    reqs.append(dist.isend(torch.from_numpy(cur[..., nl - 2].ravel(order="F").copy()), rank + 1))
+                    reqs.append(dist.irecv(hi_buf, rank + 1))
+                for r in reqs:
+                    r.wait()
+                if rank > 0:
+                    cur[..., 0] = lo_buf.numpy().reshape(shape[:-1], order="F")
+                if rank < world - 1:
+                    cur[..., nl - 1] = hi_buf.numpy().reshape(shape[:-1], order="F")
+                prev = cur.copy(order="F")
+                a, b = cur.copy(order="F"), cur.copy(order="F")
+                new = oracle.jacobi(oracle.FArray(a), oracle.FArray(b), 1, coeff)
+                cur = np.asfortranarray(b if new else a)
+            done += k
+            local = oracle.maxabsdiff(oracle.FArray(np.asfortranarray(cur[inner + (slice(1, nl - 1),)])),
+                                      oracle.FArray(np.asfortranarray(prev[inner + (slice(1, nl - 1),)])))
+            vals = [torch.empty(1, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(vals, torch.tensor([local], dtype=torch.float64))
+            res = max(v.item() for v in vals)
+            if res <= tol:
+                break
+        parts = [None] * world
+        dist.all_gather_object(parts, (g0 + 1, cur[..., 1:nl - 1].copy(order="F")))
+        if rank == 0:
+            q.put((done, res, parts))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("shape,check,tol", [((23, 31), 4, 1e-2), ((11, 9, 14), 3, -1.0)])
+def test_distributed_solve_protocol_matches_undivided(world, shape, check, tol):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, q, shape, 17, check, tol)) for r in range(world)]
+    for p in procs:
+        p.start()
+    done, res, parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    coeff = 0.25 if len(shape) == 2 else 1.0 / 6.0
+    full = synth.jacobi_init(shape, array_id=5)
+    a, b = full.copy(order="F"), full.copy(order="F")
+    d_o, r_o, n_o = oracle.jacobi_solve(oracle.FArray(a), oracle.FArray(b), 17, check, tol, coeff)
+    ref = b if n_o else a
+    assert (done, res) == (d_o, r_o)
+    for first, owned in parts:
+        np.testing.assert_array_equal(owned, ref[..., first:first + owned.shape[-1]])
