@@ -371,6 +371,200 @@ __global__ void __launch_bounds__(256) ta_h(const __grid_constant__ TAParams p, 
     }
 }
 
+// ---------------------------------------------------------------- ta_h with TMA (the default
+// when all seven 3-D inputs are TMA-able): a CTA walks KC consecutive k-planes of one 32 x 32
+// tile; the seven inputs of plane k+1 (36 x 36 boxes at (i0-2, j0-2), zero outside the array)
+// arrive by TMA into the other half of a double buffer while plane k is computed, so the
+// loads are in flight during the whole step instead of between barriers.
+constexpr int TB = TH_X + 4;                 // box edge (36)
+constexpr int TBOX = TB * TB * 8;            // bytes per field box
+constexpr int TNF = 7;                       // md, tsn, tmask, umask, vmask, pun, pvn
+constexpr int TKC = 16;                      // planes per CTA
+struct TAMaps {
+  CUtensorMap m[TNF];
+};
+struct TAHsmem {
+  double box[2][TNF][TB][TB];                // double-buffered input boxes
+  double zi[TH_Y + 1][TH_X + 1];
+  double wx[TH_Y][TH_X + 3];
+  double wy[TH_Y + 3][TH_X];
+  double sx[TH_Y][TH_X + 2];
+  double sy[TH_Y + 2][TH_X];
+  double f2[3][TH_Y + 1][TH_X + 1];          // ztfreez, rnfmsk, upsmsk at the zind region
+  uint64_t full[2];
+};
+
+__global__ void __launch_bounds__(256, 1) ta_h_tma(const __grid_constant__ TAMaps maps,
+                                                   const __grid_constant__ TAParams p,
+                                                   const __grid_constant__ TAFused q) {
+  extern __shared__ __align__(128) uint8_t ta_tma_raw[];
+  TAHsmem& S = *reinterpret_cast<TAHsmem*>((reinterpret_cast<uintptr_t>(ta_tma_raw) + 127) & ~uintptr_t(127));
+  constexpr int MX = TH_X / 32, RY = TH_Y / 8;
+  enum { MD = 0, TSN = 1, TM = 2, UM = 3, VM = 4, PU = 5, PV = 6 };
+  const int64_t ni = p.ni, nj = p.nj, nk = p.nk;
+  const int64_t i0 = (int64_t)blockIdx.x * TH_X, j0 = (int64_t)blockIdx.y * TH_Y;
+  const int64_t ka = (int64_t)blockIdx.z * TKC, kb = min(ka + TKC, nk);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  auto issue = [&](int64_t k, int st) {
+    dev::mbar_arrive_expect_tx(&S.full[st], TNF * TBOX);
+    for (int f = 0; f < TNF; ++f)
+      dev::tma_load_3d(&S.box[st][f][0][0], &maps.m[f], &S.full[st], (int32_t)(i0 - 2), (int32_t)(j0 - 2), (int32_t)k);
+  };
+  if (threadIdx.x == 0) {
+    dev::mbar_init(&S.full[0], 1);
+    dev::mbar_init(&S.full[1], 1);
+    dev::fence_barrier_init();
+    for (int f = 0; f < TNF; ++f) dev::prefetch_tma(&maps.m[f]);
+    issue(ka, 0);
+  }
+  // the 2-D fields of the zind region (constant over k)
+  for (int ly = ty; ly < TH_Y + 1; ly += 8) {
+    const int64_t j = j0 - 1 + ly;
+    for (int lx = tx; lx < TH_X + 1; lx += 32) {
+      const int64_t i = i0 - 1 + lx;
+      const bool in = i >= 0 && i < ni && j >= 0 && j < nj;
+      S.f2[0][ly][lx] = in ? p.ztfreez(i, j) : 0.0;
+      S.f2[1][ly][lx] = in ? p.rnfmsk(i, j) : 0.0;
+      S.f2[2][ly][lx] = in ? p.upsmsk(i, j) : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int64_t k = ka; k < kb; ++k) {
+    const int st = (int)((k - ka) & 1);
+    if (threadIdx.x == 0 && k + 1 < kb) issue(k + 1, st ^ 1);  // its buffer was released at the end of k-1
+    dev::mbar_wait(&S.full[st], (uint32_t)(((k - ka) >> 1) & 1));
+    double (*B)[TB][TB] = S.box[st];
+    const double rzk = *reinterpret_cast<const double*>(p.rz + k * p.rz_s);
+    // zind over i0-1 .. i0+31, j0-1 .. j0+31 (box offset +1); the tile's own points to global
+    for (int ly = ty; ly < TH_Y + 1; ly += 8) {
+      const int64_t j = j0 - 1 + ly;
+      for (int lx = tx; lx < TH_X + 1; lx += 32) {
+        const int64_t i = i0 - 1 + lx;
+        const double zice = B[TSN][ly + 1][lx + 1] <= S.f2[0][ly][lx] + 0.1 ? 1.0 : 0.0;
+        double m = S.f2[1][ly][lx] * rzk;
+        m = fmax(fmax(m, S.f2[2][ly][lx]), zice);
+        const double z = 1.0 - m * B[TM][ly + 1][lx + 1];
+        S.zi[ly][lx] = z;
+        if (lx >= 1 && ly >= 1 && i < ni && j < nj) p.zind(i, j, k) = z;
+      }
+    }
+    if (k == nk - 1) {  // top plane: zind only, md6 = md
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int m = 0; m < MX; ++m) {
+          const int ly = ty + 8 * r, c = tx + 32 * m;
+          const int64_t i = i0 + c, j = j0 + ly;
+          if (i < ni && j < nj) q.md6(i, j, k) = B[MD][ly + 2][c + 2];
+        }
+      __syncthreads();
+      continue;
+    }
+    // step 2 (and the carried-over zwx of the last column, R#28)
+    for (int ly = ty; ly < TH_Y; ly += 8) {
+      const int64_t j = j0 + ly;
+      for (int lx = tx; lx < TH_X + 3; lx += 32) {
+        const int64_t s2 = i0 - 2 + lx;
+        double v = 0.0;
+        if (j < nj - 1 && s2 >= 0 && s2 < ni - 1) v = B[UM][ly + 2][lx] * (B[MD][ly + 2][lx + 1] - B[MD][ly + 2][lx]);
+        else if (j < nj && s2 == ni - 1) v = q.side[j + nj * k];
+        S.wx[ly][lx] = v;
+      }
+    }
+    for (int ly = ty; ly < TH_Y + 3; ly += 8) {
+      const int64_t t = j0 - 2 + ly;
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int c = tx + 32 * m;
+        const int64_t i = i0 + c;
+        double v = 0.0;
+        if (i < ni - 1 && t >= 0 && t < nj - 1) v = B[VM][ly][c + 2] * (B[MD][ly + 1][c + 2] - B[MD][ly][c + 2]);
+        S.wy[ly][c] = v;
+      }
+    }
+    __syncthreads();
+    // steps 3-4
+    for (int ly = ty; ly < TH_Y; ly += 8)
+      for (int lx = tx; lx < TH_X + 2; lx += 32) S.sx[ly][lx] = ta_limit(S.wx[ly][lx + 1], S.wx[ly][lx]);
+    for (int ly = ty; ly < TH_Y + 2; ly += 8)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int c = tx + 32 * m;
+        S.sy[ly][c] = ta_limit(S.wy[ly + 1][c], S.wy[ly][c]);
+      }
+    __syncthreads();
+    // step 5
+    auto xflux = [&](int ly, int lx) {  // f = i0-1+lx, row j0+ly
+      const int64_t f = i0 - 1 + lx, j = j0 + ly;
+      if (f >= 1 && f <= ni - 2 && j >= 1 && j <= nj - 2) {
+        const double zi = S.zi[ly + 1][lx], u = B[PU][ly + 2][lx + 1];
+        const double z0u = fsign(0.5, u);
+        const double zalpha = 0.5 - z0u;
+        const double zu = z0u - (0.5 * u) * 1.0;
+        const double zzwx = B[MD][ly + 2][lx + 2] + zi * (zu * S.sx[ly][lx + 1]);
+        const double zzwy = B[MD][ly + 2][lx + 1] + zi * (zu * S.sx[ly][lx]);
+        return u * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+      }
+      return f == 0 ? S.wx[ly][lx + 1] : 0.0;
+    };
+    double fx[RY][MX][2], fy[RY + 1][MX];
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int ly = ty + 8 * r, c = tx + 32 * m;
+        fx[r][m][0] = xflux(ly, c);
+        fx[r][m][1] = xflux(ly, c + 1);
+      }
+#pragma unroll
+    for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int ly = ty + 8 * r, c = tx + 32 * m;
+        fy[r][m] = 0.0;
+        if (ly >= TH_Y + 1) continue;
+        const int64_t i = i0 + c, g = j0 - 1 + ly;
+        if (g >= 1 && g <= nj - 2 && i >= 1 && i <= ni - 2) {
+          const double zi = S.zi[ly][c + 1], w = B[PV][ly + 1][c + 2];
+          const double z0v = fsign(0.5, w);
+          const double zalpha = 0.5 - z0v;
+          const double zv = z0v - (0.5 * w) * 1.0;
+          const double zzwx = B[MD][ly + 2][c + 2] + zi * (zv * S.sy[ly + 1][c]);
+          const double zzwy = B[MD][ly + 1][c + 2] + zi * (zv * S.sy[ly][c]);
+          fy[r][m] = w * (zalpha * zzwx + (1.0 - zalpha) * zzwy);
+        } else if (g == 0) {
+          fy[r][m] = S.wy[ly + 1][c];
+        }
+      }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int ly = ty + 8 * r, c = tx + 32 * m;
+        if (ly < TH_Y + 1) S.wy[ly][c] = fy[r][m];
+      }
+    __syncthreads();
+    // step 6
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int ly = ty + 8 * r, c = tx + 32 * m;
+        const int64_t i = i0 + c, j = j0 + ly;
+        if (i >= ni || j >= nj) continue;
+        double v = B[MD][ly + 2][c + 2];
+        if (i >= 1 && i <= ni - 2 && j >= 1 && j <= nj - 2) {
+          const double ztra = -(1.0 * (((fx[r][m][1] - fx[r][m][0]) + S.wy[ly + 1][c]) - S.wy[ly][c]));
+          v = v + ztra;
+        }
+        q.md6(i, j, k) = v;
+      }
+    __syncthreads();  // the boxes of plane k are free for plane k+2 (and S.zi / wx / ... for k+1)
+    if (threadIdx.x == 0) dev::fence_proxy_async();
+  }
+}
+
 __global__ void __launch_bounds__(256) ta_v(const __grid_constant__ TAParams p, const __grid_constant__ TAFused q) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x, j = blockIdx.y;
   const int64_t ni = p.ni, nj = p.nj, nk = p.nk;
@@ -545,8 +739,33 @@ ftn_status_t ftn_tra_adv(const ftn_desc_t* md, const ftn_desc_t* tsn, const ftn_
     q.side = reinterpret_cast<double*>(p.zwy.b);          // workspace array 2 (jpj x jpk used)
     const dim3 gh((unsigned)((ni + TH_X - 1) / TH_X), (unsigned)((nj + TH_Y - 1) / TH_Y), (unsigned)nk);
     const dim3 gv((unsigned)((ni + 255) / 256), (unsigned)nj);
+    // TMA path: every 3-D input TMA-able (unit stride in ji, 16-byte aligned base and strides)
+    const ftn_desc_t* tf[TNF] = {md, tsn, tmask, umask, vmask, pun, pvn};
+    bool tma = getenv("FTN_TA_TMA") == nullptr || atoi(getenv("FTN_TA_TMA")) != 0;
+    for (int f = 0; f < TNF && tma; ++f)
+      tma = tf[f]->dim[0].sm == 8 && ((uintptr_t)tf[f]->base_addr % 16) == 0 && tf[f]->dim[1].sm > 0 &&
+            tf[f]->dim[2].sm > 0 && (tf[f]->dim[1].sm % 16) == 0 && (tf[f]->dim[2].sm % 16) == 0;
+    TAMaps maps;
+    if (tma) {
+      for (int f = 0; f < TNF; ++f) {
+        uint64_t dims[3] = {(uint64_t)ni, (uint64_t)nj, (uint64_t)nk};
+        uint64_t strides[2] = {(uint64_t)tf[f]->dim[1].sm, (uint64_t)tf[f]->dim[2].sm};
+        uint32_t box[3] = {TB, TB, 1};
+        FTN_CHECK(encode_tma(&maps.m[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, tf[f]->base_addr, dims, strides, box,
+                             CU_TENSOR_MAP_SWIZZLE_NONE));
+      }
+      static std::atomic<bool> attr2[64] = {};
+      if (!attr2[dev & 63]) {
+        FTN_CUDA(cudaFuncSetAttribute(ta_h_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TAHsmem) + 128));
+        attr2[dev & 63] = true;
+      }
+    }
+    const dim3 ght((unsigned)((ni + TH_X - 1) / TH_X), (unsigned)((nj + TH_Y - 1) / TH_Y), (unsigned)((nk + TKC - 1) / TKC));
     for (int64_t it = 0; it < iters; ++it) {
-      ta_h<<<gh, 256, sizeof(TASmem), s>>>(p, q);
+      if (tma)
+        ta_h_tma<<<ght, 256, sizeof(TAHsmem) + 128, s>>>(maps, p, q);
+      else
+        ta_h<<<gh, 256, sizeof(TASmem), s>>>(p, q);
       FTN_CHECK(after_launch("tra_adv_h"));
       ta_v<<<gv, 256, 0, s>>>(p, q);
       FTN_CHECK(after_launch("tra_adv_v"));
