@@ -622,6 +622,9 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             gbs = 72 * cells * iters * ns / t / 1e9
             rows["f4_tra_adv_1024x512x512_x20"] = {
                 "value": gcs, "unit": "Gcell-iterations/s", "ms_per_step": t / ns * 1e3, "achieved_gbs": gbs,
+                "note": ("one GPU" if N == 1 else
+                         "N independent jj-slabs without halo exchange: aggregate throughput of replicas, "
+                         "not a distributed tra-adv (its fields change every iteration)"),
                 "roofline": {"bound": "hbm", "algorithmic_bytes_per_cell_iteration": 72,
                              "implementation_bytes_per_cell_iteration": 115, "frac": gbs / N / hbm_peak,
                              "frac_of_moved_bytes": 115 / 72 * gbs / N / hbm_peak}}
