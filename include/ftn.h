@@ -110,6 +110,14 @@ ftn_status_t ftn_ubound(const ftn_desc_t* x, int32_t dim, int64_t* out);
 ftn_status_t ftn_size(const ftn_desc_t* x, int32_t dim, int64_t* out);
 ftn_status_t ftn_shape(const ftn_desc_t* x, int64_t* out /* [rank] */);
 
+/* May a and b share a byte of memory?  The alias test behind R#5's temporaries.
+ * *out = 0 only when they provably do not: empty, disjoint byte ranges, or
+ * element addresses that fall in disjoint residue classes modulo the gcd of all
+ * strides (e.g. a(1::2,:) and a(2::2,:) of an array with an even leading
+ * extent); otherwise 1 (conservative: never 0 for sections that share a byte).
+ * Host-only. */
+ftn_status_t ftn_desc_may_overlap(const ftn_desc_t* a, const ftn_desc_t* b, int32_t* out);
+
 /* ---------------------------------------------------------------- a3
  * Element-wise array expressions.  Fortran assignment semantics: the whole
  * right-hand side is evaluated before the left-hand side is defined (R#5);

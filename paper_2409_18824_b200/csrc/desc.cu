@@ -131,13 +131,37 @@ void desc_byte_range(const ftn_desc_t* d, uintptr_t* lo, uintptr_t* hi) {
   *hi = (uintptr_t)d->base_addr + h + d->elem_len;
 }
 
+static uint64_t gcd_u64(uint64_t x, uint64_t y) {
+  while (y) {
+    const uint64_t t = x % y;
+    x = y;
+    y = t;
+  }
+  return x;
+}
+
+// Conservative alias test (R#5): false only if a and b provably share no byte.  Beyond the
+// bounding intervals: every element of a starts at base_a + (a multiple of g), every element
+// of b at base_b + (a multiple of g), g = gcd of all strides of both with extent > 1; with
+// elem_len <= g the elements occupy the residue intervals [ra, ra + len_a) and
+// [rb, rb + len_b) modulo g, and disjoint residue intervals mean disjoint memory.
 bool desc_overlap(const ftn_desc_t* a, const ftn_desc_t* b) {
   if (desc_size(a) == 0 || desc_size(b) == 0) return false;
   uintptr_t al, ah, bl, bh;
   desc_byte_range(a, &al, &ah);
   desc_byte_range(b, &bl, &bh);
-  return al < bh && bl < ah;
+  if (!(al < bh && bl < ah)) return false;
+  uint64_t g = 0;
+  for (const ftn_desc_t* d : {a, b})
+    for (int k = 0; k < d->rank; ++k)
+      if (d->dim[k].extent > 1) g = gcd_u64(g, (uint64_t)(d->dim[k].sm < 0 ? -d->dim[k].sm : d->dim[k].sm));
+  const uint64_t la = (uint64_t)a->elem_len, lb = (uint64_t)b->elem_len;
+  if (g == 0 || la > g || lb > g) return true;  // a single element each, or elements wider than g
+  const uint64_t ra = (uint64_t)(uintptr_t)a->base_addr % g, rb = (uint64_t)(uintptr_t)b->base_addr % g;
+  const uint64_t d = (rb + g - ra) % g;  // b's residue interval starts d bytes after a's
+  return d < la || d + lb > g;           // [0, la) and [d, d + lb) intersect modulo g
 }
+
 
 bool desc_identical(const ftn_desc_t* a, const ftn_desc_t* b) {
   if (a->base_addr != b->base_addr || a->rank != b->rank || a->elem_len != b->elem_len) return false;
@@ -276,6 +300,14 @@ ftn_status_t encode_tma(CUtensorMap* map, CUtensorMapDataType dt, int rank, void
 using namespace ftn;
 
 extern "C" {
+
+ftn_status_t ftn_desc_may_overlap(const ftn_desc_t* a, const ftn_desc_t* b, int32_t* out) {
+  FTN_CHECK(ftn::check_desc(a, "ftn_desc_may_overlap", 0, FTN_MAX_RANK));
+  FTN_CHECK(ftn::check_desc(b, "ftn_desc_may_overlap", 0, FTN_MAX_RANK));
+  if (!out) return ftn::fail(FTN_ERR_NULL, "ftn_desc_may_overlap: out NULL");
+  *out = ftn::desc_overlap(a, b) ? 1 : 0;
+  return FTN_OK;
+}
 
 ftn_status_t ftn_desc_contiguous(ftn_desc_t* out, void* base, int32_t type, int32_t rank,
                                  const int64_t* lower_bounds, const int64_t* extents) {

@@ -115,3 +115,49 @@ def test_jacobi_launch_plan(ftn):
     assert ftn.jacobi_plan(100, 8) == [8] * 2 + [7] * 12   # 14 launches, none short
     assert ftn.jacobi_plan(100, 5) == [5] * 20          # no short launch
     assert ftn.jacobi_plan(100, 2) == [2] * 50          # C5's plan
+
+
+def _bytes(d):
+    """Brute force: the set of byte addresses a descriptor's elements occupy."""
+    import itertools
+    out = set()
+    exts = [d.dim[k].extent for k in range(d.rank)]
+    for idx in itertools.product(*[range(e) for e in exts]):
+        a = d.base_addr + sum(i * d.dim[k].sm for k, i in enumerate(idx))
+        out.update(range(a, a + d.elem_len))
+    return out
+
+
+def test_may_overlap_is_sound_and_sees_interleaved_sections(ftn):
+    """ftn_desc_may_overlap (R#5's alias test) against brute-force byte sets: never 0 when two
+    sections share a byte; 0 for the interleaved disjoint pairs a(1::2,:) / a(2::2,:) of an
+    array with an even leading extent, and for disjoint byte ranges."""
+    rng = np.random.default_rng(5)
+    out = ctypes.c_int32()
+    for type_, lead in ((4, 6), (4, 5), (3, 8)):
+        par = _desc(ftn, [1, 1], [lead, 5], type_=type_)
+        secs = []
+        for _ in range(60):
+            lo = [int(rng.integers(1, lead + 1)), int(rng.integers(1, 6))]
+            hi = [int(rng.integers(lo[0], lead + 1)), int(rng.integers(lo[1], 6))]
+            st = [int(rng.choice([1, 2, 3])), int(rng.choice([1, 2]))]
+            rc, s = _section(ftn, par, list(zip(lo, hi, st)))
+            assert rc == 0
+            secs.append((s, _bytes(s)))
+        for a, ba in secs:
+            for b, bb in secs[:20]:
+                assert ftn.lib.ftn_desc_may_overlap(ctypes.byref(a), ctypes.byref(b), ctypes.byref(out)) == 0
+                if ba & bb:
+                    assert out.value == 1
+    par = _desc(ftn, [1, 1], [8, 4], type_=4)
+    rc, odd = _section(ftn, par, [(1, 8, 2), (1, 4, 1)])
+    rc, even = _section(ftn, par, [(2, 8, 2), (1, 4, 1)])
+    assert ftn.lib.ftn_desc_may_overlap(ctypes.byref(odd), ctypes.byref(even), ctypes.byref(out)) == 0
+    assert out.value == 0 and not (_bytes(odd) & _bytes(even))
+    assert ftn.lib.ftn_desc_may_overlap(ctypes.byref(odd), ctypes.byref(odd), ctypes.byref(out)) == 0
+    assert out.value == 1
+    par7 = _desc(ftn, [1, 1], [7, 4], type_=4)   # odd leading extent: the residue test cannot tell
+    rc, odd7 = _section(ftn, par7, [(1, 7, 2), (1, 4, 1)])
+    rc, even7 = _section(ftn, par7, [(2, 7, 2), (1, 4, 1)])
+    assert ftn.lib.ftn_desc_may_overlap(ctypes.byref(odd7), ctypes.byref(even7), ctypes.byref(out)) == 0
+    assert out.value == 1

@@ -180,3 +180,24 @@ def test_errors_launch_nothing(ftn):
     with pytest.raises(ftn.FtnError) as e:
         ftn.assign(a, ftn.FArray.empty((4, 5), dtype=torch.float32))
     assert e.value.name == "FTN_ERR_TYPE"
+
+
+def test_interleaved_disjoint_sections_need_no_temporary(ftn):
+    """a(2::2,:) = a(1::2,:)*2 + 1 (even leading extent): the sections interleave but share no
+    element, so the alias test (ftn_desc_may_overlap) lets the kernel write in place -- one
+    launch, no temporary -- and the result equals the oracle's.  With an odd leading extent the
+    test cannot prove it and the temporary path runs; the result is the same either way."""
+    for lead, launches in ((64, 1), (63, None)):
+        a = synth.farray((lead, 9), mode=synth.U11, array_id=11)
+        A, Ao = _pair(ftn, a)
+        hi = lead - (lead % 2 == 1)
+        dst, src = A.section((2, hi, 2), (1, 9)), A.section((1, hi - 1, 2), (1, 9))
+        torch.cuda.synchronize()
+        n0 = ftn.launch_count()
+        ftn.muladd(dst, src, 2.0, 1.0)
+        torch.cuda.synchronize()
+        if launches is not None:
+            assert ftn.launch_count() - n0 == launches
+        oracle.elemental(oracle.MULADD, Ao.section((2, hi, 2), (1, 9, 1)), Ao.section((1, hi - 1, 2), (1, 9, 1)),
+                         OA(np.array(2.0)), OA(np.array(1.0)))
+        np.testing.assert_array_equal(A.to_numpy(), Ao.arr)
