@@ -69,6 +69,22 @@ def test_transpose_int32_large(ftn):
     np.testing.assert_array_equal(t, (i + n1 * j).astype(np.int32))
 
 
+def test_transpose_real8_large_tma_path(ftn):
+    """real(8) 4100 x 3002 (the TMA path: 32 x 32 tiles, ragged in both dimensions, ~14 tiles
+    per persistent CTA) with the exact offset encoding i + n1 j; and a strided section of it
+    (the 16-byte-load path)."""
+    n1, n2 = 4100, 3002
+    a = ftn.FArray.empty((n1, n2))
+    ftn.gen_fill(a, 0, 0, ftn.GEN_LINEAR)
+    r = ftn.FArray.empty((n2, n1))
+    ftn.transpose(r, a)
+    j, i = np.meshgrid(np.arange(n2), np.arange(n1), indexing="ij")
+    np.testing.assert_array_equal(r.to_numpy(), (i + n1 * j).astype(np.float64))
+    r2 = ftn.FArray.empty((n2, n1 // 2))
+    ftn.transpose(r2, a.section((2, n1, 2), (1, n2)))
+    np.testing.assert_array_equal(r2.to_numpy(), (i[:, 1::2] + n1 * j[:, 1::2]).astype(np.float64))
+
+
 def _small(m, n, k):
     """ftn_matmul's small-product rule (matmul.cu small_matmul): the sequential-fold kernel."""
     return m * n * k <= (1 << 21) and k <= 4096
