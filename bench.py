@@ -153,8 +153,14 @@ def c5_checksum(torch, ftn, R, p_lo, p_hi, comm):
 
 
 def jacobi_faces(ftn, U, n1, n2):
-    """synth.jacobi_init recipe on the device: interior U[0,1), j=1 face 1.0, other faces 0."""
-    ftn.gen_fill(U, SEED, 0, ftn.GEN_U01)
+    """synth.jacobi_init recipe on the device: interior U[0,1), j=1 face 1.0, other faces 0.
+    --mode intvalued: interior integers in [-8, 8]; --mode closed: the whole array is the
+    linear (discrete-harmonic) field u(i,j) = (i-1) + n1 (j-1), a fixed point of the sweep:
+    every step must return it bit for bit (checked after the timed region)."""
+    if MODE == "closed":
+        ftn.gen_fill(U, SEED, 0, ftn.GEN_LINEAR)
+        return
+    ftn.gen_fill(U, SEED, 0, ftn.GEN_INT8 if MODE == "intvalued" else ftn.GEN_U01)
     for tr in (((1, n1), (n2, n2)), ((1, 1), (1, n2)), ((n1, n1), (1, n2))):
         ftn.fill(U.section(*tr), 0.0)
     ftn.fill(U.section((1, n1), (1, 1)), 1.0)
@@ -162,7 +168,7 @@ def jacobi_faces(ftn, U, n1, n2):
 
 # ----------------------------------------------------------------------------------- headline
 def bench_jacobi2d(torch, ftn, args, ctx):
-    n, sweeps = 8192, 100
+    n, sweeps = 8192, SWEEPS
     N, rank = ctx["world"], ctx["rank"]
     if N == 1 and not ctx.get("force_dist"):
         U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
@@ -177,13 +183,16 @@ def bench_jacobi2d(torch, ftn, args, ctx):
         halo = max(1, ftn.jacobi_fusion())
         nl = n + 2 * halo
         U, W = ftn.FArray.empty((n, nl)), ftn.FArray.empty((n, nl))
-        ftn.gen_fill(U, SEED, 1 + rank, ftn.GEN_U01)
-        ftn.fill(U.section((1, 1), (1, nl)), 0.0)
-        ftn.fill(U.section((n, n), (1, nl)), 0.0)
-        if rank == 0:
-            ftn.fill(U.section((1, n), (halo, halo)), 1.0)            # global boundary plane j = 1
-        if rank == N - 1:
-            ftn.fill(U.section((1, n), (nl - halo + 1, nl - halo + 1)), 0.0)   # global plane j = N
+        if MODE == "closed":   # the linear field (i-1) + n (global column + halo - 1): harmonic
+            ftn.gen_fill(U, SEED, 0, ftn.GEN_LINEAR, t0=n * n * rank)
+        else:
+            ftn.gen_fill(U, SEED, 1 + rank, ftn.GEN_INT8 if MODE == "intvalued" else ftn.GEN_U01)
+            ftn.fill(U.section((1, 1), (1, nl)), 0.0)
+            ftn.fill(U.section((n, n), (1, nl)), 0.0)
+            if rank == 0:
+                ftn.fill(U.section((1, n), (halo, halo)), 1.0)            # global boundary plane j = 1
+            if rank == N - 1:
+                ftn.fill(U.section((1, n), (nl - halo + 1, nl - halo + 1)), 0.0)   # global plane j = N
         ftn.assign(W, U)
         comm = ctx["comm"]
         step = lambda: comm.jacobi(U, W, sweeps, halo=halo)  # noqa: E731
@@ -203,6 +212,24 @@ def bench_jacobi2d(torch, ftn, args, ctx):
            "achieved_gbs": achieved, "per_launch_bytes": per_launch_bytes,
            "plan": {"max_sweeps_per_launch": halo_T, "launches_per_step": len(plan),
                     "sweeps_per_launch": {str(k): plan.count(k) for k in sorted(set(plan))}}}
+    if MODE == "closed":
+        # the harmonic field is a fixed point: after every step the result array must hold the
+        # initial field bit for bit (MAXVAL(ABS(result - initial)) over the owned planes = 0)
+        R = U if sweeps % 2 == 0 else W
+        G = ftn.FArray.empty(tuple(U.shape))
+        if N == 1 and not ctx.get("force_dist"):
+            ftn.gen_fill(G, SEED, 0, ftn.GEN_LINEAR)
+            diff = float(ftn.maxval_absdiff(R, G).item())
+        else:
+            ftn.gen_fill(G, SEED, 0, ftn.GEN_LINEAR, t0=n * n * rank)
+            own = ((1, n), (halo + 1, U.shape[1] - halo))
+            d = ftn.maxval_absdiff(R.section(*own), G.section(*own)).reshape(1)
+            if ctx["dist"] is not None:
+                ctx["dist"].all_reduce(d, op=ctx["dist"].ReduceOp.MAX)
+            diff = float(d.item())
+        res["check"] = {"mode": "closed", "field": "u(i,j) = (i-1) + 8192 (j-1) (discrete-harmonic)",
+                        "max_abs_diff_vs_initial": diff, "bit_exact": diff == 0.0}
+        del G, R
     # ---- e2e: through the C ABI from pinned host buffers (H2D of u, D2H of the result inside);
     # at N > 1 every rank moves its own slab, timed as the max over ranks
     shape = tuple(U.shape)
@@ -333,7 +360,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         for q, x in enumerate(b48):
             ftn.gen_fill(x, SEED, 2 + q, ftn.GEN_U11)
         out = torch.empty((), dtype=torch.float64, device="cuda")
-        ops = {"muladd_r=s*c+d": lambda: ftn.muladd(r, s, c, e),
+        ops = {"muladd_r=s*c+d": lambda: ftn.muladd(r, s, c, e, contract=CONTRACT),
                "sum_s": lambda: ftn.sum(s, out),
                "maxval_s": lambda: ftn.maxval(s, out),
                "minval_s": lambda: ftn.minval(s, out),
@@ -421,7 +448,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             ftn.gen_fill(a, SEED, 10 + k, ftn.GEN_U01)
         b, c, d, r = arrs
         n_el = 1024 * 1024 * nk
-        gbs_row("c4_muladd_r=b*c+d", 32 * n_el, lambda: ftn.muladd(r, b, c, d))
+        gbs_row("c4_muladd_r=b*c+d", 32 * n_el, lambda: ftn.muladd(r, b, c, d, contract=CONTRACT))
         gbs_row("hbm_copy_r=b", 16 * n_el, lambda: ftn.assign(r, b))      # the in-run copy ceiling
         out = torch.empty((), dtype=torch.float64, device="cuda")
         if not distmode:
@@ -451,7 +478,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         for k, p in enumerate(parents):
             ftn.gen_fill(p, SEED, 20 + k, ftn.GEN_U01)
         secs = [p.section((1, 1024), (1, 1024), (1, 2 * nk, 2)) for p in parents]
-        gbs_row("c4_section_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2]))
+        gbs_row("c4_section_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2], contract=CONTRACT))
         if N == 1:
             gbs_row("c4_section_sum", 8 * n_el, lambda: ftn.sum(secs[0], out))
         del parents, secs
@@ -463,7 +490,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
             for k, p in enumerate(parents):
                 ftn.gen_fill(p, SEED, 30 + k, ftn.GEN_U01)
             secs = [p.section((0, 2047, 2), (1, 1024), (1, nk)) for p in parents]
-            gbs_row("c4_dim1_strided_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2]))
+            gbs_row("c4_dim1_strided_muladd", 32 * n_el, lambda: ftn.muladd(secs[3], secs[0], secs[1], secs[2], contract=CONTRACT))
             gbs_row("c4_dim1_strided_sum", 8 * n_el, lambda: ftn.sum(secs[0], out))
             for nm in ("c4_dim1_strided_muladd", "c4_dim1_strided_sum"):
                 rows[nm]["roofline"]["note"] = "sector-limited: 2 of every 4 elements of a 32-byte sector are used"
@@ -704,7 +731,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         n_el = 1024 * 1024 * (1024 // P8)
         out = torch.empty((), dtype=torch.float64, device="cuda")
         for name, nb, fn, full in (("c4_sum_share_1024x1024x128", 8 * n_el, lambda: ftn.sum(b, out), "c4_sum"),
-                                   ("c4_muladd_share_1024x1024x128", 32 * n_el, lambda: ftn.muladd(r, b, c, d),
+                                   ("c4_muladd_share_1024x1024x128", 32 * n_el, lambda: ftn.muladd(r, b, c, d, contract=CONTRACT),
                                     "c4_muladd_r=b*c+d")):
             t = timed(torch, fn, steps, warm, None, None)
             g = nb * steps / t / 1e9
@@ -770,9 +797,14 @@ def run_reference(args):
     import oracle
     import synth
     N = max(1, args.gpus)
-    n, sweeps = 8192, 100
+    n, sweeps = 8192, SWEEPS
     n2 = n if N == 1 else n * N + 2
-    u = synth.jacobi_init((n, n2))
+    if MODE == "closed":
+        u = np.asfortranarray(np.add.outer(np.arange(n, dtype=np.float64), n * np.arange(n2, dtype=np.float64)))
+    else:
+        u = synth.jacobi_init((n, n2), seed=SEED)
+        if MODE == "intvalued":
+            u[1:-1, 1:-1] = synth.farray((n - 2, n2 - 2), seed=SEED, mode=synth.INT8, array_id=0)
     w = u.copy(order="F")
     U, Wd = oracle.FArray(u), oracle.FArray(w)
     for _ in range(args.warmup):
@@ -785,11 +817,11 @@ def run_reference(args):
     glups = interior * sweeps * args.steps / t / 1e9
     cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     cpu = {"value": glups, "unit": "GLUPS", "cores": cores, "kind": "oracle",
-           "sample": f"the whole workload: {args.steps} steps of 100 sweeps of the {n}x{n2} grid, OpenMP over rows"}
-    line = {"impl": "reference", "metric": METRIC, "value": glups, "unit": "GLUPS", "n_gpus": args.gpus,
+           "sample": f"the whole workload: {args.steps} steps of {sweeps} sweeps of the {n}x{n2} grid, OpenMP over rows"}
+    line = {"impl": "reference", "metric": metric(), "value": glups, "unit": "GLUPS", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(CONFIG, parallelism=f"slab{N}" if N > 1 else "1 GPU",
+            "config": dict(config(), parallelism=f"slab{N}" if N > 1 else "1 GPU",
                            global_grid=f"{n}x{n2}"),
             "cpu_baseline": cpu,
             "e2e": {"value": glups, "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -798,9 +830,21 @@ def run_reference(args):
     return 0
 
 
-METRIC = "Jacobi GLUPS (2-D 5-point, real(8) 8192^2, 100 sweeps per step)"
-CONFIG = {"workload": "BASELINE configs[1]: 2-D 5-point Jacobi stencil, real(8) 8192x8192, 100 sweeps",
-          "l2": "working set 2 x 512 MiB > 126 MB L2 (no flush needed)", "seed": SEED}
+SWEEPS = 100          # sweeps per step of the C2 headline (BASELINE: 100; --sweeps)
+MODE = "random"       # C2 input (--mode): random U[0,1) interior | closed (a harmonic field) | intvalued
+CONTRACT = False      # MULADD rows as one fused multiply-add (--contract, R#6)
+
+
+def metric():
+    return f"Jacobi GLUPS (2-D 5-point, real(8) 8192^2, {SWEEPS} sweeps per step)"
+
+
+def config():
+    c = {"workload": f"BASELINE configs[1]: 2-D 5-point Jacobi stencil, real(8) 8192x8192, {SWEEPS} sweeps",
+         "l2": "working set 2 x 512 MiB > 126 MB L2 (no flush needed)", "seed": SEED}
+    if MODE != "random":
+        c["input_mode"] = MODE
+    return c
 
 
 HBM_SPEC_GBS = 8000.0   # B200 datasheet HBM3e bandwidth (BASELINE's ~8 TB/s)
@@ -835,6 +879,7 @@ def traffic_from_profiles():
 
 
 def main():
+    global SEED, SWEEPS, MODE, CONTRACT
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -844,7 +889,33 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")
+    # SURVEY §5 bench CLI
+    ap.add_argument("--config", default=None,
+                    help="which SURVEY §8 configs run beside the C2 headline: a comma list of C1, C3, C4, C5, P "
+                         "(the paper's shapes), F4, SHARES, or ALL / NONE (overrides --rows)")
+    ap.add_argument("--seed", type=int, default=SEED, help="generator seed of every synthetic input (18824)")
+    ap.add_argument("--sweeps", type=int, default=SWEEPS, help="sweeps per step of the C2 headline (100)")
+    ap.add_argument("--mode", choices=["random", "closed", "intvalued"], default=MODE,
+                    help="C2 input: U[0,1) interior (BASELINE), the harmonic field (i-1) + 8192 (j-1) (a fixed "
+                         "point, checked bit for bit after the timed region), or integers in [-8, 8]")
+    ap.add_argument("--contract", action="store_true",
+                    help="the MULADD rows as one fused multiply-add per element (R#6)")
     args = ap.parse_args()
+    SEED, SWEEPS, MODE, CONTRACT = args.seed, args.sweeps, args.mode, args.contract
+    if SWEEPS < 1:
+        ap.error("--sweeps must be >= 1")
+    if args.config is not None:
+        groups = {"C1": "c1", "C3": "c3", "C4": "c4", "C5": "c5", "P": "paper", "F4": "f4", "SHARES": "shares"}
+        sel = [c.strip().upper() for c in args.config.split(",") if c.strip()]
+        if sel in (["ALL"],):
+            args.rows = ",".join(groups.values())
+        elif sel in (["NONE"], ["C2"]):
+            args.rows = "none"
+        else:
+            bad = [c for c in sel if c not in groups and c != "C2"]
+            if bad:
+                ap.error(f"--config: unknown {bad}; choose from C1..C5, P, F4, SHARES, ALL, NONE")
+            args.rows = ",".join(groups[c] for c in sel if c in groups) or "none"
     args.rows = [] if args.rows == "none" else args.rows.split(",")
     if args.impl == "reference":
         return run_reference(args)
@@ -887,14 +958,15 @@ def main():
         # achieved_gbs is per GPU already (one rank's slab bytes per launch / max-over-ranks time)
         frac = head["achieved_gbs"] / hbm_peak
         line = {
-            "metric": METRIC, "value": head["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
+            "metric": metric(), "value": head["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "ms_per_step_min": head["ms_step_min"], "ms_per_step_median": head["ms_step_median"],
             "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(CONFIG, parallelism=f"slab{world}" if world > 1 else "1 GPU",
+            "config": dict(config(), parallelism=f"slab{world}" if world > 1 else "1 GPU",
                            global_grid=f"8192x{8192 * world + (2 if world > 1 else 0)}"),
             "e2e": head.get("e2e"),
+            **({"check": head["check"]} if "check" in head else {}),
             "gpu_launches": head["launches"],
             "roofline": {"bound": "hbm",
                          "kernel": fused_kernel_name(head["plan"]["sweeps_per_launch"]),
