@@ -633,7 +633,7 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
                                         "launches_per_step": nl3, "sweeps_per_launch_max": T3,
                                         "roofline": {"bound": "hbm", "achieved_gbs_per_gpu": gbs,
                                                      "frac": gbs / hbm_peak},
-                                        "checksum": checksum}
+                                        "checksum": dict(checksum or {}, sweeps_done=(1 + ns) * sweeps)}
 
     # f4: pw-advection, three fields (k, j, i) = 2048 x 1024 x 1024 (R#26/R#27); at N > 1
     # every rank owns 1024/N i-planes plus one halo plane per side (inputs do not change

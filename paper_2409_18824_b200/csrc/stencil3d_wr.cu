@@ -28,7 +28,9 @@
 // Work: tiles (i fastest) x planes laid end to end, the tiles touching the global i / j
 // boundary weighted by their select path's cost; CTA b of one persistent wave takes the
 // planes whose weighted start lies in [b W / G, (b+1) W / G) -- one or a few pieces (a tile's
-// plane range) per CTA, equal weighted work, no wave quantisation.
+// plane range) per CTA, equal weighted work, no wave quantisation.  Large grids instead deal
+// (tile, 512-plane band) cells round-robin (launch_wr): neighbouring tiles are then swept at
+// the same planes at the same time and share their box halos through L2.
 #include "ftn_internal.cuh"
 
 #include <algorithm>
@@ -74,6 +76,7 @@ struct W3Params {
   int32_t fix_lo, fix_hi;      // planes <= fix_lo and >= fix_hi keep their value at every level
   int64_t w_iedge, w_jedge, w_in, W;  // weighted flattened split (see the header comment)
   int64_t G;                   // CTAs
+  int64_t rr_band;             // > 0: (tile, k-band) cells dealt round-robin (experiment)
   double coeff;
 };
 
@@ -127,6 +130,16 @@ __device__ __forceinline__ int64_t w3_tile_of(const W3Params& p, int64_t x) {
 // Piece k of CTA b: tile t, output planes [ka, kb) (absolute); false: no piece k.
 __device__ __forceinline__ bool w3_piece(const W3Params& p, int64_t b, int64_t k, int64_t t0, int64_t t1,
                                          int64_t& t, int32_t& ka, int32_t& kb) {
+  if (p.rr_band > 0) {
+    const int64_t nt = (int64_t)p.tiles_i * p.tiles_j, nb = (p.nplanes + p.rr_band - 1) / p.rr_band;
+    const int64_t c = b + k * p.G;
+    if (c >= nt * nb) return false;
+    t = c % nt;
+    const int64_t band = c / nt, e = (band + 1) * p.rr_band;
+    ka = p.plane_lo + (int32_t)(band * p.rr_band);
+    kb = p.plane_lo + (int32_t)(e < p.nplanes ? e : p.nplanes);
+    return true;
+  }
   const int64_t A = b * p.W / p.G, B = (b + 1) * p.W / p.G;
   t = t0 + k;
   if (A >= B || t > t1) return false;
@@ -472,6 +485,23 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   int64_t grid = num_sms();
   const int64_t need = (TI * TJ * nk + 15) / 16;  // at least ~16 planes of a tile per CTA
   if (grid > need) grid = need < 1 ? 1 : need;
+  // Large grids: deal (tile, 512-plane band) cells round-robin instead (cell c to CTA c mod G).
+  // CTAs launched together then sweep neighbouring tiles at the same planes and share the box
+  // halos through L2: at 2048^3 the DRAM reads fall from 1.92x to ~1.4x the algorithmic bytes,
+  // and under the board's power cap that is +5.5 % (602-605 -> 635-637 GLUPS; bands of 384-768
+  // planes are equal, 1024 623).  The grid is made coprime to the tile-row length so a CTA's
+  // cells rotate through the tile columns (the edge tiles spread over all CTAs).  It needs >= 40
+  // cells per CTA for the statistical balance (512^3: 390 vs 495, 1024^3: 514 vs 595 GLUPS with
+  // 10 cells per CTA), so smaller grids keep the weighted split.  FTN_W3_RR = band (0: off).
+  static const int64_t rr_env = getenv("FTN_W3_RR") ? atoll(getenv("FTN_W3_RR")) : -1;
+  {
+    const int64_t band = rr_env >= 0 ? rr_env : 512;
+    int64_t g2 = grid;
+    while (g2 > 1 && std::__gcd<int64_t>(g2, p.tiles_i) != 1) --g2;
+    const int64_t cells = band > 0 ? TI * TJ * ((nk + band - 1) / band) : 0;
+    p.rr_band = band > 0 && (rr_env > 0 || cells >= 40 * g2) ? band : 0;
+    if (p.rr_band > 0) grid = g2;
+  }
   p.G = grid;
 #if FTN_W3_TRACE
   {
