@@ -487,7 +487,7 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   if (grid > need) grid = need < 1 ? 1 : need;
   // Large grids: deal (tile, 512-plane band) cells round-robin instead (cell c to CTA c mod G).
   // CTAs launched together then sweep neighbouring tiles at the same planes and share the box
-  // halos through L2: at 2048^3 the DRAM reads fall from 1.92x to ~1.4x the algorithmic bytes,
+  // halos through L2: at 2048^3 the DRAM reads fall from 1.92x to 1.34x the algorithmic bytes,
   // and under the board's power cap that is +5.5 % (602-605 -> 635-637 GLUPS; bands of 384-768
   // planes are equal, 1024 623).  The grid is made coprime to the tile-row length so a CTA's
   // cells rotate through the tile columns (the edge tiles spread over all CTAs).  It needs >= 40
