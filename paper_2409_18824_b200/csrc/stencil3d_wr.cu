@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <numeric>
 #include <type_traits>
 #include <vector>
 
@@ -497,7 +498,7 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   {
     const int64_t band = rr_env >= 0 ? rr_env : 512;
     int64_t g2 = grid;
-    while (g2 > 1 && std::__gcd<int64_t>(g2, p.tiles_i) != 1) --g2;
+    while (g2 > 1 && std::gcd(g2, (int64_t)p.tiles_i) != 1) --g2;
     const int64_t cells = band > 0 ? TI * TJ * ((nk + band - 1) / band) : 0;
     p.rr_band = band > 0 && (rr_env > 0 || cells >= 40 * g2) ? band : 0;
     if (p.rr_band > 0) grid = g2;
