@@ -29,13 +29,15 @@
 // boundary weighted by their select path's cost; CTA b of one persistent wave takes the
 // planes whose weighted start lies in [b W / G, (b+1) W / G) -- one or a few pieces (a tile's
 // plane range) per CTA, equal weighted work, no wave quantisation.  Large grids instead deal
-// (tile, 512-plane band) cells round-robin (launch_wr): neighbouring tiles are then swept at
-// the same planes at the same time and share their box halos through L2.
+// (tile, 512-plane band) cells in order -- taken from a ticket counter, or round-robin under
+// stream capture (launch_wr): neighbouring tiles are then swept at the same planes at the same
+// time and share their box halos through L2.
 #include "ftn_internal.cuh"
 
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <numeric>
 #include <type_traits>
 #include <vector>
@@ -65,7 +67,7 @@ struct W3Cfg {
   static constexpr int H = T + (T & 1);
   static constexpr int OX = W3_BX - 2 * H, OY = W3_BY - 2 * T;
   static constexpr int NHALO = T > 1 ? 2 * (T - 1) : 1;  // edge-row slots: level x step parity
-  static constexpr int SMEM = W3_NS * W3_PLANE + NHALO * W3_HALO + 128 + 8 * W3_NS;
+  static constexpr int SMEM = W3_NS * W3_PLANE + NHALO * W3_HALO + 128 + 8 * W3_NS + 32;  // + the cell queue
 };
 
 struct W3Params {
@@ -77,7 +79,8 @@ struct W3Params {
   int32_t fix_lo, fix_hi;      // planes <= fix_lo and >= fix_hi keep their value at every level
   int64_t w_iedge, w_jedge, w_in, W;  // weighted flattened split (see the header comment)
   int64_t G;                   // CTAs
-  int64_t rr_band;             // > 0: (tile, k-band) cells dealt round-robin (experiment)
+  int64_t rr_band;             // > 0: (tile, k-band) cells instead of the weighted split
+  unsigned long long* ticket;  // dynamic cells: [0] next cell, [1] CTAs done (zero at launch; reset by the last CTA)
   double coeff;
 };
 
@@ -128,19 +131,23 @@ __device__ __forceinline__ int64_t w3_tile_of(const W3Params& p, int64_t x) {
   return lo;
 }
 
-// Piece k of CTA b: tile t, output planes [ka, kb) (absolute); false: no piece k.
+// Cell c of the banded order (tile fastest, then 512-plane band): tile t, planes [ka, kb).
+__device__ __forceinline__ bool w3_cell(const W3Params& p, int64_t c, int64_t& t, int32_t& ka, int32_t& kb) {
+  const int64_t nt = (int64_t)p.tiles_i * p.tiles_j, nb = (p.nplanes + p.rr_band - 1) / p.rr_band;
+  if (c >= nt * nb) return false;
+  t = c % nt;
+  const int64_t band = c / nt, e = (band + 1) * p.rr_band;
+  ka = p.plane_lo + (int32_t)(band * p.rr_band);
+  kb = p.plane_lo + (int32_t)(e < p.nplanes ? e : p.nplanes);
+  return true;
+}
+
+// Piece k of CTA b: tile t, output planes [ka, kb) (absolute); false: no piece k.  Banded
+// cells: cell b + k G (static), or the k-th cell this CTA's TMA issuer took from the ticket
+// counter (dynamic; cellq holds the last four).
 __device__ __forceinline__ bool w3_piece(const W3Params& p, int64_t b, int64_t k, int64_t t0, int64_t t1,
-                                         int64_t& t, int32_t& ka, int32_t& kb) {
-  if (p.rr_band > 0) {
-    const int64_t nt = (int64_t)p.tiles_i * p.tiles_j, nb = (p.nplanes + p.rr_band - 1) / p.rr_band;
-    const int64_t c = b + k * p.G;
-    if (c >= nt * nb) return false;
-    t = c % nt;
-    const int64_t band = c / nt, e = (band + 1) * p.rr_band;
-    ka = p.plane_lo + (int32_t)(band * p.rr_band);
-    kb = p.plane_lo + (int32_t)(e < p.nplanes ? e : p.nplanes);
-    return true;
-  }
+                                         int64_t& t, int32_t& ka, int32_t& kb, const int64_t* cellq) {
+  if (p.rr_band > 0) return w3_cell(p, p.ticket ? cellq[k & 3] : b + k * p.G, t, ka, kb);
   const int64_t A = b * p.W / p.G, B = (b + 1) * p.W / p.G;
   t = t0 + k;
   if (A >= B || t > t1) return false;
@@ -161,10 +168,11 @@ struct W3Cursor {
   int64_t k, t;
   int32_t plane, pend, i0, j0;
   bool live;
-  __device__ __forceinline__ void find(const W3Params& p, int64_t b, int64_t t0, int64_t t1) {
+  __device__ __forceinline__ void find(const W3Params& p, int64_t b, int64_t t0, int64_t t1, int64_t* cellq) {
     int32_t ka, kb;
     for (;;) {
-      live = w3_piece(p, b, k, t0, t1, t, ka, kb);
+      if (p.ticket) cellq[k & 3] = (int64_t)atomicAdd(p.ticket, 1ull);  // take the next cell
+      live = w3_piece(p, b, k, t0, t1, t, ka, kb, cellq);
       if (!live || kb > ka) break;
       ++k;
     }
@@ -180,10 +188,10 @@ struct W3Cursor {
     dev::mbar_arrive_expect_tx(&full[s], W3_PLANE);
     dev::tma_load_3d(ring + s * W3_PLANE, map, &full[s], i0, j0, plane);
   }
-  __device__ __forceinline__ void advance(const W3Params& p, int64_t b, int64_t t0, int64_t t1) {
+  __device__ __forceinline__ void advance(const W3Params& p, int64_t b, int64_t t0, int64_t t1, int64_t* cellq) {
     if (live && ++plane == pend) {
       ++k;
-      find(p, b, t0, t1);
+      find(p, b, t0, t1, cellq);
     }
   }
 };
@@ -208,6 +216,7 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const uint32_t soff = (uint32_t)(smem - smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + W3_NS * W3_PLANE + C::NHALO * W3_HALO);
+  int64_t* cellq = reinterpret_cast<int64_t*>(full + W3_NS);  // dynamic cells taken by thread 0
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = blockIdx.x;
   // this CTA's tile range
@@ -219,10 +228,10 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
     dev::fence_barrier_init();
     dev::prefetch_tma(&map);
     cur.k = 0;
-    cur.find(p, b, t0, t1);
+    cur.find(p, b, t0, t1, cellq);
     for (uint32_t g = 0; g < W3_NS && cur.live; ++g) {
       cur.issue(&map, smem, full, g);
-      cur.advance(p, b, t0, t1);
+      cur.advance(p, b, t0, t1, cellq);
     }
   }
   __syncthreads();
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
   int64_t tr_edge = 0, tr_in = 0;
 #endif
-  for (int64_t pk = 0; w3_piece(p, b, pk, t0, t1, t, ka, kb); ++pk) {
+  for (int64_t pk = 0; w3_piece(p, b, pk, t0, t1, t, ka, kb, cellq); ++pk) {
     if (kb <= ka) continue;
 #if FTN_W3_TRACE
     if (w3_edge_tile(p, t)) tr_edge += kb - ka;
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
           if (tt == 0 && threadIdx.x == 0 && cur.live) {  // level-0 plane of this step consumed
             dev::fence_proxy_async();
             cur.issue(&map, smem, full, g + W3_NS);
-            cur.advance(p, b, t0, t1);
+            cur.advance(p, b, t0, t1, cellq);
           }
 #pragma unroll
           for (int r = 0; r < W3_R; ++r) {
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
         if (threadIdx.x == 0 && cur.live) {
           dev::fence_proxy_async();
           cur.issue(&map, smem, full, g + W3_NS);
-          cur.advance(p, b, t0, t1);
+          cur.advance(p, b, t0, t1, cellq);
         }
       }
       ++g;
@@ -390,6 +399,13 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
       else step(q, false);
     }
   }
+  if (p.ticket && threadIdx.x == 0) {  // the last CTA to finish leaves the ticket slot zeroed
+    __threadfence();
+    if (atomicAdd(p.ticket + 1, 1ull) == (unsigned long long)(p.G - 1)) {
+      p.ticket[0] = 0;
+      p.ticket[1] = 0;
+    }
+  }
 #if FTN_W3_TRACE
   if (threadIdx.x == 0 && w3_trace) {
     uint64_t tr1;
@@ -400,6 +416,23 @@ __global__ void __launch_bounds__(W3_THREADS, 1) jacobi3d_wr(const __grid_consta
     w3_trace[4 * b + 3] = tr_in;
   }
 #endif
+}
+
+// Ticket slots for the dynamic cell order: per device, 256 slots of {next cell, CTAs done},
+// zeroed once; a launch takes the next slot and its last CTA leaves it zeroed again (a slot
+// is reused only 256 launches later).
+unsigned long long* ticket_slot() {
+  static std::mutex mu;
+  static unsigned long long* slots[64] = {};
+  static unsigned next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!slots[dev & 63]) {
+    if (cudaMalloc(&slots[dev & 63], 256 * 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaMemset(slots[dev & 63], 0, 256 * 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  }
+  return slots[dev & 63] + 2 * (next[dev & 63]++ % 256);
 }
 
 template <int T>
@@ -494,14 +527,31 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
   // cells rotate through the tile columns (the edge tiles spread over all CTAs).  It needs >= 40
   // cells per CTA for the statistical balance (512^3: 390 vs 495, 1024^3: 514 vs 595 GLUPS with
   // 10 cells per CTA), so smaller grids keep the weighted split.  FTN_W3_RR = band (0: off).
+  // By default the cells are not dealt but taken, in order, from a per-launch ticket counter
+  // (FTN_W3_DYN=1): a CTA that finishes early takes the next cell, so no grid adjustment is
+  // needed and the load balances exactly (+2.7 % over the static deal at 2048^3).
   static const int64_t rr_env = getenv("FTN_W3_RR") ? atoll(getenv("FTN_W3_RR")) : -1;
+  static const int dyn_env = getenv("FTN_W3_DYN") ? atoi(getenv("FTN_W3_DYN")) : 1;
+  p.ticket = nullptr;
   {
     const int64_t band = rr_env >= 0 ? rr_env : 512;
     int64_t g2 = grid;
     while (g2 > 1 && std::gcd(g2, (int64_t)p.tiles_i) != 1) --g2;
     const int64_t cells = band > 0 ? TI * TJ * ((nk + band - 1) / band) : 0;
-    p.rr_band = band > 0 && (rr_env > 0 || cells >= 40 * g2) ? band : 0;
-    if (p.rr_band > 0) grid = g2;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    const bool large = band > 0 && (rr_env > 0 || cells >= 40 * g2);
+    if (large && dyn_env && cap == cudaStreamCaptureStatusNone) {
+      // dynamic cells: CTAs take (tile, band) cells from a ticket counter in launch order
+      // (2048^3: 649 vs 630-632 GLUPS for the static round-robin; no capture: a replayed graph
+      // would share the slot between replays)
+      p.rr_band = band;
+      p.ticket = ticket_slot();
+      if (!p.ticket) return fail(FTN_ERR_CUDA, "jacobi3d_wr: ticket slots");
+    } else {
+      p.rr_band = large ? band : 0;
+      if (p.rr_band > 0) grid = g2;
+    }
   }
   p.G = grid;
 #if FTN_W3_TRACE

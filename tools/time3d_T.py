@@ -1,4 +1,6 @@
 """Time the 3-D Jacobi (jacobi3d_wr<T>) at several fusion factors: GLUPS of `sweeps` sweeps.
+The rank-3 fusion is capped at FTN_J3_T (default 3): set FTN_J3_T=4 to time T = 4; the line
+prints the T actually used.
 
     python tools/time3d_T.py [--sweeps S] [--reps K] n [n ...]
 """
@@ -38,9 +40,10 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             ms = min(ts)
-            nl = len(ftn.jacobi_plan(a.sweeps, T))
+            Ta = ftn.jacobi_fusion(U)          # the sweeps per launch actually used (rank 3: <= FTN_J3_T)
+            nl = len(ftn.jacobi_plan(a.sweeps, Ta))
             gl = (n - 2) ** 3 * a.sweeps / ms / 1e6
-            print(f"n={n} T={T} launches={nl} {ms:.2f} ms {gl:.1f} GLUPS per-launch HBM "
+            print(f"n={n} T={Ta} launches={nl} {ms:.2f} ms {gl:.1f} GLUPS per-launch HBM "
                   f"{16 * (n - 2) ** 3 * nl / ms / 1e6:.0f} GB/s", flush=True)
         ftn.jacobi_set_fusion(0)
         del U, W
