@@ -400,7 +400,7 @@ ftn_status_t ftn_dot_product_global(ftn_comm_t comm, const ftn_desc_t* x_local,
  * and on the first (last) rank local plane halo-1 (n_last-halo) is the global boundary
  * plane.  Per step the k owned planes next to each neighbour are exchanged with
  * ncclSend/ncclRecv (k = 1, or k = T sweeps fused per step for TMA-able slabs,
- * T = min(halo, ftn_jacobi_get_fusion()) for rank 2 and min(halo, 2, fusion) for rank 3)
+ * T = min(halo, ftn_jacobi_fusion_for(u_local)): for rank 3 at most FTN_J3_T, default 3)
  * and ftn_jacobi_slab advances the owned planes by k sweeps.  Results are bit-identical to ftn_jacobi on the undivided array;
  * *result_in_unew as for ftn_jacobi. */
 ftn_status_t ftn_jacobi_dist(ftn_comm_t comm, const ftn_desc_t* u_local, const ftn_desc_t* unew_local,
@@ -425,7 +425,7 @@ ftn_status_t ftn_jacobi_solve_dist(ftn_comm_t comm, const ftn_desc_t* u_local, c
  * slab laid out as for ftn_jacobi_dist whose halo planes are current, src -> dst.  Reads src
  * planes [halo - sweeps, n_last - halo + sweeps); writes only the owned interior of dst.
  * first / last: this slab holds the global lower / upper boundary plane.  sweeps > 1 needs
- * a TMA-able slab: rank 2 up to 6 sweeps, rank 3 exactly 2 (FTN_ERR_UNSUPPORTED otherwise). */
+ * a TMA-able slab: rank 2 up to 8 sweeps, rank 3 up to 4 (FTN_ERR_UNSUPPORTED otherwise). */
 ftn_status_t ftn_jacobi_slab(const ftn_desc_t* src, const ftn_desc_t* dst, int32_t sweeps, double coeff,
                              int32_t halo, int32_t first, int32_t last, ftn_stream_t stream);
 

@@ -168,9 +168,10 @@ def test_2d_temporal_blocking_long_strip(ftn):
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 4, 5])
 def test_3d_temporal_blocking(ftn, T, shape, sweeps):
     """Rank-3 launches of T fused sweeps (jacobi3d_wr<T>) are bit-identical to
-    the oracle's DO nest; boxes of 64 x 32 with (64 - 2H) x (32 - 2T) outputs (56 x 24 at
-    T = 4, 56 x 26 at T = 3, 60 x 28 at T = 2), so these shapes cover one tile, exact multiples
-    and ragged tails in i and j."""
+    the oracle's DO nest; boxes of 64 x 32 with (64 - 2H) x (32 - 2T) outputs (56 x 26 at
+    T = 3, 60 x 28 at T = 2), so these shapes cover one tile, exact multiples and ragged tails
+    in i and j.  ftn_jacobi caps rank-3 launches at FTN_J3_T (3), so T = 4 here runs T = 3;
+    wr<4> is covered by test_3d_slab_step_every_fusion."""
     ftn.jacobi_set_fusion(T)
     try:
         u0 = synth.jacobi_init(shape, array_id=sum(shape) + sweeps)
@@ -178,6 +179,32 @@ def test_3d_temporal_blocking(ftn, T, shape, sweeps):
         np.testing.assert_array_equal(got, ref)
     finally:
         ftn.jacobi_set_fusion(DEFAULT_FUSION)
+
+
+@pytest.mark.parametrize("sweeps", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(62, 31, 12), (122, 57, 20), (64, 64, 30), (200, 90, 13)])   # TMA-able: even n1
+def test_3d_slab_step_every_fusion(ftn, sweeps, shape):
+    """ftn_jacobi_slab on one whole-array slab runs exactly `sweeps` fused sweeps per launch
+    (jacobi3d_tb2 for 2, jacobi3d_wr<3>, jacobi3d_wr<4> -- ftn_jacobi caps rank-3 launches at
+    FTN_J3_T = 3, so this is the path that reaches wr<4>); the owned planes equal the oracle's
+    DO nest after `sweeps` sweeps, bit for bit."""
+    from paper_2409_18824_b200 import dist as D
+    halo = sweeps
+    n = shape[-1]
+    g0, nl = D.jacobi_slab(n, 1, 0, halo)
+    u0 = synth.jacobi_init(shape, array_id=sum(shape) + sweeps)
+    part = np.full(shape[:-1] + (nl,), 7.0e300, order="F")
+    for q in range(nl):
+        if 0 <= g0 + q < n:
+            part[..., q] = u0[..., g0 + q]
+    U, W = ftn.FArray.from_numpy(part), ftn.FArray.from_numpy(part)
+    ftn.jacobi_slab(U, W, sweeps, halo, True, True)
+    a, b = u0.copy(order="F"), u0.copy(order="F")
+    new = oracle.jacobi(OA(a), OA(b), sweeps, C3)
+    ref = b if new else a
+    owned = nl - 2 * halo
+    got = W.to_numpy()
+    np.testing.assert_array_equal(got[..., halo:halo + owned], ref[..., g0 + halo:g0 + halo + owned])
 
 
 def test_3d_temporal_blocking_many_units(ftn):
