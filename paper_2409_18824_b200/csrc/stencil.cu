@@ -493,6 +493,8 @@ int jacobi_fuse_T() {
 // jacobi3d_wr<3> (stencil3d_wr.cu), measured at 2048^3 x 100: T = 2 jacobi3d_tb2 539-570,
 // T = 3 631, T = 4 620 GLUPS.  Launches of 2 sweeps use jacobi3d_tb2 (faster
 // than jacobi3d_wr<2>: 539 vs 486), launches of 3 or 4 jacobi3d_wr.
+int jacobi2d_max_T();  // stencil_wq.cu
+
 int jacobi3d_T() {
   static const int t = [] {
     const char* e = getenv("FTN_J3_T");
@@ -510,7 +512,7 @@ int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
     const int64_t pts = u->dim[0].extent * u->dim[1].extent;
     T = pts <= (int64_t(1) << 21) ? 6 : pts <= (int64_t(1) << 23) ? 5 : 8;
   }
-  return u->rank == 2 ? T : (T < jacobi3d_T() ? T : jacobi3d_T());
+  return u->rank == 2 ? (T < jacobi2d_max_T() ? T : jacobi2d_max_T()) : (T < jacobi3d_T() ? T : jacobi3d_T());
 }
 
 // k >= 2 fused sweeps src -> dst

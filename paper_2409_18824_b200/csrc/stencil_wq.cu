@@ -448,4 +448,13 @@ ftn_status_t jacobi2d_wq_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int 
   return fail(FTN_ERR_UNSUPPORTED, "jacobi2d_wq: T must be 1..8 (1..12 in -DFTN_WQ_BIG_T builds)");
 }
 
+// The most sweeps one rank-2 launch of this build fuses (ftn_jacobi caps the fusion at it).
+int jacobi2d_max_T() {
+#ifdef FTN_WQ_BIG_T
+  return 12;
+#else
+  return 8;
+#endif
+}
+
 }  // namespace ftn

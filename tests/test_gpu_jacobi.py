@@ -396,3 +396,18 @@ def test_subnormal_values_are_not_flushed(ftn):
         got, ref = _run_both(ftn, u0, sweeps, coeff)
         np.testing.assert_array_equal(got, ref)
         assert np.count_nonzero((np.abs(got) < 2.0 ** -1022) & (got != 0)) > 0
+
+
+def test_fusion_above_the_build_limit_is_capped(ftn):
+    """ftn_jacobi_set_fusion accepts 1..12, the default build fuses at most 8 rank-2 sweeps per
+    launch: a setting of 10 runs launches of <= 8 (ftn_jacobi_fusion_for reports 8), results
+    bit-identical to the oracle."""
+    ftn.jacobi_set_fusion(10)
+    try:
+        U = ftn.FArray.empty((300, 200))
+        assert ftn.jacobi_fusion(U) == 8
+        u0 = synth.jacobi_init((300, 200), array_id=10)
+        got, ref = _run_both(ftn, u0, 23, C2, [1, 1])
+        np.testing.assert_array_equal(got, ref)
+    finally:
+        ftn.jacobi_set_fusion(DEFAULT_FUSION)
