@@ -532,6 +532,29 @@ def bench_rows(torch, ftn, args, ctx, hbm_peak):
         torch.cuda.empty_cache()
 
     # paper Table III shapes (1 GPU): transpose int32 32768^2, sum 32768^2, dot 2^27, matmul 4096^3
+    # f2: Jacobi to convergence on the headline grid -- 100 sweeps in blocks of 20, the residual
+    # MAXVAL(ABS(u_s - u_{s-1})) fused into each block's last launch and read back by the host
+    # (tol = 0: all 100 sweeps run, 5 checks), against the plain 100 sweeps of the headline
+    if "f2" in args.rows and N == 1:
+        n, sweeps, every = 8192, SWEEPS, 20
+        U, W = ftn.FArray.empty((n, n)), ftn.FArray.empty((n, n))
+        jacobi_faces(ftn, U, n, n)
+        ftn.assign(W, U)
+        out = {}
+
+        def solve_step():
+            out["r"] = ftn.jacobi_solve(U, W, sweeps, every, 0.0)
+        t = timed(torch, solve_step, max(2, steps // 2), 1, ctx["clocks"], dist)
+        ns = max(2, steps // 2)
+        done, resid, _ = out["r"]
+        gl = (n - 2) ** 2 * done * ns / t / 1e9
+        rows["f2_jacobi_solve_8192"] = {"value": gl, "unit": "GLUPS", "sweeps_per_call": done,
+                                        "check_every": every, "last_residual": resid,
+                                        "note": "residual fused into the last launch of each block; one host read "
+                                                "per block; compare the headline's plain sweeps"}
+        del U, W
+        torch.cuda.empty_cache()
+
     if "paper" in args.rows and N == 1:
         n = 32768
         a = ftn.FArray.empty((n, n), dtype=torch.int32)
@@ -885,14 +908,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ftn", choices=["ftn", "reference"])
-    ap.add_argument("--rows", default="c1,c4,c3,paper,c5,f4,shares", help="comma list of extra rows, or 'none'")
+    ap.add_argument("--rows", default="c1,c4,c3,f2,paper,c5,f4,shares", help="comma list of extra rows, or 'none'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU code path (NCCL communicator, ftn_jacobi_dist) even at N=1")
     # SURVEY §5 bench CLI
     ap.add_argument("--config", default=None,
                     help="which SURVEY §8 configs run beside the C2 headline: a comma list of C1, C3, C4, C5, P "
-                         "(the paper's shapes), F4, SHARES, or ALL / NONE (overrides --rows)")
+                         "(the paper's shapes), F2 (solve to convergence), F4, SHARES, or ALL / NONE (overrides --rows)")
     ap.add_argument("--seed", type=int, default=SEED, help="generator seed of every synthetic input (18824)")
     ap.add_argument("--sweeps", type=int, default=SWEEPS, help="sweeps per step of the C2 headline (100)")
     ap.add_argument("--mode", choices=["random", "closed", "intvalued"], default=MODE,
@@ -905,7 +928,8 @@ def main():
     if SWEEPS < 1:
         ap.error("--sweeps must be >= 1")
     if args.config is not None:
-        groups = {"C1": "c1", "C3": "c3", "C4": "c4", "C5": "c5", "P": "paper", "F4": "f4", "SHARES": "shares"}
+        groups = {"C1": "c1", "C3": "c3", "C4": "c4", "C5": "c5", "P": "paper", "F2": "f2", "F4": "f4",
+                  "SHARES": "shares"}
         sel = [c.strip().upper() for c in args.config.split(",") if c.strip()]
         if sel in (["ALL"],):
             args.rows = ",".join(groups.values())
@@ -914,7 +938,7 @@ def main():
         else:
             bad = [c for c in sel if c not in groups and c != "C2"]
             if bad:
-                ap.error(f"--config: unknown {bad}; choose from C1..C5, P, F4, SHARES, ALL, NONE")
+                ap.error(f"--config: unknown {bad}; choose from C1..C5, P, F2, F4, SHARES, ALL, NONE")
             args.rows = ",".join(groups[c] for c in sel if c in groups) or "none"
     args.rows = [] if args.rows == "none" else args.rows.split(",")
     if args.impl == "reference":

@@ -263,7 +263,7 @@ ftn_status_t ftn_jacobi_ws(const ftn_desc_t* u, const ftn_desc_t* unew, int64_t 
  * bit-identical for every T; the array that does not hold the result holds an earlier
  * iterate.  T in 1..12 (1 = one sweep per launch; the kernels fuse up to 8 and a larger T
  * runs launches of 8, except in -DFTN_WQ_BIG_T tuning builds); default 8 or the FTN_JACOBI_FUSE environment variable; unless T is set
- * explicitly, rank-2 grids of <= 2^23 points use 5 and of <= 2^21 points 6 (measured best;
+ * explicitly, rank-2 grids of <= 2^22 points use 6 and of < 2^24 points 7 (measured best;
  * small launches are latency bound).  ftn_jacobi_get_fusion returns
  * the process-wide T (8 by default).  ftn_jacobi_set_fusion(0) restores the default.
  * Process-wide. */

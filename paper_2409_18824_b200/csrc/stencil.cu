@@ -510,7 +510,8 @@ int jacobi_fuse_for(const ftn_desc_t* u, const ftn_desc_t* unew) {
     if (u->dim[d].extent < 3) return 1;
   if (u->rank == 2 && !g_fuse_explicit.load()) {
     const int64_t pts = u->dim[0].extent * u->dim[1].extent;
-    T = pts <= (int64_t(1) << 21) ? 6 : pts <= (int64_t(1) << 23) ? 5 : 8;
+    // measured best: 1024^2 6 (wf), 1536^2 / 2048^2 6 (wq), 3072^2 7, 4096^2+ 8
+    T = pts <= (int64_t(1) << 22) ? 6 : pts < (int64_t(1) << 24) ? 7 : 8;
   }
   return u->rank == 2 ? (T < jacobi2d_max_T() ? T : jacobi2d_max_T()) : (T < jacobi3d_T() ? T : jacobi3d_T());
 }

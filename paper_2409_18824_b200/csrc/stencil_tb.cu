@@ -400,9 +400,14 @@ ftn_status_t jacobi2d_wq_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int 
 ftn_status_t jacobi2d_fused_rows(const ftn_desc_t* src, const ftn_desc_t* dst, int T, double coeff, int64_t row_lo,
                                  int64_t row_hi, int64_t fix_lo, int64_t fix_hi, cudaStream_t s, double* res) {
   if (res) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, res, s);
-  // jacobi2d_wq (stencil_wq.cu) for T = 7, 8, or for every T with FTN_WF_WQ=1: at T = 5 it
-  // measured 1215 vs 1602 GLUPS for jacobi2d_wf<5>, so wf is the default
-  static const bool wq = getenv("FTN_WF_WQ") && atoi(getenv("FTN_WF_WQ")) != 0;
+  // jacobi2d_wq (stencil_wq.cu) for T = 7, 8, for T = 4..6 on launches of more than 2^21
+  // points, or for every T with FTN_WF_WQ=1 (=0: wf whenever T <= 6).  GLUPS over 100 sweeps
+  // (wf / wq, both 2 CTAs per SM for wq at T = 4..6): 8192^2 T=4 1218 / 1395, T=5 1600 / 1771,
+  // T=6 1469 / 1916; 2048^2 T=5 905 / 990, T=6 892 / 1027; 1536^2 T=6 670 / 723; but 1024^2
+  // T=6 463 / 360 and T <= 3 at every size favour wf
+  static const int wq_env = getenv("FTN_WF_WQ") ? atoi(getenv("FTN_WF_WQ")) : -1;
+  const int64_t pts = src->dim[0].extent * (row_hi - row_lo + 1);
+  const bool wq = wq_env > 0 || (wq_env < 0 && T >= 4 && pts > (int64_t(1) << 21));
   if (wq || T > 6) return jacobi2d_wq_rows(src, dst, T, coeff, row_lo, row_hi, fix_lo, fix_hi, nullptr, s);
   // FTN_WF_CFG selects a tuning variant for every T that has one; other T use the default
   static const int cfg = getenv("FTN_WF_CFG") ? atoi(getenv("FTN_WF_CFG")) : -1;
