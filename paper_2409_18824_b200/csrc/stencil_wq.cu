@@ -43,8 +43,8 @@
 #ifndef FTN_WQ_UNROLL
 #define FTN_WQ_UNROLL 2
 #endif
-#ifndef FTN_WQ_MINB_LO   // T <= 3
-#define FTN_WQ_MINB_LO 4
+#ifndef FTN_WQ_MINB_LO   // T <= 3 (the fused-residual launches): 2 CTAs per SM (8192^2 T=3 963 vs 860 GLUPS with 4)
+#define FTN_WQ_MINB_LO 2
 #endif
 #ifndef FTN_WQ_MINB_MID  // T = 4..6: 2 CTAs per SM (8192^2 T=6: 3.50 vs 4.77 ms per 100 sweeps with 3)
 #define FTN_WQ_MINB_MID 2
