@@ -539,7 +539,10 @@ ftn_status_t launch_wr(const ftn_desc_t* src, const ftn_desc_t* dst, double coef
     while (g2 > 1 && std::gcd(g2, (int64_t)p.tiles_i) != 1) --g2;
     const int64_t cells = band > 0 ? TI * TJ * ((nk + band - 1) / band) : 0;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cap);
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {  // e.g. the legacy stream during a global capture
+      cudaGetLastError();
+      cap = cudaStreamCaptureStatusActive;
+    }
     const bool large = band > 0 && (rr_env > 0 || cells >= 40 * g2);
     if (large && dyn_env && cap == cudaStreamCaptureStatusNone) {
       // dynamic cells: CTAs take (tile, band) cells from a ticket counter in launch order
