@@ -1,5 +1,7 @@
 """GPU parity: Jacobi sweeps (TMA 2-D / 3-D kernels and the generic strided kernel) vs the
 oracle, bit-exact (R#16, R#23)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -411,3 +413,54 @@ def test_fusion_above_the_build_limit_is_capped(ftn):
         np.testing.assert_array_equal(got, ref)
     finally:
         ftn.jacobi_set_fusion(DEFAULT_FUSION)
+
+
+def test_3d_banded_cells_dynamic_and_captured(tmp_path):
+    """The (tile, band) cell orders of jacobi3d_wr forced on a small grid
+    (FTN_W3_RR=16 in a fresh process): dynamic cells from the ticket counter in a plain call,
+    the static round-robin deal inside a CUDA-graph capture (replayed twice); both bit-identical
+    to the oracle's DO nest."""
+    import subprocess
+    import sys
+    import textwrap
+    script = textwrap.dedent("""
+        import sys
+        import numpy as np
+        import torch
+        sys.path.insert(0, %r)
+        import oracle, synth
+        from oracle import FArray as OA
+        from paper_2409_18824_b200 import ftn
+        C3 = 1.0 / 6.0
+        shape, sweeps = (130, 90, 70), 6
+        u0 = synth.jacobi_init(shape, array_id=77)
+        a, b = u0.copy(order="F"), u0.copy(order="F")
+        new = oracle.jacobi(OA(a), OA(b), sweeps, C3)
+        ref = b if new else a
+        U, W = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+        got_new = ftn.jacobi(U, W, sweeps, C3)
+        assert got_new == new
+        np.testing.assert_array_equal((W if new else U).to_numpy(), ref)
+        U, W, U0 = ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0), ftn.FArray.from_numpy(u0)
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            ftn.jacobi(U, W, 1, C3, stream=s)     # warm-up (attributes, tensor maps) outside the capture
+            s.synchronize()
+            ftn.assign(U, U0, stream=s)
+            ftn.assign(W, U0, stream=s)
+            s.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                ftn.jacobi(U, W, sweeps, C3, stream=s)
+        for rep in range(2):   # replay twice from the initial state
+            ftn.assign(U, U0)
+            ftn.assign(W, U0)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal((W if new else U).to_numpy(), ref)
+        print("ok")
+    """) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FTN_W3_RR="16")
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
